@@ -1,0 +1,242 @@
+"""Generate golden fixtures by running the REFERENCE implementation.
+
+Run in the build container only (it imports /root/reference, which does not
+exist on the GPU box):
+
+    python tests/golden/make_golden.py
+
+Outputs ``tests/golden/*.npz``.  Each fixture stores the inputs (or the seeded
+recipe that rebuilds them) and the reference's own outputs: permutation,
+swap log, R, Y, tau, W, trailing block, rank, counters and resample count.
+Large outputs are stored as a sha256 of their bytes plus a few slices, so the
+directory stays small.  The oracle (``oracle/port.py``) and the GPU path are
+both checked against these files.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import os
+import sys
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def _gaussian(seed, m, n):
+    return np.random.default_rng(seed).standard_normal((m, n))
+
+
+def _lowrank(seed, m, n, r):
+    g = np.random.default_rng(seed)
+    return g.standard_normal((m, r)) @ g.standard_normal((r, n))
+
+
+def _geometric(seed, n, decades):
+    g = np.random.default_rng(seed)
+    U = np.linalg.qr(g.standard_normal((n, n)))[0]
+    V = np.linalg.qr(g.standard_normal((n, n)))[0]
+    s = 10.0 ** (-decades * np.arange(n) / (n - 1))
+    return np.asfortranarray((U * s) @ V.T)
+
+
+def _decay(seed, m, n, base=0.9):
+    g = np.random.default_rng(seed)
+    q1, _ = np.linalg.qr(g.standard_normal((m, m)))
+    q2, _ = np.linalg.qr(g.standard_normal((n, n)))
+    r = min(m, n)
+    return q1[:, :r] * (base ** np.arange(r)) @ q2[:r]
+
+
+# (name, driver, A-builder, k, block, padding, seed, store_full)
+CASES = [
+    ("rq_gauss_60x45_k20", "rqrcp", lambda: _gaussian(0, 60, 45), 20, 8, 4, 0, True),
+    ("rq_gauss_45x60_full", "rqrcp", lambda: _gaussian(1, 45, 60), None, 8, 4, 1, True),
+    ("rq_gauss_64x64_full", "rqrcp", lambda: _gaussian(2, 64, 64), None, 16, 8, 2, True),
+    ("rq_gauss_130x97_full", "rqrcp", lambda: _gaussian(3, 130, 97), None, 32, 8, 5, True),
+    ("rq_lowrank_50x40_r10", "rqrcp", lambda: _lowrank(5, 50, 40, 10), 20, 8, 4, 0, True),
+    ("rq_lowrank_80x70_r13", "rqrcp", lambda: _lowrank(6, 80, 70, 13), None, 8, 4, 3, True),
+    ("rq_zero_12x9", "rqrcp", lambda: np.zeros((12, 9)), None, 4, 2, 0, True),
+    ("rq_geom16_128_b8", "rqrcp", lambda: _geometric(0, 128, 16.0), None, 8, 8, 0, True),
+    ("rq_geom20_192_b16", "rqrcp", lambda: _geometric(0, 192, 20.0), None, 16, 8, 0, True),
+    ("rq_geom12_512_b32", "rqrcp", "geom:1:512:12", None, 32, 8, 0, False),
+    ("rq_dup_cols_40x30", "rqrcp",
+     lambda: np.repeat(_gaussian(7, 40, 10), 3, axis=1), None, 8, 4, 0, True),
+    ("rs_gauss_64x48_k32", "rsrqrcp", lambda: _gaussian(6, 64, 48), 32, 8, 4, 5, True),
+    ("rs_lowrank_50x40_r10", "rsrqrcp", lambda: _lowrank(5, 50, 40, 10), 20, 8, 4, 0, True),
+    ("rs_geom16_128_b8", "rsrqrcp", lambda: _geometric(0, 128, 16.0), None, 8, 8, 0, True),
+    ("ss_gauss_48x36_k12", "ssrqrcp", lambda: _gaussian(9, 48, 36), 12, 12, 8, 7, True),
+    ("ss_lowrank_40x30_r8", "ssrqrcp", lambda: _lowrank(3, 40, 30, 8), 8, 32, 8, 1, True),
+    ("tr_gauss_64x48_k16", "trqrcp", lambda: _gaussian(42, 64, 48), 16, 8, 4, 3, True),
+    ("tr_gauss_48x64_k24", "trqrcp", lambda: _gaussian(42, 48, 64), 24, 8, 4, 3, True),
+    ("tr_gauss_50x50_k32", "trqrcp", lambda: _gaussian(42, 50, 50), 32, 8, 4, 3, True),
+    ("tr_lowrank_60x50_r10", "trqrcp", lambda: _lowrank(9, 60, 50, 10), 24, 8, 4, 0, True),
+    ("tr_geom16_128_full", "trqrcp", lambda: _geometric(0, 128, 16.0), 128, 8, 8, 0, True),
+    ("tr_geom20_192_full", "trqrcp", lambda: _geometric(0, 192, 20.0), 192, 16, 8, 0, True),
+    ("tr_geom12_512_k256", "trqrcp", "geom:1:512:12", 256, 32, 8, 0, False),
+    ("tx_diag_531", "tuxv", lambda: np.diag([5.0, 3.0, 1.0]), 2, 2, 1, 0, True),
+    ("tx_lowrank_45x35_r9", "tuxv", lambda: _lowrank(11, 45, 35, 9), 9, 4, 4, 1, True),
+    ("tx_decay_72x56_k16", "tuxv", lambda: _decay(6, 72, 56), 16, 8, 8, 3, True),
+    ("tx_gauss_200x150_k40", "tuxv", lambda: _gaussian(13, 200, 150), 40, 8, 4, 2, True),
+]
+
+# config 1 of BASELINE.json: full RQRCP of a seeded 1000x1000 Gaussian
+CFG1 = ("cfg1_rq_gauss_1000", "rqrcp", "gauss:0:1000:1000", None, 32, 8, 0, False)
+
+
+def build_recipe(recipe):
+    """Seeded recipes for the inputs that are not stored in the fixture.
+    ``gauss`` is bit-portable (PCG64 + ziggurat); ``geom`` goes through
+    LAPACK QR and is only bit-stable on the CPU that generated it."""
+    kind, *args = recipe.split(":")
+    if kind == "gauss":
+        seed, m, n = map(int, args)
+        return _gaussian(seed, m, n)
+    if kind == "geom":
+        seed, n, dec = int(args[0]), int(args[1]), float(args[2])
+        return _geometric(seed, n, dec)
+    raise ValueError(recipe)
+
+
+def _run_reference(rq, driver, A, k, block, padding, seed):
+    cfg = rq.RandomizedConfig(block=block, padding=padding, seed=seed)
+    if driver == "rqrcp":
+        return rq.rqrcp(A, k=k, config=cfg)
+    if driver == "rsrqrcp":
+        return rq.rsrqrcp(A, k=k, config=cfg)
+    if driver == "ssrqrcp":
+        return rq.ssrqrcp(A, k=k, config=cfg)
+    if driver == "trqrcp":
+        return rq.trqrcp(A, k=k, config=cfg)
+    if driver == "tuxv":
+        return rq.tuxv(A, k=k, config=cfg)
+    raise ValueError(driver)
+
+
+def _store(name, driver, A, k, block, padding, seed, full, f, recipe=""):
+    rec = dict(driver=driver, k=-1 if k is None else k, block=block, padding=padding,
+               seed=seed, m=A.shape[0], n=A.shape[1], full=full)
+    c = f.counters
+    rec.update(gemm_flops=c.gemm_flops, level2_flops=c.level2_flops,
+               bytes_touched=c.bytes_touched, resamples=c.resamples, rank=f.rank)
+    if driver == "tuxv":
+        outs = dict(U=f.U, V=f.V, X=f.X, sv=f.singular_values())
+    else:
+        outs = dict(perm=np.asarray(f.perm.forward, dtype=np.int64),
+                    swaps=np.asarray(f.perm.swaps, dtype=np.int64).reshape(-1, 2),
+                    R=f.R, Y=f.reflectors.Y, tau=f.reflectors.tau)
+        if getattr(f, "trailing", None) is not None:
+            outs["trailing"] = f.trailing
+        if f.reflectors.W is not None:
+            outs["W"] = f.reflectors.W
+    if full:
+        rec["A"] = np.asarray(A)
+        rec.update(outs)
+    else:
+        rec["recipe"] = recipe
+        for key, val in outs.items():
+            rec[f"sha_{key}"] = _sha(val)
+        for key in ("perm", "tau", "swaps"):
+            if key in outs:
+                rec[key] = outs[key]
+        rec["R_diag"] = np.diag(outs["R"]).copy()
+        rec["R_head"] = outs["R"][:8].copy()
+    np.savez_compressed(os.path.join(OUT, name + ".npz"), **rec)
+
+
+def main():
+    sys.path.insert(0, REF)
+    import rqrcp as rq  # the reference package
+
+    # Ω stream known answers (rng.py:36-41), used to pin host RNG replays
+    st = rq.RngState(0)
+    om40 = rq.gaussian_matrix(st, 40, 8)
+    st2 = rq.RngState(0, position=40 * 8)
+    tail = rq.gaussian_matrix(st2, 40, 3)
+    st3 = rq.RngState(0)
+    om72 = rq.gaussian_matrix(st3, 72, 2)
+    np.savez_compressed(os.path.join(OUT, "kat_rng.npz"), om40=om40, tail=tail, om72=om72)
+
+    # reflector KATs (test_kernels.py:71-98 style inputs)
+    xs = [np.array([3.0, 4.0]), np.array([2.0, 0.0, 0.0]), np.zeros(3),
+          np.array([-1.0, 2.0, -2.0]), np.array([0.0, 1.0]), np.array([7.0])]
+    refl = []
+    for x in xs:
+        r = rq.form_reflector(x)
+        refl.append(np.concatenate([[r.tau, r.beta], r.v]))
+    np.savez_compressed(os.path.join(OUT, "kat_reflector.npz"),
+                        **{f"x{i}": x for i, x in enumerate(xs)},
+                        **{f"r{i}": r for i, r in enumerate(refl)})
+
+    # select_pivots on fixed samples: diag KAT plus random samples
+    samples = {}
+    b = np.zeros((4, 6))
+    np.fill_diagonal(b, [2.0, 5.0, 1.0, 4.0])
+    samples["diag"] = (b, 4)
+    for s in range(6):
+        g = np.random.default_rng(100 + s)
+        ell = int(g.integers(6, 20))
+        nt = int(g.integers(ell, 60))
+        samples[f"rand{s}"] = (g.standard_normal((ell, nt)) * g.uniform(0.1, 3.0, nt), ell - 3)
+    g = np.random.default_rng(7)
+    big = g.standard_normal((72, 700)) * np.exp(g.uniform(-3, 3, 700))
+    samples["wide72"] = (big, 64)
+    # duplicated columns force exact norm ties (first max by position)
+    dup = np.repeat(np.random.default_rng(8).standard_normal((10, 5)), 4, axis=1)
+    samples["ties"] = (dup, 6)
+    # norm-recompute guard: columns that lie almost in the span of others
+    base = np.random.default_rng(9).standard_normal((16, 6))
+    near = base @ np.random.default_rng(10).standard_normal((6, 20))
+    near += 1e-9 * np.random.default_rng(11).standard_normal(near.shape)
+    samples["guard"] = (np.hstack([base, near]), 12)
+    rec = {}
+    for key, (B, want) in samples.items():
+        smp = rq.SampleState(B=np.asfortranarray(B.copy()), ell=B.shape[0],
+                             frob_a=float(np.linalg.norm(B)))
+        ctr = rq.OpCounters()
+        perm, got = rq.select_pivots(smp, want, ctr)
+        rec[f"{key}_B"] = B
+        rec[f"{key}_want"] = want
+        rec[f"{key}_got"] = got
+        rec[f"{key}_perm"] = np.asarray(perm.forward, dtype=np.int64)
+        rec[f"{key}_swaps"] = np.asarray(perm.swaps, dtype=np.int64).reshape(-1, 2)
+        rec[f"{key}_S"] = smp.B.copy()
+        rec[f"{key}_Ys"] = smp.reflectors.Y
+        rec[f"{key}_taus"] = smp.reflectors.tau
+        rec[f"{key}_l2"] = ctr.level2_flops
+    np.savez_compressed(os.path.join(OUT, "kat_select.npz"), **rec)
+
+    # panel + T matrix KATs
+    rec = {}
+    for s, (mm, bw) in enumerate([(40, 8), (300, 32), (33, 33), (70, 5)]):
+        P = np.random.default_rng(200 + s).standard_normal((mm, bw))
+        if s == 3:
+            P[:, 2] = 0.0  # a zero column: identity reflector
+        Pc = np.asfortranarray(P.copy())
+        ctr = rq.OpCounters()
+        Yp, tp = rq.qrcp.panel_householder(Pc, ctr)
+        rec[f"p{s}_P"] = P
+        rec[f"p{s}_R"] = Pc
+        rec[f"p{s}_Y"] = Yp
+        rec[f"p{s}_tau"] = tp
+        rec[f"p{s}_T"] = rq.build_t_matrix(Yp, tp)
+        rec[f"p{s}_l2"] = ctr.level2_flops
+    np.savez_compressed(os.path.join(OUT, "kat_panel.npz"), **rec)
+
+    for name, driver, build, k, block, padding, seed, full in CASES + [CFG1]:
+        recipe = build if isinstance(build, str) else ""
+        A = build_recipe(build) if recipe else build()
+        f = _run_reference(rq, driver, A, k, block, padding, seed)
+        _store(name, driver, A, k, block, padding, seed, full, f, recipe)
+        extra = "" if driver == "tuxv" else f" resamples={f.counters.resamples}"
+        print(f"{name}: rank={f.rank}{extra}")
+
+
+if __name__ == "__main__":
+    main()
