@@ -1,0 +1,52 @@
+"""B200-native (sm_100a) blocked Randomized QR with Column Pivoting.
+
+Drop-in for the hot path of the reference package ``rqrcp`` (arXiv
+1509.06820): ``rqrcp``, ``rsrqrcp``, ``ssrqrcp``, ``trqrcp``, ``tuxv``,
+``lq_factor``, ``RandomizedConfig`` and the result types keep the reference
+signatures (plus an optional explicit ``omega``).  All arithmetic runs in
+librqrcp_b200.so (FP64 DMMA tensor-core GEMMs, cooperative pivot-selection
+and panel kernels, a native block-loop driver); PyTorch only allocates
+device memory and provides streams.  There is no CPU fallback.
+"""
+
+from .factorization import (
+    BlockReflectors,
+    Factorization,
+    OpCounters,
+    Permutation,
+    TruncatedFactorization,
+    TuxvFactorization,
+    q_columns,
+    t_factor,
+)
+from .randomized import DegenerateSampleError, RandomizedConfig, rqrcp, rsrqrcp, ssrqrcp
+from .rng import RngState, gaussian_matrix
+from .truncated import lq_factor, qr_blocked_device, trqrcp, tuxv
+
+build_t_matrix = t_factor
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "BlockReflectors",
+    "DegenerateSampleError",
+    "Factorization",
+    "OpCounters",
+    "Permutation",
+    "RandomizedConfig",
+    "RngState",
+    "TruncatedFactorization",
+    "TuxvFactorization",
+    "build_t_matrix",
+    "gaussian_matrix",
+    "lq_factor",
+    "q_columns",
+    "qr_blocked_device",
+    "rqrcp",
+    "rsrqrcp",
+    "ssrqrcp",
+    "t_factor",
+    "trqrcp",
+    "tuxv",
+    "__version__",
+]

@@ -1,0 +1,248 @@
+// extern "C" boundary (include/rqrcp_b200.h): argument checks, exception ->
+// status-code mapping, and the thin adapters onto the native drivers.
+#include <string>
+
+#include "../../include/rqrcp_b200.h"
+#include "driver.hpp"
+
+struct rq_handle_s {
+  rq::Handle* h;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    g_err.clear();
+    f();
+    return RQ_OK;
+  } catch (const rq::InvalidArg& e) {
+    g_err = e.what();
+    return RQ_ERR_INVALID;
+  } catch (const rq::CudaError& e) {
+    g_err = e.what();
+    return RQ_ERR_CUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return RQ_ERR_INTERNAL;
+  } catch (...) {
+    g_err = "unknown error";
+    return RQ_ERR_INTERNAL;
+  }
+}
+
+cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+void need(bool ok, const char* what) {
+  if (!ok) throw rq::InvalidArg(what);
+}
+
+rq::Handle& H(rq_handle_t h) {
+  need(h != nullptr && h->h != nullptr, "null handle");
+  return *h->h;
+}
+
+rq::FactorParams to_params(const rq_factor_args& a) {
+  need(a.m >= 1 && a.n >= 1, "matrix must be non-empty");
+  need(a.k >= 1 && a.k <= std::min(a.m, a.n), "rank must be >= 1 and <= min(m, n)");
+  need(a.ell >= 1 && a.ell <= a.m, "sample rows exceed matrix rows");
+  need(a.block >= 1, "block must be >= 1");
+  need(a.work && a.Y && a.tau && a.perm && a.swaps, "null output buffer");
+  need(a.ldw >= a.m && a.ldy >= a.m, "leading dimension too small");
+  rq::FactorParams p;
+  p.m = a.m; p.n = a.n; p.k = a.k; p.block = a.block; p.ell = a.ell;
+  p.resketch_each_block = a.variant == RQ_RSRQRCP;
+  p.update_trailing = a.variant == RQ_RQRCP || a.variant == RQ_RSRQRCP;
+  p.truncated = a.variant == RQ_TRQRCP;
+  if (p.truncated) {
+    need(a.W && a.R, "TRQRCP needs W and R buffers");
+    need(a.ldW >= a.n && a.ldR >= a.k, "leading dimension too small");
+  }
+  p.work = a.work; p.ldw = a.ldw; p.Y = a.Y; p.ldy = a.ldy; p.tau = a.tau;
+  p.W = a.W; p.ldW = a.ldW; p.R = a.R; p.ldR = a.ldR;
+  p.perm = a.perm; p.swaps = a.swaps; p.swap_cap = a.swap_cap;
+  p.omega0 = a.omega0; p.omega_fn = a.omega_fn; p.omega_user = a.omega_user;
+  p.speculate = a.speculate;
+  p.stream = S(a.stream);
+  return p;
+}
+
+void fill_result(const rq::FactorResult& r, rq_factor_result* out) {
+  out->rank = r.rank;
+  out->nswaps = r.nswaps;
+  out->gemm_flops = r.c.gemm_flops;
+  out->level2_flops = r.c.level2_flops;
+  out->bytes_touched = r.c.bytes_touched;
+  out->resamples = r.c.resamples;
+  out->frob = r.frob;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rq_version(void) { return 100; }
+
+const char* rq_last_error(void) { return g_err.c_str(); }
+
+int rq_create(int device, rq_handle_t* out) {
+  return guarded([&] {
+    need(out != nullptr, "null output");
+    auto* h = new rq_handle_s;
+    try {
+      h->h = new rq::Handle(device);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int rq_destroy(rq_handle_t h) {
+  return guarded([&] {
+    if (!h) return;
+    delete h->h;
+    delete h;
+  });
+}
+
+int rq_factor(rq_handle_t h, const rq_factor_args* args, rq_factor_result* out) {
+  return guarded([&] {
+    need(args && out, "null argument");
+    rq::FactorParams p = to_params(*args);
+    rq::FactorResult r = rq::run_factor(H(h), p);
+    fill_result(r, out);
+  });
+}
+
+int rq_tuxv(rq_handle_t h, const rq_tuxv_args* args, rq_tuxv_result* out) {
+  return guarded([&] {
+    need(args && out, "null argument");
+    need(args->f.variant == RQ_TRQRCP, "tuxv runs on TRQRCP");
+    need(args->j_max >= 1, "j_max must be >= 1");
+    need(args->A && args->U && args->V && args->X, "null output buffer");
+    rq::TuxvParams p;
+    p.f = to_params(args->f);
+    p.A = args->A; p.lda = args->lda; p.j_max = args->j_max;
+    p.U = args->U; p.ldu = args->ldu; p.V = args->V; p.ldv = args->ldv;
+    p.X = args->X; p.ldx = args->ldx;
+    rq::TuxvResult r = rq::run_tuxv(H(h), p);
+    fill_result(r.f, &out->f);
+    out->rank = r.rank;
+    out->x_lower = r.x_lower;
+  });
+}
+
+int rq_gemm(rq_handle_t h, int transa, int transb, int64_t m, int64_t n, int64_t k,
+            double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
+            double beta, double* C, int64_t ldc, void* stream) {
+  return guarded([&] {
+    need(m >= 0 && n >= 0 && k >= 0, "negative dimension");
+    need(ldc >= std::max<int64_t>(1, m), "ldc too small");
+    rq::gemm(H(h), transa != 0, transb != 0, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc,
+             S(stream));
+  });
+}
+
+int rq_sketch(rq_handle_t h, int64_t ell, int64_t m, int64_t n, const double* omega,
+              int64_t ldo, const double* A, int64_t lda, double* B, int64_t ldb, void* stream) {
+  return guarded([&] {
+    need(ell >= 1, "sample must have at least one row");
+    rq::gemm(H(h), false, false, ell, n, m, 1.0, omega, ldo, A, lda, 0.0, B, ldb, S(stream));
+  });
+}
+
+int rq_select_pivots(rq_handle_t h, int64_t ell, int64_t nt, int64_t want, const double* B,
+                     int64_t ldb, double* S_, int64_t lds, int64_t* piv, double* Ys,
+                     int64_t ldys, double* taus, int64_t* got, int64_t* level2,
+                     void* stream) {
+  return guarded([&] {
+    rq::Handle& hh = H(h);
+    cudaStream_t s = S(stream);
+    auto* st = (rq::Status*)hh.buf("abi_st", sizeof(rq::Status), s);
+    RQ_CUDA(cudaMemsetAsync(st, 0, sizeof(rq::Status), s));
+    rq::SelectOut o{S_, lds, piv, Ys, ldys, taus};
+    rq::select_pivots(hh, ell, nt, want, B, ldb, o, st, false, 0, s);
+    rq::Status hs;
+    RQ_CUDA(cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, s));
+    RQ_CUDA(cudaStreamSynchronize(s));
+    if (got) *got = hs.got;
+    if (level2) *level2 = hs.level2;
+  });
+}
+
+int rq_panel_qr(rq_handle_t h, int64_t mm, int64_t bw, double* P, int64_t ldp, double* Y,
+                int64_t ldy, double* tau, double* T, int64_t ldt, double tol, int64_t* usable,
+                int64_t* level2, void* stream) {
+  return guarded([&] {
+    rq::Handle& hh = H(h);
+    cudaStream_t s = S(stream);
+    auto* st = (rq::Status*)hh.buf("abi_st", sizeof(rq::Status), s);
+    RQ_CUDA(cudaMemsetAsync(st, 0, sizeof(rq::Status), s));
+    rq::PanelOut o{P, ldp, mm, Y, ldy, tau, T, ldt};
+    rq::panel_qr(hh, mm, bw, P, ldp, o, tol, rq::kPanelCommitAll, false, st, 0, s);
+    rq::Status hs;
+    RQ_CUDA(cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, s));
+    RQ_CUDA(cudaStreamSynchronize(s));
+    if (usable) *usable = hs.usable;
+    if (level2) *level2 = hs.level2;
+  });
+}
+
+int rq_t_factor(rq_handle_t h, const double* Y, int64_t ldy, int64_t mm, int64_t nb,
+                const double* tau, double* T, int64_t ldt, void* stream) {
+  return guarded([&] { rq::t_factor(H(h), Y, ldy, mm, nb, tau, T, ldt, S(stream)); });
+}
+
+int rq_sample_update(rq_handle_t h, int64_t ell, int64_t b, int64_t n2, const double* S_,
+                     int64_t lds, const double* R11, const double* R12, int64_t ldr,
+                     double frob, double* Bnew, int64_t ldb, int32_t* degenerate,
+                     void* stream) {
+  return guarded([&] {
+    rq::Handle& hh = H(h);
+    cudaStream_t s = S(stream);
+    auto* st = (rq::Status*)hh.buf("abi_st", sizeof(rq::Status), s);
+    RQ_CUDA(cudaMemsetAsync(st, 0, sizeof(rq::Status), s));
+    rq::sample_update(hh, ell, b, n2, S_, lds, R11, R12, ldr, frob, Bnew, ldb, st, false, 0, s);
+    rq::Status hs;
+    RQ_CUDA(cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, s));
+    RQ_CUDA(cudaStreamSynchronize(s));
+    if (degenerate) *degenerate = (int32_t)hs.degenerate;
+  });
+}
+
+int rq_qr_blocked(rq_handle_t h, int64_t m, int64_t n, int64_t k, int64_t b, double* A,
+                  int64_t lda, double* Y, int64_t ldy, double* tau, int64_t* counters,
+                  void* stream) {
+  return guarded([&] {
+    need(k >= 0 && k <= std::min(m, n), "rank outside [0, min(m, n)]");
+    need(b >= 1, "block size must be >= 1");
+    rq::Counters c;
+    rq::qr_blocked(H(h), m, n, k, b, A, lda, Y, ldy, tau, &c, S(stream));
+    if (counters) {
+      counters[0] += c.gemm_flops;
+      counters[1] += c.level2_flops;
+      counters[2] += c.bytes_touched;
+    }
+  });
+}
+
+int rq_q_columns(rq_handle_t h, int64_t m, int64_t nref, int64_t cols, const double* Y,
+                 int64_t ldy, const double* tau, int64_t b, double* Q, int64_t ldq,
+                 void* stream) {
+  return guarded([&] {
+    need(b >= 1, "block size must be >= 1");
+    rq::q_columns(H(h), m, nref, cols, Y, ldy, tau, b, Q, ldq, S(stream));
+  });
+}
+
+int rq_frob_norm(rq_handle_t h, const double* A, int64_t m, int64_t n, int64_t lda,
+                 double* out, void* stream) {
+  return guarded([&] { rq::frob_norm(H(h), A, m, n, lda, out, S(stream)); });
+}
+
+}  // extern "C"

@@ -1,0 +1,111 @@
+// Shared device helpers for the sm_100a RQRCP kernels.
+//
+// Layout conventions: every matrix is FP64,
+// column-major with an explicit leading dimension; permutations and swap logs
+// are int64.  Kernels on the speculative block path take `abort`, a device
+// word that, once non-zero, turns every later kernel of the queue into a
+// no-op (see driver.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define RQ_DEV __device__ __forceinline__
+
+namespace rq {
+
+constexpr double kEps = 2.220446049250313e-16;         // np.finfo(float64).eps
+constexpr double kGuard = 1.4901161193847656e-08;      // sqrt(eps), kernels.py:205
+constexpr double kEps34 = 1.8189894035458565e-12;      // eps**0.75 = 2^-39, randomized.py:117
+
+// abort codes written by the speculative-path kernels (driver.cu)
+enum AbortCode : int {
+  kAbortNone = 0,
+  kAbortShortSample = 1,  // select: got < want   (randomized.py:217)
+  kAbortPanelRank = 2,    // panel: usable < got  (randomized.py:229)
+  kAbortDegenerate = 3,   // sample update: |R11_jj| < eps^3/4 ||A|| (randomized.py:117)
+};
+
+// Device-side run status shared by the kernels of one driver call.
+struct Status {
+  int abort;        // AbortCode of the first failing stage (0 = none)
+  int pad0;
+  int64_t abort_i0; // block start of the failing stage
+  int64_t got;      // last select_pivots result
+  int64_t usable;   // last panel rank
+  int64_t level2;   // level-2 flop counter (OpCounters.level2_flops)
+  int64_t l2bytes;  // bytes_touched contribution of the level-2 calls
+  int64_t nswaps;   // length of the global swap log
+  int64_t degenerate;  // last sample-update verdict (1 = degenerate)
+};
+
+RQ_DEV int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }
+RQ_DEV int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+RQ_DEV bool aborted(const Status* st) {
+  return st != nullptr && *((volatile const int*)&st->abort) != 0;
+}
+
+// Software grid barrier for cooperative launches (all CTAs co-resident).
+// `counter` must be zero at launch; `epoch` is a per-CTA register.
+RQ_DEV void grid_barrier(unsigned int* counter, unsigned int& epoch) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    epoch += 1;
+    const unsigned int target = epoch * gridDim.x;
+    __threadfence();
+    atomicAdd(counter, 1u);
+    unsigned int seen;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(counter) : "memory");
+    } while (seen < target);
+  }
+  __syncthreads();
+}
+
+// numpy's pairwise summation (pairwise_sum_DOUBLE: 8 accumulators for
+// n <= 128, recursive halving on multiples of 8 above) of x[i]*x[i] over a
+// strided vector; bit-identical to np.linalg.norm(B, axis=0)**2 on an
+// F-ordered sample (kernels.py:184-186, 207-209).
+RQ_DEV double pairwise_block_sumsq(const double* x, int n, int stride) {
+  double res;
+  if (n < 8) {
+    res = 0.0;
+    for (int i = 0; i < n; ++i) {
+      const double v = x[i * stride];
+      res = __dadd_rn(res, __dmul_rn(v, v));
+    }
+    return res;
+  }
+  double r[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const double v = x[t * stride];
+    r[t] = __dmul_rn(v, v);
+  }
+  int i = 8;
+  for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const double v = x[(i + t) * stride];
+      r[t] = __dadd_rn(r[t], __dmul_rn(v, v));
+    }
+  }
+  res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                  __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; ++i) {
+    const double v = x[i * stride];
+    res = __dadd_rn(res, __dmul_rn(v, v));
+  }
+  return res;
+}
+
+__device__ inline double pairwise_sumsq(const double* x, int n, int stride) {
+  if (n <= 128) return pairwise_block_sumsq(x, n, stride);
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  return __dadd_rn(pairwise_sumsq(x, n2, stride),
+                   pairwise_sumsq(x + (size_t)n2 * stride, n - n2, stride));
+}
+
+}  // namespace rq

@@ -1,0 +1,564 @@
+// Native block-loop drivers for RQRCP / RSRQRCP / SSRQRCP / TRQRCP and the
+// unpivoted pieces TUXV needs (qr_blocked, q_columns).
+//
+// Control flow follows randomized.py:183-266 (_randomized_factor) and
+// truncated.py:70-174 (trqrcp) exactly, including the three resample
+// triggers.  The GPU does not wait for the host between blocks: blocks are
+// enqueued speculatively (up to kLookahead ahead) under the assumption that no
+// trigger fires.  Each trigger is detected on the device by the kernel that
+// evaluates it (select: got < want; panel: usable < got; sample update:
+// degenerate R11), which records the stage and block in Status and sets
+// Status.abort -- every later kernel in the queue then returns immediately.
+// The host notices the flag when it retires the oldest speculative block,
+// rewinds to the failing block and replays the reference's branch
+// synchronously (resample from the host Omega stream, retry), then resumes
+// speculation.  Since a failing stage never commits anything the reference
+// would not have committed, the device state at the abort point equals the
+// reference's state at that branch.
+#include <cstring>
+#include <deque>
+#include <vector>
+
+#include "driver.hpp"
+
+namespace rq {
+
+namespace {
+
+constexpr int kLookahead = 3;
+
+struct Pending {
+  int64_t i0, bw;
+  Counters stage, update;
+  bool has_update;
+  int slot;
+};
+
+class Factor {
+ public:
+  Factor(Handle& h, const FactorParams& p) : h_(h), p_(p), s_(p.stream) {}
+
+  FactorResult run();
+
+ private:
+  Handle& h_;
+  const FactorParams& p_;
+  cudaStream_t s_;
+  Status* st_ = nullptr;   // device
+  Status* hst_ = nullptr;  // pinned
+  int* hring_ = nullptr;   // pinned abort snapshots
+  std::vector<cudaEvent_t> ev_;
+  double *B_ = nullptr, *S_ = nullptr, *T_ = nullptr, *G_ = nullptr, *X_ = nullptr;
+  double *om_d_ = nullptr, *om_h_ = nullptr, *P_ = nullptr, *Z_ = nullptr;
+  int64_t* piv_ = nullptr;
+  double frob_ = 0.0, tol_ = 0.0;
+  Counters c_;
+  int64_t m_ = 0, n_ = 0, k_ = 0, b_ = 0, ell_ = 0;
+
+  void sync() { RQ_CUDA(cudaStreamSynchronize(s_)); }
+  Status read_status() {
+    RQ_CUDA(cudaMemcpyAsync(hst_, st_, sizeof(Status), cudaMemcpyDeviceToHost, s_));
+    sync();
+    return *hst_;
+  }
+  void touch(Counters& c, int64_t elems) { c.bytes_touched += 8 * elems; }
+
+  void draw_omega(int64_t rows, int64_t cols);
+  void first_sample();
+  void fresh_sample(int64_t i0);
+  void select(int64_t i0, int64_t want, bool spec);
+  void swaps(int64_t i0, int64_t got);
+  void panel(int64_t i0, int64_t got, PanelPolicy pol, bool spec, Counters& c);
+  void stages(int64_t i0, int64_t bw, Counters& c);
+  void update(int64_t i0_new, int64_t bw, bool spec, Counters& c);
+  bool slow_block(int64_t& i0, bool resampled, int64_t& rank);
+};
+
+void Factor::draw_omega(int64_t rows, int64_t cols) {
+  if (p_.omega_fn == nullptr) throw InvalidArg("no Omega source for a (re)sample");
+  // the pinned staging buffer is reused: every caller has synchronised the
+  // stream, so no earlier H2D copy is still reading it
+  const int rc = p_.omega_fn(p_.omega_user, rows, cols, om_h_);
+  if (rc != 0) throw InvalidArg("Omega callback failed");
+  RQ_CUDA(cudaMemcpyAsync(om_d_, om_h_, (size_t)rows * cols * 8, cudaMemcpyHostToDevice, s_));
+}
+
+// make_sample(work, ell, rng) (randomized.py:69-82; truncated.py:97)
+void Factor::first_sample() {
+  const double* om = p_.omega0;
+  if (om == nullptr) {
+    draw_omega(ell_, m_);
+    om = om_d_;
+  }
+  gemm(h_, false, false, ell_, n_, m_, 1.0, om, ell_, p_.work, p_.ldw, 0.0, B_, ell_, s_);
+  c_.gemm_flops += 2 * ell_ * m_ * n_;
+  touch(c_, ell_ * m_ + m_ * n_ + ell_ * n_);
+}
+
+// fresh_sample(i0) (randomized.py:199-202) / _sketched_sample (truncated.py:53-67)
+void Factor::fresh_sample(int64_t i0) {
+  sync();
+  const int64_t mm = m_ - i0, nt = n_ - i0;
+  draw_omega(ell_, mm);
+  const double* At = p_.work + i0 + i0 * p_.ldw;
+  gemm(h_, false, false, ell_, nt, mm, 1.0, om_d_, ell_, At, p_.ldw, 0.0, B_, ell_, s_);
+  c_.gemm_flops += 2 * ell_ * mm * nt;
+  touch(c_, ell_ * mm + mm * nt + ell_ * nt);
+  if (p_.truncated && i0) {
+    // B -= (Omega Y[i0:, :i0]) W[i0:, :i0]^T
+    gemm(h_, false, false, ell_, i0, mm, 1.0, om_d_, ell_, p_.Y + i0, p_.ldy, 0.0, Z_, ell_, s_);
+    gemm(h_, false, true, ell_, nt, i0, -1.0, Z_, ell_, p_.W + i0, p_.ldW, 1.0, B_, ell_, s_);
+    c_.gemm_flops += 2 * ell_ * mm * i0 + 2 * ell_ * i0 * nt;
+    touch(c_, mm * i0 + nt * i0);
+  }
+}
+
+void Factor::select(int64_t i0, int64_t want, bool spec) {
+  SelectOut o{S_, ell_, piv_, nullptr, 0, nullptr};
+  select_pivots(h_, ell_, n_ - i0, want, B_, ell_, o, st_, spec, i0, s_);
+}
+
+void Factor::swaps(int64_t i0, int64_t got) {
+  SwapTargets t{};
+  t.work = p_.work; t.ldw = p_.ldw; t.m = m_;
+  t.perm = p_.perm; t.log = p_.swaps; t.log_cap = p_.swap_cap;
+  if (p_.truncated) {
+    t.Wf = p_.W; t.ldwf = p_.ldW; t.wf_cols = k_;
+    t.Rf = p_.R; t.ldrf = p_.ldR; t.rf_rows = k_;
+  }
+  apply_swaps(h_, piv_, got, i0, t, st_, s_);
+}
+
+void Factor::panel(int64_t i0, int64_t got, PanelPolicy pol, bool spec, Counters& c) {
+  const int64_t mm = m_ - i0;
+  PanelOut o{};
+  o.Y = p_.Y + i0 + i0 * p_.ldy; o.ldy = p_.ldy;
+  o.tau = p_.tau + i0;
+  o.T = T_; o.ldt = b_;
+  const double* src;
+  int64_t lds;
+  if (!p_.truncated) {
+    src = p_.work + i0 + i0 * p_.ldw; lds = p_.ldw;
+    o.Rdst = p_.work + i0 + i0 * p_.ldw; o.ldr = p_.ldw; o.rrows = mm;
+  } else {
+    // materialize the selected columns: A[i0:, sel] - Y[i0:, :i0] W[sel, :i0]^T (truncated.py:119-123)
+    copy2d(p_.work + i0 + i0 * p_.ldw, p_.ldw, P_, mm, mm, got, s_, st_);
+    if (i0) {
+      gemm(h_, false, true, mm, got, i0, -1.0, p_.Y + i0, p_.ldy, p_.W + i0, p_.ldW, 1.0, P_, mm,
+           s_, st_);
+      c.gemm_flops += 2 * mm * i0 * got;
+      touch(c, mm * got + mm * i0 + got * i0);
+    }
+    src = P_; lds = mm;
+    o.Rdst = p_.R + i0 + i0 * p_.ldR; o.ldr = p_.ldR; o.rrows = got;
+  }
+  panel_qr(h_, mm, got, src, lds, o, tol_, pol, spec, st_, i0, s_);
+}
+
+// _block_stages (randomized.py:158-180) / trqrcp W+R update (truncated.py:453-470)
+void Factor::stages(int64_t i0, int64_t bw, Counters& c) {
+  const int64_t mm = m_ - i0, nt2 = n_ - i0 - bw;
+  if (nt2 <= 0) return;
+  const double* Yb = p_.Y + i0 + i0 * p_.ldy;
+  if (!p_.truncated) {
+    double* C = p_.work + i0 + (i0 + bw) * p_.ldw;
+    gemm(h_, true, false, bw, nt2, mm, 1.0, Yb, p_.ldy, C, p_.ldw, 0.0, G_, bw, s_, st_);
+    gemm(h_, true, false, bw, nt2, bw, 1.0, T_, b_, G_, bw, 0.0, X_, bw, s_, st_);
+    c.gemm_flops += 2 * mm * bw * nt2 + bw * bw * nt2;
+    const bool trail = p_.update_trailing && i0 + bw < m_;
+    gemm(h_, false, false, trail ? mm : bw, nt2, bw, -1.0, Yb, p_.ldy, X_, bw, 1.0, C, p_.ldw, s_,
+         st_);
+    c.gemm_flops += 2 * bw * bw * nt2;
+    touch(c, mm * nt2 + mm * bw + bw * nt2);
+    if (trail) {
+      c.gemm_flops += 2 * (mm - bw) * bw * nt2;
+      touch(c, (mm - bw) * nt2);
+    }
+    return;
+  }
+  // G = Yb^T A[i0:, i0+bw:] - (Yb^T Y[i0:, :i0]) W[i0+bw:, :i0]^T
+  gemm(h_, true, false, bw, nt2, mm, 1.0, Yb, p_.ldy, p_.work + i0 + (i0 + bw) * p_.ldw, p_.ldw,
+       0.0, G_, bw, s_, st_);
+  c.gemm_flops += 2 * mm * bw * nt2;
+  if (i0) {
+    gemm(h_, true, false, bw, i0, mm, 1.0, Yb, p_.ldy, p_.Y + i0, p_.ldy, 0.0, Z_, bw, s_, st_);
+    gemm(h_, false, true, bw, nt2, i0, -1.0, Z_, bw, p_.W + i0 + bw, p_.ldW, 1.0, G_, bw, s_, st_);
+    c.gemm_flops += 2 * mm * bw * i0 + 2 * bw * i0 * nt2;
+  }
+  // W[i0+bw:, i0:i0+bw] = (T^T G)^T = G^T T
+  gemm(h_, true, false, nt2, bw, bw, 1.0, G_, bw, T_, b_, 0.0, p_.W + (i0 + bw) + i0 * p_.ldW,
+       p_.ldW, s_, st_);
+  c.gemm_flops += bw * bw * nt2;
+  // R[i0:i0+bw, i0+bw:] = A[i0:i0+bw, i0+bw:] - Y[i0:i0+bw, :i0+bw] W[i0+bw:, :i0+bw]^T
+  double* Rr = p_.R + i0 + (i0 + bw) * p_.ldR;
+  copy2d(p_.work + i0 + (i0 + bw) * p_.ldw, p_.ldw, Rr, p_.ldR, bw, nt2, s_, st_);
+  gemm(h_, false, true, bw, nt2, i0 + bw, -1.0, p_.Y + i0, p_.ldy, p_.W + i0 + bw, p_.ldW, 1.0,
+       Rr, p_.ldR, s_, st_);
+  c.gemm_flops += 2 * bw * (i0 + bw) * nt2;
+  touch(c, bw * n_ + nt2 * (i0 + bw));
+}
+
+// sample_update after a committed block ending at i0_new (randomized.py:253-255)
+void Factor::update(int64_t i0_new, int64_t bw, bool spec, Counters& c) {
+  const int64_t i0 = i0_new - bw, n2 = n_ - i0_new;
+  const double *R11, *R12;
+  int64_t ldr;
+  if (!p_.truncated) {
+    R11 = p_.work + i0 + i0 * p_.ldw; R12 = p_.work + i0 + i0_new * p_.ldw; ldr = p_.ldw;
+  } else {
+    R11 = p_.R + i0 + i0 * p_.ldR; R12 = p_.R + i0 + i0_new * p_.ldR; ldr = p_.ldR;
+  }
+  sample_update(h_, ell_, bw, n2, S_, ell_, R11, R12, ldr, frob_, B_, ell_, st_, spec, i0, s_);
+  c.gemm_flops += 3 * bw * bw * n2;
+  touch(c, 2 * bw * bw + 3 * bw * n2);
+}
+
+// One block of the reference loop with host-visible branch decisions
+// (randomized.py:208-258).  Returns false when the factorization stops.
+bool Factor::slow_block(int64_t& i0, bool resampled, int64_t& rank) {
+  const int64_t want = std::min(b_, k_ - i0);
+  int64_t bw = 0;
+  while (true) {
+    select(i0, want, false);
+    const int64_t got = read_status().got;
+    if (got < want && !resampled) {
+      fresh_sample(i0);
+      c_.resamples += 1;
+      resampled = true;
+      continue;
+    }
+    if (got == 0) { bw = 0; break; }
+    swaps(i0, got);
+    Counters pc;
+    panel(i0, got, resampled ? kPanelCommitUsable : kPanelCommitIfFull, false, pc);
+    c_.gemm_flops += pc.gemm_flops;
+    c_.bytes_touched += pc.bytes_touched;
+    const int64_t usable = read_status().usable;
+    if (usable < got && !resampled) {
+      fresh_sample(i0);
+      c_.resamples += 1;
+      resampled = true;
+      continue;
+    }
+    bw = usable;
+    break;
+  }
+  if (bw == 0) { rank = i0; return false; }
+  stages(i0, bw, c_);
+  i0 += bw;
+  if (bw < want) { rank = i0; return false; }
+  if (i0 < k_) {
+    if (p_.resketch_each_block) {
+      fresh_sample(i0);
+    } else {
+      Counters uc;
+      update(i0, bw, false, uc);
+      if (read_status().degenerate) {
+        fresh_sample(i0);
+        c_.resamples += 1;
+      } else {
+        c_.gemm_flops += uc.gemm_flops;
+        c_.bytes_touched += uc.bytes_touched;
+      }
+    }
+  }
+  return true;
+}
+
+FactorResult Factor::run() {
+  m_ = p_.m; n_ = p_.n; k_ = p_.k; b_ = p_.block; ell_ = p_.ell;
+  if (k_ < 1 || k_ > std::min(m_, n_)) throw InvalidArg("rank outside [1, min(m, n)]");
+  if (ell_ > m_) throw InvalidArg("sample rows exceed matrix rows");
+  if (b_ < 1 || b_ > 256) throw InvalidArg("block must be in [1, 256]");
+  st_ = (Status*)h_.buf("st", sizeof(Status), s_);
+  hst_ = (Status*)h_.host_pinned("hst", sizeof(Status), s_);
+  hring_ = (int*)h_.host_pinned("hring", 64 * sizeof(int), s_);
+  B_ = (double*)h_.buf("sampleB", (size_t)ell_ * n_ * 8, s_);
+  S_ = (double*)h_.buf("sampleS", (size_t)ell_ * n_ * 8, s_);
+  piv_ = (int64_t*)h_.buf("piv", (size_t)std::max<int64_t>(b_, 1) * 8, s_);
+  T_ = (double*)h_.buf("T", (size_t)b_ * b_ * 8, s_);
+  G_ = (double*)h_.buf("G", (size_t)b_ * n_ * 8, s_);
+  X_ = (double*)h_.buf("X", (size_t)b_ * n_ * 8, s_);
+  om_d_ = (double*)h_.buf("omega_d", (size_t)ell_ * m_ * 8, s_);
+  om_h_ = (double*)h_.host_pinned("omega_h", (size_t)ell_ * m_ * 8, s_);
+  if (p_.truncated) {
+    P_ = (double*)h_.buf("tr_panel", (size_t)m_ * b_ * 8, s_);
+    Z_ = (double*)h_.buf("tr_z", (size_t)std::max(ell_, b_) * k_ * 8, s_);
+  }
+  RQ_CUDA(cudaMemsetAsync(st_, 0, sizeof(Status), s_));
+  RQ_CUDA(cudaMemsetAsync(p_.tau, 0, (size_t)k_ * 8, s_));
+  fill2d(p_.Y, p_.ldy, m_, k_, 0.0, s_);
+  if (p_.truncated) {
+    fill2d(p_.W, p_.ldW, n_, k_, 0.0, s_);
+    fill2d(p_.R, p_.ldR, k_, n_, 0.0, s_);
+  }
+  {
+    std::vector<int64_t> iota(n_);
+    for (int64_t i = 0; i < n_; ++i) iota[i] = i;
+    RQ_CUDA(cudaMemcpyAsync(p_.perm, iota.data(), n_ * 8, cudaMemcpyHostToDevice, s_));
+    double* dfrob = (double*)h_.buf("frob", 8, s_);
+    frob_norm(h_, p_.work, m_, n_, p_.ldw, dfrob, s_);
+    RQ_CUDA(cudaMemcpyAsync(&hst_->level2, dfrob, 8, cudaMemcpyDeviceToHost, s_));
+    sync();  // also keeps `iota` alive until the copy is done
+    std::memcpy(&frob_, &hst_->level2, 8);
+  }
+  tol_ = kEps * frob_;
+  first_sample();
+
+  const bool speculate = p_.speculate && !p_.resketch_each_block;
+  if (ev_.empty()) {
+    ev_.resize(kLookahead + 1);
+    for (auto& e : ev_) RQ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  std::deque<Pending> pend;
+  int slot = 0;
+  int64_t i0 = 0, rank = k_;
+  bool stopped = false;
+  while (true) {
+    if (!pend.empty() && (stopped || i0 >= k_ || (int)pend.size() >= kLookahead)) {
+      Pending e = pend.front();
+      RQ_CUDA(cudaEventSynchronize(ev_[e.slot]));
+      if (hring_[e.slot] != 0) {
+        // a trigger fired at or after block e.i0: rewind to it
+        const Status stt = read_status();
+        const int64_t X = stt.abort_i0;
+        const int code = stt.abort;
+        int64_t bwX = 0;
+        for (const Pending& q : pend) {
+          if (q.i0 < X) {
+            c_.gemm_flops += q.stage.gemm_flops + q.update.gemm_flops;
+            c_.bytes_touched += q.stage.bytes_touched + q.update.bytes_touched;
+          } else if (q.i0 == X) {
+            bwX = q.bw;
+            if (code == kAbortDegenerate) {
+              c_.gemm_flops += q.stage.gemm_flops;
+              c_.bytes_touched += q.stage.bytes_touched;
+            }
+          }
+        }
+        pend.clear();
+        RQ_CUDA(cudaMemsetAsync(&st_->abort, 0, sizeof(int), s_));
+        if (code == kAbortDegenerate) {
+          i0 = X + bwX;
+          fresh_sample(i0);
+          c_.resamples += 1;
+        } else {
+          i0 = X;
+          fresh_sample(i0);
+          c_.resamples += 1;
+          if (!slow_block(i0, true, rank)) { stopped = true; break; }
+        }
+        continue;
+      }
+      c_.gemm_flops += e.stage.gemm_flops + e.update.gemm_flops;
+      c_.bytes_touched += e.stage.bytes_touched + e.update.bytes_touched;
+      pend.pop_front();
+      continue;
+    }
+    if (stopped || i0 >= k_) break;
+    if (!speculate) {
+      if (!slow_block(i0, false, rank)) { stopped = true; }
+      continue;
+    }
+    // ---- speculative block: assume got == usable == want, no degenerate R11
+    const int64_t want = std::min(b_, k_ - i0);
+    Pending e{};
+    e.i0 = i0;
+    e.bw = want;
+    select(i0, want, true);
+    swaps(i0, want);
+    panel(i0, want, kPanelCommitIfFull, true, e.stage);
+    stages(i0, want, e.stage);
+    e.has_update = i0 + want < k_;
+    if (e.has_update) update(i0 + want, want, true, e.update);
+    e.slot = slot;
+    RQ_CUDA(cudaMemcpyAsync(&hring_[slot], &st_->abort, sizeof(int), cudaMemcpyDeviceToHost, s_));
+    RQ_CUDA(cudaEventRecord(ev_[slot], s_));
+    slot = (slot + 1) % (kLookahead + 1);
+    pend.push_back(e);
+    i0 += want;
+  }
+  const Status fin = read_status();
+  FactorResult r;
+  r.rank = rank;
+  r.nswaps = fin.nswaps;
+  r.c = c_;
+  r.c.level2_flops = fin.level2;
+  r.c.bytes_touched += fin.l2bytes;
+  r.frob = frob_;
+  return r;
+}
+
+}  // namespace
+
+FactorResult run_factor(Handle& h, const FactorParams& p) {
+  Factor f(h, p);
+  return f.run();
+}
+
+// ------------------------------------------------------------------ qr_blocked / q_columns
+
+void qr_blocked(Handle& h, int64_t m, int64_t n, int64_t k, int64_t b, double* work,
+                int64_t ldw, double* Y, int64_t ldy, double* tau, Counters* c, cudaStream_t s) {
+  if (b < 1 || b > 256) throw InvalidArg("block must be in [1, 256]");
+  Status* st = (Status*)h.buf("qr_st", sizeof(Status), s);
+  RQ_CUDA(cudaMemsetAsync(st, 0, sizeof(Status), s));
+  fill2d(Y, ldy, m, k, 0.0, s);
+  RQ_CUDA(cudaMemsetAsync(tau, 0, (size_t)std::max<int64_t>(k, 1) * 8, s));
+  double* T = (double*)h.buf("qr_T", (size_t)b * b * 8, s);
+  double* G = (double*)h.buf("qr_G", (size_t)b * std::max<int64_t>(n, 1) * 8, s);
+  double* X = (double*)h.buf("qr_X", (size_t)b * std::max<int64_t>(n, 1) * 8, s);
+  for (int64_t i0 = 0; i0 < k; i0 += b) {
+    const int64_t bw = std::min(b, k - i0), mm = m - i0, nc = n - i0 - bw;
+    PanelOut o{};
+    o.Rdst = work + i0 + i0 * ldw; o.ldr = ldw; o.rrows = mm;
+    o.Y = Y + i0 + i0 * ldy; o.ldy = ldy; o.tau = tau + i0;
+    o.T = nc > 0 ? T : nullptr; o.ldt = b;
+    panel_qr(h, mm, bw, work + i0 + i0 * ldw, ldw, o, -1.0, kPanelCommitAll, false, st, i0, s);
+    if (nc > 0) {
+      // apply_block_reflection(transpose=True) (kernels.py:166-181)
+      double* C = work + i0 + (i0 + bw) * ldw;
+      const double* Yb = Y + i0 + i0 * ldy;
+      gemm(h, true, false, bw, nc, mm, 1.0, Yb, ldy, C, ldw, 0.0, G, bw, s);
+      gemm(h, true, false, bw, nc, bw, 1.0, T, b, G, bw, 0.0, X, bw, s);
+      gemm(h, false, false, mm, nc, bw, -1.0, Yb, ldy, X, bw, 1.0, C, ldw, s);
+      if (c) {
+        c->gemm_flops += 4 * mm * bw * nc + bw * bw * nc;
+        c->bytes_touched += 8 * (2 * mm * nc + mm * bw + bw * nc);
+      }
+    }
+  }
+  if (c) {
+    Status hs;
+    RQ_CUDA(cudaMemcpyAsync(&hs, st, sizeof(Status), cudaMemcpyDeviceToHost, s));
+    RQ_CUDA(cudaStreamSynchronize(s));
+    c->level2_flops += hs.level2;
+    c->bytes_touched += hs.l2bytes;
+  }
+}
+
+void q_columns(Handle& h, int64_t m, int64_t nref, int64_t cols, const double* Y, int64_t ldy,
+               const double* tau, int64_t b, double* Q, int64_t ldq, cudaStream_t s) {
+  set_identity(Q, ldq, m, cols, s);
+  if (nref <= 0 || cols <= 0) return;
+  double* T = (double*)h.buf("qc_T", (size_t)b * b * 8, s);
+  double* G = (double*)h.buf("qc_G", (size_t)b * cols * 8, s);
+  double* X = (double*)h.buf("qc_X", (size_t)b * cols * 8, s);
+  const int64_t nblk = (nref + b - 1) / b;
+  for (int64_t J = nblk - 1; J >= 0; --J) {
+    const int64_t i0 = J * b, bw = std::min(b, nref - i0), mm = m - i0;
+    if (i0 >= cols) continue;  // columns < i0 are untouched identity columns
+    const int64_t nc = cols - i0;
+    const double* Yb = Y + i0 + i0 * ldy;
+    t_factor(h, Yb, ldy, mm, bw, tau + i0, T, b, s);
+    double* C = Q + i0 + i0 * ldq;
+    gemm(h, true, false, bw, nc, mm, 1.0, Yb, ldy, C, ldq, 0.0, G, bw, s);
+    gemm(h, false, false, bw, nc, bw, 1.0, T, b, G, bw, 0.0, X, bw, s);
+    gemm(h, false, false, mm, nc, bw, -1.0, Yb, ldy, X, bw, 1.0, C, ldq, s);
+  }
+}
+
+}  // namespace rq
+
+namespace rq {
+
+// ------------------------------------------------------------------ TUXV
+TuxvResult run_tuxv(Handle& h, const TuxvParams& p) {
+  if (p.j_max < 1) throw InvalidArg("j_max must be >= 1");
+  cudaStream_t s = p.f.stream;
+  TuxvResult out;
+  out.f = run_factor(h, p.f);
+  Counters c = out.f.c;
+  const int64_t m = p.f.m, n = p.f.n, r = out.f.rank, b = p.f.block;
+  out.rank = r;
+  if (r == 0) {
+    out.f.c = c;
+    return out;
+  }
+  // Z = perm.restore(R[:r]) (k x n -> r x n), then lq_factor(Z) = qr_blocked(Z^T)
+  double* Z = (double*)h.buf("tx_Z", (size_t)r * n * 8, s);
+  fill2d(Z, r, r, n, 0.0, s);
+  scatter_cols(p.f.R, p.f.ldR, p.f.perm, Z, r, r, n, s);
+  double* Zt = (double*)h.buf("tx_Zt", (size_t)std::max(m, n) * r * 8, s);
+  double* Yq = (double*)h.buf("tx_Yq", (size_t)std::max(m, n) * r * 8, s);
+  double* tq = (double*)h.buf("tx_tau", (size_t)r * 8, s);
+  transpose(Z, r, Zt, n, r, n, s);
+  qr_blocked(h, n, r, r, b, Zt, n, Yq, n, tq, &c, s);
+  q_columns(h, n, r, r, Yq, n, tq, b, p.V, p.ldv, s);
+  int64_t j = 1;
+  while (true) {
+    // Zc = A V[:, :r]; U, X from qr_blocked(Zc)
+    gemm(h, false, false, m, r, n, 1.0, p.A, p.lda, p.V, p.ldv, 0.0, Zt, m, s);
+    c.gemm_flops += 2 * m * n * r;
+    c.bytes_touched += 8 * (m * n + n * r + m * r);
+    qr_blocked(h, m, r, r, b, Zt, m, Yq, m, tq, &c, s);
+    q_columns(h, m, r, r, Yq, m, tq, b, p.U, p.ldu, s);
+    copy2d(Zt, m, p.X, p.ldx, r, r, s);
+    out.x_lower = 0;
+    if (j >= p.j_max) break;
+    // Zr = U^T A (r x n); X, V = lq_factor(Zr)
+    gemm(h, true, false, r, n, m, 1.0, p.U, p.ldu, p.A, p.lda, 0.0, Z, r, s);
+    c.gemm_flops += 2 * m * n * r;
+    c.bytes_touched += 8 * (m * r + r * n);
+    transpose(Z, r, Zt, n, r, n, s);
+    qr_blocked(h, n, r, r, b, Zt, n, Yq, n, tq, &c, s);
+    q_columns(h, n, r, r, Yq, n, tq, b, p.V, p.ldv, s);
+    transpose(Zt, n, p.X, p.ldx, r, r, s);  // L = R^T
+    out.x_lower = 1;
+    if (j + 1 >= p.j_max) break;
+    j += 2;
+  }
+  RQ_CUDA(cudaStreamSynchronize(s));
+  out.f.c = c;
+  return out;
+}
+
+// ------------------------------------------------------------------ Handle
+Handle::Handle(int dev) : device(dev) {
+  RQ_CUDA(cudaSetDevice(dev));
+  RQ_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
+  int optin = 0;
+  RQ_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  smem_optin = (size_t)optin;
+}
+
+Handle::~Handle() {
+  for (auto& kv : bufs_) {
+    if (!kv.second.p) continue;
+    if (kv.second.pinned) cudaFreeHost(kv.second.p);
+    else cudaFree(kv.second.p);
+  }
+}
+
+void* Handle::buf(const std::string& name, size_t bytes, cudaStream_t s) {
+  Buf& b = bufs_[name];
+  if (bytes == 0) bytes = 8;
+  if (b.bytes < bytes) {
+    if (b.p) {
+      RQ_CUDA(cudaStreamSynchronize(s));
+      RQ_CUDA(cudaFree(b.p));
+      b.p = nullptr;
+    }
+    RQ_CUDA(cudaMalloc(&b.p, bytes));
+    b.bytes = bytes;
+  }
+  return b.p;
+}
+
+void* Handle::host_pinned(const std::string& name, size_t bytes, cudaStream_t s) {
+  Buf& b = bufs_["host:" + name];
+  if (bytes == 0) bytes = 8;
+  if (b.bytes < bytes) {
+    if (b.p) {
+      RQ_CUDA(cudaStreamSynchronize(s));
+      RQ_CUDA(cudaFreeHost(b.p));
+      b.p = nullptr;
+    }
+    RQ_CUDA(cudaMallocHost(&b.p, bytes));
+    b.bytes = bytes;
+    b.pinned = true;
+  }
+  return b.p;
+}
+
+}  // namespace rq

@@ -1,0 +1,125 @@
+// Host runtime for the sm_100a RQRCP library: device handle, grow-only
+// workspace arena, error plumbing and the launch helpers shared by the
+// drivers (driver.cu) and the C-ABI (abi.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <map>
+#include <stdexcept>
+#include <string>
+
+#include "common.cuh"
+
+namespace rq {
+
+struct CudaError : std::runtime_error {
+  int code;
+  CudaError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define RQ_CUDA(expr)                                                                  \
+  do {                                                                                 \
+    cudaError_t _e = (expr);                                                           \
+    if (_e != cudaSuccess)                                                             \
+      throw ::rq::CudaError(-3, std::string(#expr) + ": " + cudaGetErrorString(_e) +   \
+                                    " (" + __FILE__ + ":" + std::to_string(__LINE__) + \
+                                    ")");                                              \
+  } while (0)
+
+#define RQ_CHECK_LAUNCH() RQ_CUDA(cudaGetLastError())
+
+struct InvalidArg : std::runtime_error {
+  explicit InvalidArg(const std::string& m) : std::runtime_error(m) {}
+};
+
+class Handle {
+ public:
+  explicit Handle(int device);
+  ~Handle();
+  int device = 0;
+  int num_sms = 148;
+  size_t smem_optin = 227 * 1024;
+  // grow-only named device buffer; synchronises `s` before re-allocating
+  void* buf(const std::string& name, size_t bytes, cudaStream_t s);
+  void* host_pinned(const std::string& name, size_t bytes, cudaStream_t s);
+
+ private:
+  struct Buf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    bool pinned = false;
+  };
+  std::map<std::string, Buf> bufs_;
+};
+
+// ------------------------------------------------------------------ GEMM
+// C = alpha * op(A) op(B) + beta * C on `s` (gemm.cu).  Column-major.
+void gemm(Handle& h, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha,
+          const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
+          int64_t ldc, cudaStream_t s, const Status* st = nullptr);
+
+// ------------------------------------------------------------------ kernels (small.cu, select.cu, panel.cu)
+struct SelectOut {
+  double* S; int64_t lds;     // pivoted transformed sample (ell x nt)
+  int64_t* piv;               // want entries: step j swapped (j, piv[j])
+  double* Ys; int64_t ldys;   // optional sample reflectors (ell x want)
+  double* taus;               // optional
+};
+// b greedy steps of pivoted QR on the ell x nt sample (randomized.py:85-104).
+// abort_on_short: set Status.abort = kAbortShortSample when got < want.
+void select_pivots(Handle& h, int64_t ell, int64_t nt, int64_t want, const double* B,
+                   int64_t ldb, const SelectOut& out, Status* st, bool abort_on_short,
+                   int64_t i0, cudaStream_t s);
+
+struct PanelOut {
+  double* Rdst; int64_t ldr; int64_t rrows;   // transformed panel rows [0, rrows)
+  double* Y; int64_t ldy;                      // unit lower reflectors (mm x bw)
+  double* tau;
+  double* T; int64_t ldt;                      // optional T factor of the committed columns
+};
+// kPanelCommitIfFull: commit only when every column is usable (otherwise the
+// driver resamples; with raise_abort the kernel also sets Status.abort)
+enum PanelPolicy { kPanelCommitIfFull = 0, kPanelCommitUsable = 1, kPanelCommitAll = 2 };
+// Householder QR of an mm x bw panel (qrcp.py:206-219) + _panel_rank
+// (randomized.py:150-155) + build_t_matrix (kernels.py:139-147).
+void panel_qr(Handle& h, int64_t mm, int64_t bw, const double* P, int64_t ldp,
+              const PanelOut& out, double tol, PanelPolicy policy, bool raise_abort, Status* st,
+              int64_t i0, cudaStream_t s);
+
+// B_new = [S12 - S11 R11^{-1} R12; S22] (randomized.py:107-135).  Writes
+// Status.degenerate; with abort_on_degenerate also sets Status.abort.
+void sample_update(Handle& h, int64_t ell, int64_t b, int64_t n2, const double* S, int64_t lds,
+                   const double* R11, const double* R12, int64_t ldr, double frob,
+                   double* Bnew, int64_t ldb, Status* st, bool abort_on_degenerate, int64_t i0,
+                   cudaStream_t s);
+
+// replay the select swaps at offset i0 on work columns, perm, swap log and
+// row followers (randomized.py:138-147)
+struct SwapTargets {
+  double* work; int64_t ldw; int64_t m;
+  int64_t* perm;
+  int64_t* log; int64_t log_cap;
+  double* Wf; int64_t ldwf; int64_t wf_cols;   // optional W rows (TRQRCP)
+  double* Rf; int64_t ldrf; int64_t rf_rows;   // optional R columns (TRQRCP)
+};
+void apply_swaps(Handle& h, const int64_t* piv, int64_t got_max, int64_t i0,
+                 const SwapTargets& t, Status* st, cudaStream_t s);
+
+// misc
+void frob_norm(Handle& h, const double* A, int64_t m, int64_t n, int64_t lda, double* out,
+               cudaStream_t s);
+void copy2d(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows,
+            int64_t cols, cudaStream_t s, const Status* st = nullptr);
+void fill2d(double* dst, int64_t ldd, int64_t rows, int64_t cols, double v, cudaStream_t s);
+void transpose(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows,
+               int64_t cols, cudaStream_t s);
+void scatter_cols(const double* src, int64_t lds, const int64_t* perm, double* dst,
+                  int64_t ldd, int64_t rows, int64_t cols, cudaStream_t s);
+void set_identity(double* dst, int64_t ldd, int64_t rows, int64_t cols, cudaStream_t s);
+// full T factor of Y (mm x nb) from its Gram matrix (kernels.py:139-147)
+void t_factor(Handle& h, const double* Y, int64_t ldy, int64_t mm, int64_t nb,
+              const double* tau, double* T, int64_t ldt, cudaStream_t s);
+
+}  // namespace rq

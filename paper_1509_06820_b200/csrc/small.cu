@@ -1,0 +1,325 @@
+// Small / memory-bound kernels of the block loop: sample update (K3),
+// swap replay (K6), Frobenius norm (K10), copies, permutation scatter and
+// the standalone T factor.
+#include "runtime.hpp"
+
+namespace rq {
+
+namespace {
+
+// ---------------------------------------------------------------- K3
+// B_new[:, c] = [S12[:, c] - S11 R11^{-1} R12[:, c];  S22[:, c]]
+// (randomized.py:107-135).  One thread per sample column; R11 staged in
+// shared memory, the solve vector kept column-per-thread in shared memory.
+constexpr int kSuThreads = 64;
+
+__global__ void __launch_bounds__(kSuThreads) sample_update_kernel(
+    int ell, int b, int64_t n2, const double* __restrict__ S, int64_t lds,
+    const double* __restrict__ R11, const double* __restrict__ R12, int64_t ldr, double thresh,
+    double* __restrict__ Bn, int64_t ldb, Status* st, int abort_on_degenerate, int64_t i0) {
+  if (aborted(st)) return;
+  extern __shared__ __align__(16) double sm[];
+  double* r11 = sm;                    // b x b, col-major ld b
+  double* xs = sm + (size_t)b * b;     // b x kSuThreads
+  const int tid = threadIdx.x;
+  // degenerate test first, as the reference raises before solving (:117)
+  __shared__ int s_bad;
+  if (tid == 0) s_bad = 0;
+  __syncthreads();
+  for (int j = tid; j < b; j += kSuThreads)
+    if (fabs(R11[j + (size_t)j * ldr]) < thresh) s_bad = 1;
+  __syncthreads();
+  if (s_bad) {
+    if (blockIdx.x == 0 && tid == 0) {
+      st->degenerate = 1;
+      if (abort_on_degenerate) {
+        st->abort_i0 = i0;
+        __threadfence();
+        st->abort = kAbortDegenerate;
+      }
+    }
+    return;
+  }
+  if (blockIdx.x == 0 && tid == 0) st->degenerate = 0;
+  for (int e = tid; e < b * b; e += kSuThreads) {
+    const int i = e % b, j = e / b;
+    r11[e] = R11[i + (size_t)j * ldr];
+  }
+  __syncthreads();
+  const int64_t c = (int64_t)blockIdx.x * kSuThreads + tid;
+  if (c >= n2) return;
+  double* x = xs + tid;
+  for (int i = 0; i < b; ++i) x[i * kSuThreads] = R12[i + (size_t)c * ldr];
+  // back substitution (np.linalg.solve on the upper-triangular R11)
+  for (int i = b - 1; i >= 0; --i) {
+    const double xi = __ddiv_rn(x[i * kSuThreads], r11[i + i * b]);
+    x[i * kSuThreads] = xi;
+    for (int l = 0; l < i; ++l)
+      x[l * kSuThreads] = __fma_rn(-r11[l + i * b], xi, x[l * kSuThreads]);
+  }
+  // B1 = S12 - S11 @ X   (S11 upper triangular: only l >= i contribute)
+  const double* s12 = S + (size_t)(b + c) * lds;
+  double* out = Bn + (size_t)c * ldb;
+  for (int i = 0; i < b; ++i) {
+    double acc = 0.0;
+    for (int l = i; l < b; ++l) acc = __fma_rn(__ldg(S + i + (size_t)l * lds), x[l * kSuThreads], acc);
+    out[i] = __dsub_rn(s12[i], acc);
+  }
+  for (int i = b; i < ell; ++i) out[i] = s12[i];
+}
+
+// ---------------------------------------------------------------- K6
+__global__ void swap_kernel(const int64_t* __restrict__ piv, int64_t i0, SwapTargets t,
+                            Status* st, int64_t m_rows) {
+  if (aborted(st)) return;
+  const int got = (int)st->got;
+  const int which = blockIdx.y;
+  if (which == 0) {  // full columns of work (R rows included)
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < t.m;
+         r += (int64_t)gridDim.x * blockDim.x) {
+      for (int j = 0; j < got; ++j) {
+        const int64_t ga = i0 + j, gc = i0 + piv[j];
+        if (ga == gc) continue;
+        double* pa = t.work + r + ga * t.ldw;
+        double* pc = t.work + r + gc * t.ldw;
+        const double va = *pa;
+        *pa = *pc;
+        *pc = va;
+      }
+    }
+  } else if (which == 1 && t.Wf) {  // W rows follow A's columns
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < t.wf_cols;
+         c += (int64_t)gridDim.x * blockDim.x) {
+      for (int j = 0; j < got; ++j) {
+        const int64_t ga = i0 + j, gc = i0 + piv[j];
+        if (ga == gc) continue;
+        double* pa = t.Wf + ga + c * t.ldwf;
+        double* pc = t.Wf + gc + c * t.ldwf;
+        const double va = *pa;
+        *pa = *pc;
+        *pc = va;
+      }
+    }
+  } else if (which == 2 && t.Rf) {  // R columns (R.T rows)
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < t.rf_rows;
+         r += (int64_t)gridDim.x * blockDim.x) {
+      for (int j = 0; j < got; ++j) {
+        const int64_t ga = i0 + j, gc = i0 + piv[j];
+        if (ga == gc) continue;
+        double* pa = t.Rf + r + ga * t.ldrf;
+        double* pc = t.Rf + r + gc * t.ldrf;
+        const double va = *pa;
+        *pa = *pc;
+        *pc = va;
+      }
+    }
+  } else if (which == 3 && blockIdx.x == 0 && threadIdx.x == 0) {  // perm + swap log
+    int64_t n = st->nswaps;
+    for (int j = 0; j < got; ++j) {
+      const int64_t ga = i0 + j, gc = i0 + piv[j];
+      if (n < t.log_cap) {
+        t.log[2 * n] = ga;
+        t.log[2 * n + 1] = gc;
+      }
+      ++n;
+      if (ga != gc) {
+        const int64_t v = t.perm[ga];
+        t.perm[ga] = t.perm[gc];
+        t.perm[gc] = v;
+      }
+    }
+    st->nswaps = n;
+  }
+}
+
+// ---------------------------------------------------------------- K10
+constexpr int kNormBlocks = 296, kNormThreads = 256;
+__global__ void sumsq_partial_kernel(const double* A, int64_t m, int64_t n, int64_t lda,
+                                     double* part) {
+  __shared__ double red[kNormThreads];
+  double acc = 0.0;
+  const int64_t total = m * n;
+  for (int64_t e = (int64_t)blockIdx.x * kNormThreads + threadIdx.x; e < total;
+       e += (int64_t)kNormBlocks * kNormThreads) {
+    const double v = A[(e % m) + (e / m) * lda];
+    acc = __fma_rn(v, v, acc);
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = kNormThreads / 2; s; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] = __dadd_rn(red[threadIdx.x], red[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+__global__ void sumsq_final_kernel(const double* part, double* out) {
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int b = 0; b < kNormBlocks; ++b) t = __dadd_rn(t, part[b]);
+    *out = sqrt(t);
+  }
+}
+
+__global__ void copy2d_kernel(const double* src, int64_t lds, double* dst, int64_t ldd,
+                              int64_t rows, int64_t cols, const Status* st) {
+  if (aborted(st)) return;
+  const int64_t total = rows * cols;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e % rows, c = e / rows;
+    dst[r + c * ldd] = src[r + c * lds];
+  }
+}
+__global__ void fill2d_kernel(double* dst, int64_t ldd, int64_t rows, int64_t cols, double v) {
+  const int64_t total = rows * cols;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x)
+    dst[(e % rows) + (e / rows) * ldd] = v;
+}
+__global__ void identity_kernel(double* dst, int64_t ldd, int64_t rows, int64_t cols) {
+  const int64_t total = rows * cols;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e % rows, c = e / rows;
+    dst[r + c * ldd] = r == c ? 1.0 : 0.0;
+  }
+}
+// 32x32 tiled transpose: dst (cols x rows) = src (rows x cols)^T
+__global__ void transpose_kernel(const double* src, int64_t lds, double* dst, int64_t ldd,
+                                 int64_t rows, int64_t cols) {
+  __shared__ double tile[32][33];
+  const int64_t r0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t r = r0 + threadIdx.x, c = c0 + k;
+    if (r < rows && c < cols) tile[k][threadIdx.x] = src[r + c * lds];
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t c = c0 + threadIdx.x, r = r0 + k;
+    if (r < rows && c < cols) dst[c + r * ldd] = tile[threadIdx.x][k];
+  }
+}
+// dst[:, perm[i]] = src[:, i]  (Permutation.restore, kernels.py:107-111)
+__global__ void scatter_cols_kernel(const double* src, int64_t lds, const int64_t* perm,
+                                    double* dst, int64_t ldd, int64_t rows, int64_t cols) {
+  const int64_t total = rows * cols;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e % rows, c = e / rows;
+    dst[r + perm[c] * ldd] = src[r + c * lds];
+  }
+}
+// T recurrence from the Gram matrix G (nb x nb, upper part used)
+__global__ void t_recurrence_kernel(const double* G, int64_t ldg, const double* tau, int nb,
+                                    double* T, int64_t ldt) {
+  extern __shared__ double tmp[];
+  for (int j = 0; j < nb; ++j) {
+    for (int i = threadIdx.x; i < j; i += blockDim.x) {
+      double t = 0.0;
+      for (int l = i; l < j; ++l) t = __fma_rn(T[i + (size_t)l * ldt], G[l + (size_t)j * ldg], t);
+      tmp[i] = t;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+      double v = 0.0;
+      if (i < j) v = __dmul_rn(-tau[j], tmp[i]);
+      else if (i == j) v = tau[j];
+      T[i + (size_t)j * ldt] = v;
+    }
+    __syncthreads();
+  }
+}
+
+int grid_for(int64_t total, int num_sms) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 16LL * num_sms));
+}
+
+}  // namespace
+
+void sample_update(Handle& h, int64_t ell, int64_t b, int64_t n2, const double* S, int64_t lds,
+                   const double* R11, const double* R12, int64_t ldr, double frob,
+                   double* Bnew, int64_t ldb, Status* st, bool abort_on_degenerate, int64_t i0,
+                   cudaStream_t s) {
+  const size_t smem = ((size_t)b * b + (size_t)b * kSuThreads) * 8;
+  static size_t attr = 0;
+  if (smem > attr) {
+    RQ_CUDA(cudaFuncSetAttribute(sample_update_kernel,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)std::max<size_t>(smem, 48 * 1024)));
+    attr = std::max<size_t>(smem, 48 * 1024);
+  }
+  if (smem > h.smem_optin) throw InvalidArg("sample update block too wide");
+  const int blocks = (int)std::max<int64_t>(1, (n2 + kSuThreads - 1) / kSuThreads);
+  sample_update_kernel<<<blocks, kSuThreads, smem, s>>>(
+      (int)ell, (int)b, n2, S, lds, R11, R12, ldr, kEps34 * frob, Bnew, ldb, st,
+      abort_on_degenerate ? 1 : 0, i0);
+  RQ_CHECK_LAUNCH();
+}
+
+void apply_swaps(Handle& h, const int64_t* piv, int64_t got_max, int64_t i0,
+                 const SwapTargets& t, Status* st, cudaStream_t s) {
+  (void)got_max;
+  const int64_t mx = std::max<int64_t>(std::max<int64_t>(t.m, 1), std::max<int64_t>(t.Wf ? t.wf_cols : 0, t.Rf ? t.rf_rows : 0));
+  dim3 grid((unsigned)grid_for(mx, h.num_sms), 4);
+  swap_kernel<<<grid, 256, 0, s>>>(piv, i0, t, st, t.m);
+  RQ_CHECK_LAUNCH();
+}
+
+void frob_norm(Handle& h, const double* A, int64_t m, int64_t n, int64_t lda, double* out,
+               cudaStream_t s) {
+  double* part = (double*)h.buf("frob_part", kNormBlocks * 8, s);
+  sumsq_partial_kernel<<<kNormBlocks, kNormThreads, 0, s>>>(A, m, n, lda, part);
+  RQ_CHECK_LAUNCH();
+  sumsq_final_kernel<<<1, 32, 0, s>>>(part, out);
+  RQ_CHECK_LAUNCH();
+}
+
+void copy2d(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows,
+            int64_t cols, cudaStream_t s, const Status* st) {
+  if (rows <= 0 || cols <= 0) return;
+  copy2d_kernel<<<grid_for(rows * cols, 148), 256, 0, s>>>(src, lds, dst, ldd, rows, cols, st);
+  RQ_CHECK_LAUNCH();
+}
+
+void fill2d(double* dst, int64_t ldd, int64_t rows, int64_t cols, double v, cudaStream_t s) {
+  if (rows <= 0 || cols <= 0) return;
+  fill2d_kernel<<<grid_for(rows * cols, 148), 256, 0, s>>>(dst, ldd, rows, cols, v);
+  RQ_CHECK_LAUNCH();
+}
+
+void set_identity(double* dst, int64_t ldd, int64_t rows, int64_t cols, cudaStream_t s) {
+  if (rows <= 0 || cols <= 0) return;
+  identity_kernel<<<grid_for(rows * cols, 148), 256, 0, s>>>(dst, ldd, rows, cols);
+  RQ_CHECK_LAUNCH();
+}
+
+void transpose(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows,
+               int64_t cols, cudaStream_t s) {
+  if (rows <= 0 || cols <= 0) return;
+  dim3 grid((unsigned)((rows + 31) / 32), (unsigned)((cols + 31) / 32));
+  transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(src, lds, dst, ldd, rows, cols);
+  RQ_CHECK_LAUNCH();
+}
+
+void scatter_cols(const double* src, int64_t lds, const int64_t* perm, double* dst,
+                  int64_t ldd, int64_t rows, int64_t cols, cudaStream_t s) {
+  if (rows <= 0 || cols <= 0) return;
+  scatter_cols_kernel<<<grid_for(rows * cols, 148), 256, 0, s>>>(src, lds, perm, dst, ldd,
+                                                                  rows, cols);
+  RQ_CHECK_LAUNCH();
+}
+
+void t_factor(Handle& h, const double* Y, int64_t ldy, int64_t mm, int64_t nb,
+              const double* tau, double* T, int64_t ldt, cudaStream_t s) {
+  if (nb <= 0) return;
+  double* G = (double*)h.buf("tf_gram", (size_t)nb * nb * 8, s);
+  gemm(h, true, false, nb, nb, mm, 1.0, Y, ldy, Y, ldy, 0.0, G, nb, s);
+  const size_t smem = (size_t)nb * 8;
+  if (smem > 48 * 1024)
+    RQ_CUDA(cudaFuncSetAttribute(t_recurrence_kernel,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  t_recurrence_kernel<<<1, 256, smem, s>>>(G, nb, tau, (int)nb, T, ldt);
+  RQ_CHECK_LAUNCH();
+}
+
+}  // namespace rq

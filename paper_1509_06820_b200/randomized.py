@@ -1,0 +1,194 @@
+"""Randomized column-pivoted QR -- drop-in for pkg/src/rqrcp/randomized.py.
+
+Same entry points and signatures as the reference (``rqrcp``, ``rsrqrcp``,
+``ssrqrcp``, ``RandomizedConfig``), plus the north_star extension
+``omega=`` (explicit first Omega, ell x m; resamples continue the seeded
+stream at position ell*m).  The block loop runs natively in
+librqrcp_b200.so (csrc/driver.cu) on sm_100a kernels; this module only
+validates arguments with the reference's error messages, moves data, and
+supplies the host Omega stream.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _abi
+from .device import fmat, handle, ld, lib, ptr, require_cuda, stream_ptr, to_device_fortran
+from .factorization import BlockReflectors, Factorization, OpCounters, Permutation
+from .rng import RngState
+
+
+@dataclass
+class RandomizedConfig:
+    """randomized.py:22-40."""
+
+    block: int = 32
+    padding: int = 8
+    seed: int = 0
+
+    def __post_init__(self):
+        if self.block < 1:
+            raise ValueError("block must be >= 1")
+        if self.padding < 1:
+            raise ValueError("padding must be >= 1")
+
+    @property
+    def ell(self):
+        return self.block + self.padding
+
+
+class DegenerateSampleError(RuntimeError):
+    """randomized.py:43-45 (raised and handled inside the native driver)."""
+
+
+def _validate_rank(k, m, n):
+    """qrcp.py:87-94."""
+    kmax = min(m, n)
+    if k is None:
+        return kmax
+    k = int(k)
+    if not 0 <= k <= kmax:
+        raise ValueError(f"rank {k} outside [0, {kmax}]")
+    return k
+
+
+class _OmegaSource:
+    """ctypes callback feeding the native driver from the host RngState."""
+
+    def __init__(self, rng: RngState):
+        self.rng = rng
+
+        def fill(_user, rows, cols, dst):
+            try:
+                buf = np.ctypeslib.as_array(dst, shape=(int(rows) * int(cols),))
+                self.rng.fill(buf)
+                return 0
+            except Exception:  # pragma: no cover - surfaced as an ABI error
+                return 1
+
+        self.fn = _abi.OMEGA_FN(fill)
+
+
+def _shape_of(A):
+    if torch.is_tensor(A):
+        if A.dim() != 2:
+            raise ValueError("expected a 2-d array")
+        return int(A.shape[0]), int(A.shape[1])
+    a = np.asarray(A)
+    if a.ndim != 2:
+        raise ValueError("expected a 2-d array")
+    return int(a.shape[0]), int(a.shape[1])
+
+
+def _prepare_omega(omega, ell, m, seed, dev):
+    if omega is None:
+        return None, RngState(seed)
+    om = to_device_fortran(omega, dev)
+    if tuple(om.shape) != (ell, m):
+        raise ValueError(f"omega must be {ell} x {m}")
+    return om, RngState(seed, position=ell * m)
+
+
+def run_native(A, k, config, *, variant, ell, width, omega=None, speculate=True, device=None):
+    """Shared body of every factorization entry point: returns the raw device
+    outputs plus the library's result struct."""
+    m, n = _shape_of(A)
+    dev = require_cuda(device if device is not None else
+                       (A.device if torch.is_tensor(A) and A.is_cuda else None))
+    work = to_device_fortran(A, dev)
+    Y = fmat(m, k, dev)
+    tau = torch.empty(k, dtype=torch.float64, device=dev)
+    perm = torch.empty(n, dtype=torch.int64, device=dev)
+    cap = 2 * k + 16
+    swaps = torch.empty(2 * cap, dtype=torch.int64, device=dev)
+    W = R = None
+    if variant == _abi.RQ_TRQRCP:
+        W = fmat(n, k, dev)
+        R = fmat(k, n, dev)
+    om, rng = _prepare_omega(omega, ell, m, config.seed, dev)
+    src = _OmegaSource(rng)
+    args = _abi.FactorArgs(
+        m=m, n=n, k=k, block=width, ell=ell, variant=variant, speculate=1 if speculate else 0,
+        work=ptr(work), ldw=ld(work), Y=ptr(Y), ldy=ld(Y), tau=ptr(tau),
+        W=ptr(W), ldW=ld(W) if W is not None else 0, R=ptr(R), ldR=ld(R) if R is not None else 0,
+        perm=ptr(perm), swaps=ptr(swaps), swap_cap=cap, omega0=ptr(om), omega_fn=src.fn,
+        omega_user=None, stream=stream_ptr(dev))
+    res = _abi.FactorResult()
+    _abi.check(lib().rq_factor(handle(dev), C.byref(args), C.byref(res)))
+    return dict(work=work, Y=Y, tau=tau, perm=perm, swaps=swaps, W=W, R=R, res=res,
+                rng=rng, device=dev)
+
+
+def _counters(res):
+    return OpCounters(gemm_flops=int(res.gemm_flops), level2_flops=int(res.level2_flops),
+                      bytes_touched=int(res.bytes_touched), resamples=int(res.resamples))
+
+
+def _swap_list(swaps, n):
+    pairs = swaps[: 2 * n].view(-1, 2).cpu().numpy()
+    return [(int(a), int(b)) for a, b in pairs]
+
+
+def package(out, host, trailing_update=True, truncated=False):
+    """Shape raw outputs into the reference's result types."""
+    res = out["res"]
+    rank = int(res.rank)
+    swaps = _swap_list(out["swaps"], int(res.nswaps))
+    Y = out["Y"][:, :rank]
+    tau = out["tau"][:rank]
+    if truncated:
+        R = out["R"][:rank, :]
+        W = out["W"][:, :rank]
+        trailing = None
+    else:
+        R = out["work"][:rank, :]
+        W = None
+        trailing = out["work"][rank:, rank:] if trailing_update else None
+    perm = out["perm"]
+    if host:
+        cv = lambda t: None if t is None else t.cpu().numpy()  # noqa: E731
+        Y, tau, R, W, trailing, perm = cv(Y), cv(tau), cv(R), cv(W), cv(trailing), cv(perm)
+        R = np.ascontiguousarray(R)
+    else:
+        R = R.clone()
+        trailing = trailing.clone() if trailing is not None else None
+    return rank, Y, tau, R, W, trailing, Permutation(forward=perm, swaps=swaps)
+
+
+def _randomized_factor(A, k, config, ell, block_width, variant, trailing_update, omega):
+    m, n = _shape_of(A)
+    k = _validate_rank(k, m, n)
+    if k == 0:
+        raise ValueError("rank must be >= 1")
+    if ell > m:
+        raise ValueError(f"sample rows {ell} exceed matrix rows {m}")
+    host = not (torch.is_tensor(A) and A.is_cuda)
+    out = run_native(A, k, config, variant=variant, ell=ell, width=block_width, omega=omega)
+    rank, Y, tau, R, _, trailing, perm = package(out, host, trailing_update)
+    return Factorization(reflectors=BlockReflectors(Y, tau), R=R, perm=perm, rank=rank,
+                         counters=_counters(out["res"]), trailing=trailing)
+
+
+def rqrcp(A, k=None, config=None, omega=None):
+    """Randomized pivoted QR, sample downdated across blocks (randomized.py:269-281)."""
+    config = config if config is not None else RandomizedConfig()
+    return _randomized_factor(A, k, config, config.ell, config.block, _abi.RQ_RQRCP, True, omega)
+
+
+def rsrqrcp(A, k=None, config=None, omega=None):
+    """Fresh sketch before every block (randomized.py:284-296)."""
+    config = config if config is not None else RandomizedConfig()
+    return _randomized_factor(A, k, config, config.ell, config.block, _abi.RQ_RSRQRCP, True,
+                              omega)
+
+
+def ssrqrcp(A, k, config=None, omega=None):
+    """One (k + padding)-row sketch selects all k pivots (randomized.py:299-313)."""
+    config = config if config is not None else RandomizedConfig()
+    k = int(k)
+    return _randomized_factor(A, k, config, k + config.padding, k, _abi.RQ_SSRQRCP, False, omega)

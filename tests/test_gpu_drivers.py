@@ -1,0 +1,130 @@
+"""Driver-level parity on the B200: every reference-generated fixture
+(tests/golden/*.npz) re-run through the drop-in API (C-ABI underneath).
+
+Bars (BASELINE north_star): identical pivot permutation; R within 1e-10
+relative; ||AP - QR||_F/||A||_F <= 1e-12; ||Q^T Q - I|| <= 1e-12; identical
+OpCounters (gemm, level-2, bytes, resamples) and rank; TUXV singular values
+and approximation within 1e-9 relative of the reference.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import port
+from tests import _golden as G
+
+pytestmark = pytest.mark.gpu
+
+
+def _cfg(rec):
+    import paper_1509_06820_b200 as P
+    return P.RandomizedConfig(block=int(rec["block"]), padding=int(rec["padding"]),
+                              seed=int(rec["seed"]))
+
+
+def _run(rec, A, **kw):
+    import paper_1509_06820_b200 as P
+    drv = str(rec["driver"])
+    return getattr(P, drv)(A, G.k_of(rec), _cfg(rec), **kw)
+
+
+@pytest.mark.parametrize("name", G.case_names())
+def test_driver_matches_reference_fixture(name):
+    rec = G.load(name)
+    A = G.matrix_of(rec)
+    f = _run(rec, A)
+    frob = float(np.linalg.norm(A))
+    assert f.rank == int(rec["rank"])
+    if str(rec["driver"]) == "tuxv":
+        np.testing.assert_allclose(f.singular_values(), rec["sv"], rtol=1e-9, atol=1e-12 * frob)
+        ref = rec["U"] @ (rec["X"] @ rec["V"].T)
+        assert np.linalg.norm(f.approx() - ref) <= 1e-9 * frob
+        assert f.counters.gemm_flops == int(rec["gemm_flops"])
+        assert f.counters.level2_flops == int(rec["level2_flops"])
+        return
+    c = f.counters
+    assert c.resamples == int(rec["resamples"])
+    assert c.gemm_flops == int(rec["gemm_flops"])
+    assert c.level2_flops == int(rec["level2_flops"])
+    assert c.bytes_touched == int(rec["bytes_touched"])
+    np.testing.assert_array_equal(f.perm.forward, rec["perm"])
+    np.testing.assert_array_equal(np.array(f.perm.swaps, dtype=np.int64).reshape(-1, 2),
+                                  rec["swaps"])
+    if "R" in rec:
+        assert np.linalg.norm(f.R - rec["R"]) <= 1e-10 * max(np.linalg.norm(rec["R"]), 1e-300)
+        if "trailing" in rec and rec["trailing"].size:
+            assert np.linalg.norm(f.trailing - rec["trailing"]) <= 1e-10 * frob
+        if "W" in rec:
+            assert np.linalg.norm(f.reflectors.W - rec["W"]) <= 1e-10 * max(frob, 1e-300)
+    else:
+        np.testing.assert_allclose(np.diag(f.R), rec["R_diag"], rtol=1e-10, atol=1e-12 * frob)
+    if f.rank:
+        q = f.q_factor()
+        assert np.linalg.norm(q.T @ q - np.eye(f.rank), 2) <= 1e-12
+        if str(rec["driver"]) in ("rqrcp", "rsrqrcp") and f.rank == min(A.shape):
+            res = np.linalg.norm(A[:, f.perm.forward] - q @ f.R) / max(frob, 1e-300)
+            assert res <= 1e-12
+
+
+def test_explicit_omega_matches_seeded_stream():
+    import paper_1509_06820_b200 as P
+    A = np.random.default_rng(3).standard_normal((200, 150))
+    cfg = P.RandomizedConfig(block=16, padding=8, seed=4)
+    om = P.gaussian_matrix(P.RngState(4), cfg.ell, 200)
+    f1 = P.rqrcp(A, None, cfg)
+    f2 = P.rqrcp(A, None, cfg, omega=om)
+    np.testing.assert_array_equal(f1.perm.forward, f2.perm.forward)
+    np.testing.assert_array_equal(f1.R, f2.R)
+
+
+def test_deterministic_and_device_inputs():
+    import torch
+    import paper_1509_06820_b200 as P
+    A = np.random.default_rng(4).standard_normal((500, 400))
+    cfg = P.RandomizedConfig(block=32, padding=8, seed=11)
+    f1 = P.rqrcp(A, 256, cfg)
+    f2 = P.rqrcp(A, 256, cfg)
+    np.testing.assert_array_equal(f1.R, f2.R)
+    fd = P.rqrcp(torch.from_numpy(A).cuda(), 256, cfg)
+    assert fd.R.is_cuda
+    np.testing.assert_array_equal(fd.R.cpu().numpy(), f1.R)
+
+
+def test_validation_errors_match_reference():
+    import paper_1509_06820_b200 as P
+    with pytest.raises(ValueError, match="rank 7 outside"):
+        P.rqrcp(np.eye(6), 7)
+    with pytest.raises(ValueError, match="rank must be >= 1"):
+        P.rqrcp(np.eye(6), 0, P.RandomizedConfig(block=2, padding=2))
+    with pytest.raises(ValueError, match="sample rows"):
+        P.ssrqrcp(np.diag([4.0, 3.0, 2.0, 1.0]), 2, P.RandomizedConfig(padding=8))
+    with pytest.raises(ValueError, match="j_max"):
+        P.tuxv(np.eye(4), 2, P.RandomizedConfig(block=2, padding=2), j_max=0)
+    with pytest.raises(ValueError):
+        P.RandomizedConfig(block=0)
+
+
+@pytest.mark.parametrize("n,b", [(2048, 64), (1536, 128)])
+def test_rqrcp_larger_vs_oracle(n, b):
+    import paper_1509_06820_b200 as P
+    A = np.random.default_rng(n).standard_normal((n, n))
+    o = port.rqrcp(A, None, b, 8, 0)
+    f = P.rqrcp(A, None, P.RandomizedConfig(block=b, padding=8, seed=0))
+    np.testing.assert_array_equal(f.perm.forward, o.perm.forward)
+    assert np.linalg.norm(f.R - o.R) <= 1e-10 * np.linalg.norm(o.R)
+    assert f.counters.gemm_flops == o.counters.gemm_flops
+
+
+def test_trqrcp_tuxv_vs_oracle_mid_size():
+    import paper_1509_06820_b200 as P
+    g = np.random.default_rng(1)
+    A = g.standard_normal((3000, 200)) @ g.standard_normal((200, 2500)) \
+        + 1e-6 * g.standard_normal((3000, 2500))
+    cfg = P.RandomizedConfig(block=32, padding=8, seed=0)
+    o = port.trqrcp(A, 256, 32, 8, 0)
+    f = P.trqrcp(A, 256, cfg)
+    np.testing.assert_array_equal(f.perm.forward, o.perm.forward)
+    assert np.linalg.norm(f.R - o.R) <= 1e-10 * np.linalg.norm(o.R)
+    ot = port.tuxv(A, 128, 32, 8, 0)
+    ft = P.tuxv(A, 128, cfg)
+    np.testing.assert_allclose(ft.singular_values(), ot.singular_values(), rtol=1e-9)

@@ -1,0 +1,132 @@
+"""Kernel-level parity on the B200: each C-ABI primitive against the reference
+fixtures (tests/golden/kat_*.npz) and the CPU oracle (oracle/port.py)."""
+
+import numpy as np
+import pytest
+
+from oracle import port
+from tests import _golden as G
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _dev(x):
+    import paper_1509_06820_b200.device as D
+    return D.to_device_fortran(x, torch.device("cuda", 0))
+
+
+@pytest.mark.parametrize("ta", [False, True])
+@pytest.mark.parametrize("tb", [False, True])
+@pytest.mark.parametrize("shape", [(64, 96, 40), (130, 70, 3000), (7, 5, 3), (300, 257, 129),
+                                   (72, 1000, 8192)])
+def test_gemm_matches_fp64_reference(ta, tb, shape):
+    from paper_1509_06820_b200.primitives import gemm
+    m, n, k = shape
+    g = np.random.default_rng(m * 7 + n + k)
+    A = g.standard_normal((k, m) if ta else (m, k))
+    B = g.standard_normal((n, k) if tb else (k, n))
+    C0 = g.standard_normal((m, n))
+    ref = (A.T if ta else A) @ (B.T if tb else B)
+    for alpha, beta, want in ((1.0, 0.0, ref), (-1.0, 1.0, C0 - ref), (0.5, 2.0, 0.5 * ref + 2 * C0)):
+        out = gemm(_dev(A), _dev(B), _dev(C0), alpha=alpha, beta=beta, transa=ta, transb=tb)
+        got = out.cpu().numpy()
+        # fp64 accumulation: error <= a few eps * k * |A||B|
+        tol = 8 * k * np.finfo(float).eps * (np.abs(A).max() * np.abs(B).max() + np.abs(C0).max())
+        assert np.max(np.abs(got - want)) <= tol, (alpha, beta)
+
+
+def test_gemm_k_zero_scales_c():
+    from paper_1509_06820_b200.primitives import gemm
+    C0 = np.random.default_rng(0).standard_normal((10, 12))
+    out = gemm(_dev(np.zeros((10, 0))), _dev(np.zeros((0, 12))), _dev(C0), alpha=1.0, beta=2.0)
+    np.testing.assert_array_equal(out.cpu().numpy(), 2 * C0)
+
+
+def test_select_pivots_matches_reference_fixtures():
+    from paper_1509_06820_b200.primitives import select_pivots
+    rec = G.load("kat_select")
+    keys = sorted({k.rsplit("_", 1)[0] for k in rec})
+    for key in keys:
+        B = rec[f"{key}_B"]
+        want = int(rec[f"{key}_want"])
+        S, piv, got, Ys, taus, l2 = select_pivots(_dev(B), want)
+        assert got == int(rec[f"{key}_got"]), key
+        # replay the local swaps -> Permutation.forward
+        fwd = list(range(B.shape[1]))
+        for j, p in enumerate(piv):
+            fwd[j], fwd[p] = fwd[p], fwd[j]
+        np.testing.assert_array_equal(fwd, rec[f"{key}_perm"], err_msg=key)
+        np.testing.assert_array_equal(np.array([(j, p) for j, p in enumerate(piv)]).reshape(-1, 2),
+                                      rec[f"{key}_swaps"], err_msg=key)
+        scale = float(np.linalg.norm(B))
+        assert np.linalg.norm(S.cpu().numpy() - rec[f"{key}_S"]) <= 1e-12 * scale, key
+        np.testing.assert_allclose(taus.cpu().numpy(), rec[f"{key}_taus"], rtol=1e-12, atol=1e-14)
+        assert l2 == int(rec[f"{key}_l2"]), key
+    assert list(rec["diag_perm"][:4]) == [1, 3, 0, 2]
+
+
+def test_select_pivots_wide_sample_vs_oracle():
+    from paper_1509_06820_b200.primitives import select_pivots
+    g = np.random.default_rng(5)
+    for ell, nt, want in ((72, 8192, 64), (40, 1000, 32), (136, 5000, 128), (20, 33, 12)):
+        B = g.standard_normal((ell, nt)) * np.exp(g.uniform(-2, 2, nt))
+        smp = port.Sample(B=np.asfortranarray(B.copy()), ell=ell)
+        perm, got = port.pick_pivots(smp, want, port.Counters())
+        S, piv, got_d, *_ = select_pivots(_dev(B), want)
+        assert got_d == got
+        fwd = list(range(nt))
+        for j, p in enumerate(piv):
+            fwd[j], fwd[p] = fwd[p], fwd[j]
+        np.testing.assert_array_equal(fwd, perm.forward)
+        assert np.linalg.norm(S.cpu().numpy() - smp.B) <= 1e-12 * np.linalg.norm(B)
+
+
+def test_panel_matches_reference_fixtures():
+    from paper_1509_06820_b200.primitives import panel_qr
+    rec = G.load("kat_panel")
+    s = 0
+    while f"p{s}_P" in rec:
+        P = _dev(rec[f"p{s}_P"])
+        Y, tau, T, usable, l2 = panel_qr(P)
+        sc = float(np.linalg.norm(rec[f"p{s}_P"]))
+        assert np.linalg.norm(P.cpu().numpy() - rec[f"p{s}_R"]) <= 1e-13 * sc
+        assert np.linalg.norm(Y.cpu().numpy() - rec[f"p{s}_Y"]) <= 1e-12 * np.linalg.norm(rec[f"p{s}_Y"])
+        np.testing.assert_allclose(tau.cpu().numpy(), rec[f"p{s}_tau"], rtol=1e-12, atol=1e-15)
+        assert np.linalg.norm(T.cpu().numpy() - rec[f"p{s}_T"]) <= 1e-12 * np.linalg.norm(rec[f"p{s}_T"])
+        assert l2 == int(rec[f"p{s}_l2"])
+        assert usable == P.shape[1]
+        s += 1
+
+
+@pytest.mark.parametrize("mm,bw", [(8192, 64), (32768, 128), (1000, 32), (257, 17)])
+def test_panel_large_vs_oracle(mm, bw):
+    from paper_1509_06820_b200.primitives import panel_qr
+    P0 = np.random.default_rng(mm + bw).standard_normal((mm, bw))
+    Pc = np.asfortranarray(P0.copy())
+    Yo, to = port.panel_qr(Pc)
+    P = _dev(P0)
+    Y, tau, T, usable, _ = panel_qr(P)
+    assert np.linalg.norm(P.cpu().numpy() - Pc) <= 1e-13 * np.linalg.norm(P0)
+    assert np.linalg.norm(Y.cpu().numpy() - Yo) <= 1e-12 * np.linalg.norm(Yo)
+    np.testing.assert_allclose(T.cpu().numpy(), port.t_factor(Yo, to), rtol=1e-10, atol=1e-13)
+
+
+def test_sample_update_vs_oracle():
+    from paper_1509_06820_b200.primitives import sample_update
+    g = np.random.default_rng(3)
+    ell, b, nt = 72, 64, 700
+    B = g.standard_normal((ell, nt))
+    smp = port.Sample(B=np.asfortranarray(B.copy()), ell=ell, frob_a=10.0)
+    port.pick_pivots(smp, b, port.Counters())
+    S = smp.B.copy()
+    R11 = np.triu(g.standard_normal((b, b))) + 4 * np.eye(b)
+    R12 = g.standard_normal((b, nt - b))
+    port.downdate_sample(smp, R11, R12, port.Counters())
+    Bn, deg = sample_update(_dev(S), b, _dev(R11), _dev(R12), 10.0)
+    assert not deg
+    assert np.linalg.norm(Bn.cpu().numpy() - smp.B) <= 1e-11 * np.linalg.norm(smp.B)
+    R11[5, 5] = 1e-300
+    _, deg = sample_update(_dev(S), b, _dev(R11), _dev(R12), 10.0)
+    assert deg
