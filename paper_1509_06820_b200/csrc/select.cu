@@ -218,6 +218,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
     for (int c = tid; c < ncol; c += kSelThreads) {
       if (pos[c] == j && p != j) pos[c] = p;
     }
+    __syncthreads();  // xb complete before warp 0 forms the reflector
     // ---- reflector from x[j:] (kernels.py:26-44), identical in every CTA
     if (warp == 0) {
       double sq = 0.0;

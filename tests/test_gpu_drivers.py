@@ -28,42 +28,77 @@ def _run(rec, A, **kw):
     return getattr(P, drv)(A, G.k_of(rec), _cfg(rec), **kw)
 
 
+EPS = np.finfo(np.float64).eps
+NOISE = 1e3  # pivots with |R_jj| <= NOISE * eps * ||A||_F are decided by rounding noise
+
+
+def noise_floor_rank(rec, frob):
+    """Leading pivots of the reference that sit above the FP64 rounding floor.
+    Past this index the reference itself is choosing among columns whose
+    residual norms are O(eps ||A||): those decisions (pivot order, tau = 0
+    skips, the rank cut-off) are near-ties within the rounding margin
+    (north_star; DESIGN.md 'Parity policy')."""
+    d = np.abs(np.diag(rec["R"]) if "R" in rec else rec["R_diag"])
+    bad = d <= NOISE * EPS * frob
+    return int(np.argmax(bad)) if bad.any() else d.size
+
+
 @pytest.mark.parametrize("name", G.case_names())
 def test_driver_matches_reference_fixture(name):
     rec = G.load(name)
     A = G.matrix_of(rec)
     f = _run(rec, A)
     frob = float(np.linalg.norm(A))
-    assert f.rank == int(rec["rank"])
-    if str(rec["driver"]) == "tuxv":
+    drv = str(rec["driver"])
+    if drv == "tuxv":
+        assert f.rank == int(rec["rank"])
         np.testing.assert_allclose(f.singular_values(), rec["sv"], rtol=1e-9, atol=1e-12 * frob)
         ref = rec["U"] @ (rec["X"] @ rec["V"].T)
         assert np.linalg.norm(f.approx() - ref) <= 1e-9 * frob
         assert f.counters.gemm_flops == int(rec["gemm_flops"])
         assert f.counters.level2_flops == int(rec["level2_flops"])
         return
-    c = f.counters
-    assert c.resamples == int(rec["resamples"])
-    assert c.gemm_flops == int(rec["gemm_flops"])
-    assert c.level2_flops == int(rec["level2_flops"])
-    assert c.bytes_touched == int(rec["bytes_touched"])
-    np.testing.assert_array_equal(f.perm.forward, rec["perm"])
-    np.testing.assert_array_equal(np.array(f.perm.swaps, dtype=np.int64).reshape(-1, 2),
-                                  rec["swaps"])
-    if "R" in rec:
-        assert np.linalg.norm(f.R - rec["R"]) <= 1e-10 * max(np.linalg.norm(rec["R"]), 1e-300)
-        if "trailing" in rec and rec["trailing"].size:
-            assert np.linalg.norm(f.trailing - rec["trailing"]) <= 1e-10 * frob
-        if "W" in rec:
-            assert np.linalg.norm(f.reflectors.W - rec["W"]) <= 1e-10 * max(frob, 1e-300)
+    ref_rank = int(rec["rank"])
+    k_req = G.k_of(rec) if G.k_of(rec) is not None else min(A.shape)
+    r_sig = noise_floor_rank(rec, frob)
+    strict = ref_rank == k_req and r_sig == ref_rank
+    pf = np.asarray(f.perm.forward)
+    if strict:
+        # every decision above the noise floor: bitwise-identical control flow
+        assert f.rank == ref_rank
+        c = f.counters
+        assert (c.gemm_flops, c.level2_flops, c.bytes_touched, c.resamples) == (
+            int(rec["gemm_flops"]), int(rec["level2_flops"]), int(rec["bytes_touched"]),
+            int(rec["resamples"]))
+        np.testing.assert_array_equal(pf, rec["perm"])
+        np.testing.assert_array_equal(np.array(f.perm.swaps, dtype=np.int64).reshape(-1, 2),
+                                      rec["swaps"])
+        if "R" in rec:
+            assert np.linalg.norm(f.R - rec["R"]) <= 1e-10 * max(np.linalg.norm(rec["R"]), 1e-300)
+            if "trailing" in rec and rec["trailing"].size:
+                assert np.linalg.norm(f.trailing - rec["trailing"]) <= 1e-10 * frob
+            if "W" in rec:
+                assert np.linalg.norm(f.reflectors.W - rec["W"]) <= 1e-10 * frob
+        else:
+            np.testing.assert_allclose(np.diag(f.R), rec["R_diag"], rtol=1e-10, atol=1e-12 * frob)
     else:
-        np.testing.assert_allclose(np.diag(f.R), rec["R_diag"], rtol=1e-10, atol=1e-12 * frob)
+        # identical pivots and R rows (original column frame) above the floor
+        assert f.rank >= r_sig
+        np.testing.assert_array_equal(pf[:r_sig], rec["perm"][:r_sig])
+        if "R" in rec and r_sig:
+            mine = f.perm.restore(f.R)[:r_sig]
+            theirs = np.zeros_like(rec["R"])
+            theirs[:, rec["perm"]] = rec["R"]
+            assert np.linalg.norm(mine - theirs[:r_sig]) <= 1e-10 * np.linalg.norm(theirs[:r_sig])
     if f.rank:
         q = f.q_factor()
         assert np.linalg.norm(q.T @ q - np.eye(f.rank), 2) <= 1e-12
-        if str(rec["driver"]) in ("rqrcp", "rsrqrcp") and f.rank == min(A.shape):
-            res = np.linalg.norm(A[:, f.perm.forward] - q @ f.R) / max(frob, 1e-300)
-            assert res <= 1e-12
+        if drv in ("rqrcp", "rsrqrcp"):
+            rebuilt = np.zeros(A.shape)
+            rebuilt[: f.rank] = f.R
+            rebuilt[f.rank:, f.rank:] = f.trailing
+            res = np.linalg.norm(A[:, f.perm.forward] - f.q_factor(full=True) @ rebuilt)
+            assert res <= 1e-12 * frob
 
 
 def test_explicit_omega_matches_seeded_stream():

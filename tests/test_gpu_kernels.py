@@ -62,7 +62,9 @@ def test_select_pivots_matches_reference_fixtures():
                                       rec[f"{key}_swaps"], err_msg=key)
         scale = float(np.linalg.norm(B))
         assert np.linalg.norm(S.cpu().numpy() - rec[f"{key}_S"]) <= 1e-12 * scale, key
-        np.testing.assert_allclose(taus.cpu().numpy(), rec[f"{key}_taus"], rtol=1e-12, atol=1e-14)
+        # tau of a rounding-noise column is arbitrary in [1, 2]; compare where |beta| is significant
+        sig = np.abs(np.diag(rec[f"{key}_S"])[:got]) > 1e-8 * scale
+        np.testing.assert_allclose(taus.cpu().numpy()[sig], rec[f"{key}_taus"][sig], rtol=1e-12, atol=1e-14)
         assert l2 == int(rec[f"{key}_l2"]), key
     assert list(rec["diag_perm"][:4]) == [1, 3, 0, 2]
 
