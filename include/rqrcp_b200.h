@@ -169,6 +169,30 @@ int rq_q_columns(rq_handle_t h, int64_t m, int64_t nref, int64_t cols, const dou
 int rq_frob_norm(rq_handle_t h, const double* A, int64_t m, int64_t n, int64_t lda,
                  double* out, void* stream);
 
+/* ---------------------------------------------------------------- instrumentation */
+
+/* total kernel launches issued by this library since load (all handles) */
+int64_t rq_launch_count(void);
+
+/* kernel families timed by the profiler (CUDA events around each launch on
+ * its own stream); index order of rq_profile_read's arrays */
+#define RQ_PROF_SKETCH 0
+#define RQ_PROF_INNER 1
+#define RQ_PROF_UPDATE 2
+#define RQ_PROF_SMALL_GEMM 3
+#define RQ_PROF_SELECT 4
+#define RQ_PROF_PANEL 5
+#define RQ_PROF_SAMPLE_UPDATE 6
+#define RQ_PROF_SWAP 7
+#define RQ_PROF_MISC 8
+#define RQ_PROF_NUM 9
+
+int rq_profile_enable(rq_handle_t h, int on);
+int rq_profile_reset(rq_handle_t h);
+/* synchronises pending events; each array has RQ_PROF_NUM entries: launches,
+ * summed kernel milliseconds, algorithmic flops and algorithmic bytes */
+int rq_profile_read(rq_handle_t h, int64_t* launches, double* ms, double* flops, double* bytes);
+
 #ifdef __cplusplus
 }
 #endif

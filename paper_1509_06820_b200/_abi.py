@@ -68,7 +68,15 @@ SIGNATURES = {
                                 vp]),
     "rq_q_columns": (C.c_int, [vp, i64, i64, i64, dp, i64, dp, i64, dp, i64, vp]),
     "rq_frob_norm": (C.c_int, [vp, dp, i64, i64, i64, dp, vp]),
+    "rq_launch_count": (C.c_int64, []),
+    "rq_profile_enable": (C.c_int, [vp, C.c_int]),
+    "rq_profile_reset": (C.c_int, [vp]),
+    "rq_profile_read": (C.c_int, [vp, C.POINTER(i64), C.POINTER(f64), C.POINTER(f64),
+                                  C.POINTER(f64)]),
 }
+
+PROF_NAMES = ["sketch", "inner", "update", "small_gemm", "select", "panel", "sample_update",
+              "swap", "misc"]
 
 _lib = None
 _lock = threading.Lock()

@@ -245,4 +245,27 @@ int rq_frob_norm(rq_handle_t h, const double* A, int64_t m, int64_t n, int64_t l
   return guarded([&] { rq::frob_norm(H(h), A, m, n, lda, out, S(stream)); });
 }
 
+int64_t rq_launch_count(void) { return rq::launch_count(); }
+
+int rq_profile_enable(rq_handle_t h, int on) {
+  return guarded([&] { H(h).profiling = on != 0; });
+}
+
+int rq_profile_reset(rq_handle_t h) {
+  return guarded([&] { H(h).prof_reset(); });
+}
+
+int rq_profile_read(rq_handle_t h, int64_t* launches, double* ms, double* flops, double* bytes) {
+  return guarded([&] {
+    rq::Handle& hh = H(h);
+    hh.prof_collect();
+    for (int i = 0; i < rq::kProfNum; ++i) {
+      if (launches) launches[i] = hh.stats[i].launches;
+      if (ms) ms[i] = hh.stats[i].ms;
+      if (flops) flops[i] = hh.stats[i].flops;
+      if (bytes) bytes[i] = hh.stats[i].bytes;
+    }
+  });
+}
+
 }  // extern "C"

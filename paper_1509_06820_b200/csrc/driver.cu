@@ -90,7 +90,8 @@ void Factor::first_sample() {
     draw_omega(ell_, m_);
     om = om_d_;
   }
-  gemm(h_, false, false, ell_, n_, m_, 1.0, om, ell_, p_.work, p_.ldw, 0.0, B_, ell_, s_);
+  gemm(h_, false, false, ell_, n_, m_, 1.0, om, ell_, p_.work, p_.ldw, 0.0, B_, ell_, s_, nullptr,
+       kProfSketch);
   c_.gemm_flops += 2 * ell_ * m_ * n_;
   touch(c_, ell_ * m_ + m_ * n_ + ell_ * n_);
 }
@@ -101,13 +102,16 @@ void Factor::fresh_sample(int64_t i0) {
   const int64_t mm = m_ - i0, nt = n_ - i0;
   draw_omega(ell_, mm);
   const double* At = p_.work + i0 + i0 * p_.ldw;
-  gemm(h_, false, false, ell_, nt, mm, 1.0, om_d_, ell_, At, p_.ldw, 0.0, B_, ell_, s_);
+  gemm(h_, false, false, ell_, nt, mm, 1.0, om_d_, ell_, At, p_.ldw, 0.0, B_, ell_, s_, nullptr,
+       kProfSketch);
   c_.gemm_flops += 2 * ell_ * mm * nt;
   touch(c_, ell_ * mm + mm * nt + ell_ * nt);
   if (p_.truncated && i0) {
     // B -= (Omega Y[i0:, :i0]) W[i0:, :i0]^T
-    gemm(h_, false, false, ell_, i0, mm, 1.0, om_d_, ell_, p_.Y + i0, p_.ldy, 0.0, Z_, ell_, s_);
-    gemm(h_, false, true, ell_, nt, i0, -1.0, Z_, ell_, p_.W + i0, p_.ldW, 1.0, B_, ell_, s_);
+    gemm(h_, false, false, ell_, i0, mm, 1.0, om_d_, ell_, p_.Y + i0, p_.ldy, 0.0, Z_, ell_, s_,
+         nullptr, kProfSketch);
+    gemm(h_, false, true, ell_, nt, i0, -1.0, Z_, ell_, p_.W + i0, p_.ldW, 1.0, B_, ell_, s_,
+         nullptr, kProfSketch);
     c_.gemm_flops += 2 * ell_ * mm * i0 + 2 * ell_ * i0 * nt;
     touch(c_, mm * i0 + nt * i0);
   }
@@ -162,12 +166,13 @@ void Factor::stages(int64_t i0, int64_t bw, Counters& c) {
   const double* Yb = p_.Y + i0 + i0 * p_.ldy;
   if (!p_.truncated) {
     double* C = p_.work + i0 + (i0 + bw) * p_.ldw;
-    gemm(h_, true, false, bw, nt2, mm, 1.0, Yb, p_.ldy, C, p_.ldw, 0.0, G_, bw, s_, st_);
+    gemm(h_, true, false, bw, nt2, mm, 1.0, Yb, p_.ldy, C, p_.ldw, 0.0, G_, bw, s_, st_,
+         kProfInner);
     gemm(h_, true, false, bw, nt2, bw, 1.0, T_, b_, G_, bw, 0.0, X_, bw, s_, st_);
     c.gemm_flops += 2 * mm * bw * nt2 + bw * bw * nt2;
     const bool trail = p_.update_trailing && i0 + bw < m_;
     gemm(h_, false, false, trail ? mm : bw, nt2, bw, -1.0, Yb, p_.ldy, X_, bw, 1.0, C, p_.ldw, s_,
-         st_);
+         st_, kProfUpdate);
     c.gemm_flops += 2 * bw * bw * nt2;
     touch(c, mm * nt2 + mm * bw + bw * nt2);
     if (trail) {
@@ -178,7 +183,7 @@ void Factor::stages(int64_t i0, int64_t bw, Counters& c) {
   }
   // G = Yb^T A[i0:, i0+bw:] - (Yb^T Y[i0:, :i0]) W[i0+bw:, :i0]^T
   gemm(h_, true, false, bw, nt2, mm, 1.0, Yb, p_.ldy, p_.work + i0 + (i0 + bw) * p_.ldw, p_.ldw,
-       0.0, G_, bw, s_, st_);
+       0.0, G_, bw, s_, st_, kProfInner);
   c.gemm_flops += 2 * mm * bw * nt2;
   if (i0) {
     gemm(h_, true, false, bw, i0, mm, 1.0, Yb, p_.ldy, p_.Y + i0, p_.ldy, 0.0, Z_, bw, s_, st_);
@@ -511,54 +516,6 @@ TuxvResult run_tuxv(Handle& h, const TuxvParams& p) {
   RQ_CUDA(cudaStreamSynchronize(s));
   out.f.c = c;
   return out;
-}
-
-// ------------------------------------------------------------------ Handle
-Handle::Handle(int dev) : device(dev) {
-  RQ_CUDA(cudaSetDevice(dev));
-  RQ_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
-  int optin = 0;
-  RQ_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  smem_optin = (size_t)optin;
-}
-
-Handle::~Handle() {
-  for (auto& kv : bufs_) {
-    if (!kv.second.p) continue;
-    if (kv.second.pinned) cudaFreeHost(kv.second.p);
-    else cudaFree(kv.second.p);
-  }
-}
-
-void* Handle::buf(const std::string& name, size_t bytes, cudaStream_t s) {
-  Buf& b = bufs_[name];
-  if (bytes == 0) bytes = 8;
-  if (b.bytes < bytes) {
-    if (b.p) {
-      RQ_CUDA(cudaStreamSynchronize(s));
-      RQ_CUDA(cudaFree(b.p));
-      b.p = nullptr;
-    }
-    RQ_CUDA(cudaMalloc(&b.p, bytes));
-    b.bytes = bytes;
-  }
-  return b.p;
-}
-
-void* Handle::host_pinned(const std::string& name, size_t bytes, cudaStream_t s) {
-  Buf& b = bufs_["host:" + name];
-  if (bytes == 0) bytes = 8;
-  if (b.bytes < bytes) {
-    if (b.p) {
-      RQ_CUDA(cudaStreamSynchronize(s));
-      RQ_CUDA(cudaFreeHost(b.p));
-      b.p = nullptr;
-    }
-    RQ_CUDA(cudaMallocHost(&b.p, bytes));
-    b.bytes = bytes;
-    b.pinned = true;
-  }
-  return b.p;
 }
 
 }  // namespace rq

@@ -54,11 +54,13 @@ void launch_cfg(Handle& h, GemmArgs g, cudaStream_t s) {
   dim3 grid((unsigned)gm, (unsigned)gn, (unsigned)g.splits);
   kern<<<grid, Cfg::kThreads, Cfg::kSmem, s>>>(g);
   RQ_CHECK_LAUNCH();
+  count_launch();
   if (g.splits > 1) {
     const int64_t total = g.M * g.N;
     const int blocks = (int)std::min<int64_t>((total + 255) / 256, 8LL * h.num_sms);
     gemm_reduce_kernel<<<blocks, 256, 0, s>>>(g);
     RQ_CHECK_LAUNCH();
+    count_launch();
   }
 }
 
@@ -75,8 +77,11 @@ void launch_t(Handle& h, const GemmArgs& g, cudaStream_t s) {
 
 void gemm(Handle& h, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha,
           const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
-          int64_t ldc, cudaStream_t s, const Status* st) {
+          int64_t ldc, cudaStream_t s, const Status* st, int cat) {
   if (M <= 0 || N <= 0) return;
+  // algorithmic traffic: read A, B (+ C when beta != 0), write C
+  const double bytes = 8.0 * ((double)M * K + (double)K * N + (double)M * N * (beta != 0.0 ? 2 : 1));
+  ProfScope prof(h, cat, 2.0 * (double)M * N * K, bytes, s);
   GemmArgs g{};
   g.M = M; g.N = N; g.K = K;
   g.A = A; g.lda = lda; g.B = B; g.ldb = ldb; g.C = C; g.ldc = ldc;

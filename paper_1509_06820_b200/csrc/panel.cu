@@ -290,6 +290,8 @@ void panel_qr(Handle& h, int64_t mm, int64_t bw, const double* P, int64_t ldp,
     attr = std::max<size_t>(smem, 48 * 1024);
   }
   void* args[] = {&a};
+  ProfScope prof(h, kProfPanel, 2.0 * mm * bw * bw, 16.0 * mm * bw, s);
+  count_launch();
   RQ_CUDA(cudaLaunchCooperativeKernel((void*)panel_kernel, dim3(Q), dim3(kPanThreads), args,
                                       smem, s));
 }

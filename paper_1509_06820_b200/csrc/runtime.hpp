@@ -9,6 +9,7 @@
 #include <map>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 
@@ -34,6 +35,43 @@ struct InvalidArg : std::runtime_error {
   explicit InvalidArg(const std::string& m) : std::runtime_error(m) {}
 };
 
+// Kernel families timed by the optional in-driver profiler (bench.py reads
+// them through rq_profile_*): CUDA events bracket every launch of a family on
+// the stream it runs on.
+enum ProfCat {
+  kProfSketch = 0,   // B = Omega A (initial + resamples)
+  kProfInner,        // G = Y^T C (stage 1, split-K)
+  kProfUpdate,       // C -= Y X (stage 2/3: R12 rows + trailing update)
+  kProfSmallGemm,    // X = T^T G, TRQRCP/TUXV side products, Q formation
+  kProfSelect,       // pivot selection (cooperative)
+  kProfPanel,        // panel QR + T (cooperative)
+  kProfSampleUpd,    // sample update
+  kProfSwap,         // swap replay
+  kProfMisc,         // copies, norms, fills
+  kProfNum
+};
+struct ProfStat {
+  int64_t launches = 0;
+  double ms = 0.0, flops = 0.0, bytes = 0.0;
+};
+
+// total kernel launches issued by the library (all handles)
+void count_launch(int n = 1);
+int64_t launch_count();
+
+class Handle;
+// RAII timing scope (no-op unless profiling is enabled on the handle)
+class ProfScope {
+ public:
+  ProfScope(Handle& h, int cat, double flops, double bytes, cudaStream_t s);
+  ~ProfScope();
+
+ private:
+  Handle* h_;
+  int idx_ = -1;
+  cudaStream_t s_;
+};
+
 class Handle {
  public:
   explicit Handle(int device);
@@ -45,7 +83,23 @@ class Handle {
   void* buf(const std::string& name, size_t bytes, cudaStream_t s);
   void* host_pinned(const std::string& name, size_t bytes, cudaStream_t s);
 
+  // profiler
+  bool profiling = false;
+  ProfStat stats[kProfNum];
+  int prof_begin(int cat, double flops, double bytes, cudaStream_t s);
+  void prof_end(int idx, cudaStream_t s);
+  void prof_collect();  // synchronises the pending events into `stats`
+  void prof_reset();
+
  private:
+  struct PendEv {
+    int cat;
+    double flops, bytes;
+    cudaEvent_t a, b;
+  };
+  std::vector<PendEv> pend_;
+  std::vector<cudaEvent_t> free_ev_;
+  cudaEvent_t take_event();
   struct Buf {
     void* p = nullptr;
     size_t bytes = 0;
@@ -58,7 +112,7 @@ class Handle {
 // C = alpha * op(A) op(B) + beta * C on `s` (gemm.cu).  Column-major.
 void gemm(Handle& h, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha,
           const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
-          int64_t ldc, cudaStream_t s, const Status* st = nullptr);
+          int64_t ldc, cudaStream_t s, const Status* st = nullptr, int cat = kProfSmallGemm);
 
 // ------------------------------------------------------------------ kernels (small.cu, select.cu, panel.cu)
 struct SelectOut {

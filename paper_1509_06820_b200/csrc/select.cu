@@ -360,6 +360,8 @@ void select_pivots(Handle& h, int64_t ell, int64_t nt, int64_t want, const doubl
     attr = std::max<size_t>(smem, 48 * 1024);
   }
   void* args[] = {&a};
+  ProfScope prof(h, kProfSelect, 4.0 * ell * nt * want, 16.0 * ell * nt, s);
+  count_launch();
   RQ_CUDA(cudaLaunchCooperativeKernel((void*)select_kernel, dim3(P), dim3(kSelThreads), args,
                                       smem, s));
 }

@@ -250,6 +250,8 @@ void sample_update(Handle& h, int64_t ell, int64_t b, int64_t n2, const double* 
   }
   if (smem > h.smem_optin) throw InvalidArg("sample update block too wide");
   const int blocks = (int)std::max<int64_t>(1, (n2 + kSuThreads - 1) / kSuThreads);
+  ProfScope prof(h, kProfSampleUpd, 3.0 * b * b * n2, 8.0 * (2 * ell * n2 + b * b), s);
+  count_launch();
   sample_update_kernel<<<blocks, kSuThreads, smem, s>>>(
       (int)ell, (int)b, n2, S, lds, R11, R12, ldr, kEps34 * frob, Bnew, ldb, st,
       abort_on_degenerate ? 1 : 0, i0);
@@ -261,6 +263,8 @@ void apply_swaps(Handle& h, const int64_t* piv, int64_t got_max, int64_t i0,
   (void)got_max;
   const int64_t mx = std::max<int64_t>(std::max<int64_t>(t.m, 1), std::max<int64_t>(t.Wf ? t.wf_cols : 0, t.Rf ? t.rf_rows : 0));
   dim3 grid((unsigned)grid_for(mx, h.num_sms), 4);
+  ProfScope prof(h, kProfSwap, 0.0, 32.0 * got_max * t.m, s);
+  count_launch();
   swap_kernel<<<grid, 256, 0, s>>>(piv, i0, t, st, t.m);
   RQ_CHECK_LAUNCH();
 }
@@ -270,8 +274,10 @@ void frob_norm(Handle& h, const double* A, int64_t m, int64_t n, int64_t lda, do
   double* part = (double*)h.buf("frob_part", kNormBlocks * 8, s);
   sumsq_partial_kernel<<<kNormBlocks, kNormThreads, 0, s>>>(A, m, n, lda, part);
   RQ_CHECK_LAUNCH();
+  count_launch();
   sumsq_final_kernel<<<1, 32, 0, s>>>(part, out);
   RQ_CHECK_LAUNCH();
+  count_launch();
 }
 
 void copy2d(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows,
@@ -279,18 +285,21 @@ void copy2d(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t ro
   if (rows <= 0 || cols <= 0) return;
   copy2d_kernel<<<grid_for(rows * cols, 148), 256, 0, s>>>(src, lds, dst, ldd, rows, cols, st);
   RQ_CHECK_LAUNCH();
+  count_launch();
 }
 
 void fill2d(double* dst, int64_t ldd, int64_t rows, int64_t cols, double v, cudaStream_t s) {
   if (rows <= 0 || cols <= 0) return;
   fill2d_kernel<<<grid_for(rows * cols, 148), 256, 0, s>>>(dst, ldd, rows, cols, v);
   RQ_CHECK_LAUNCH();
+  count_launch();
 }
 
 void set_identity(double* dst, int64_t ldd, int64_t rows, int64_t cols, cudaStream_t s) {
   if (rows <= 0 || cols <= 0) return;
   identity_kernel<<<grid_for(rows * cols, 148), 256, 0, s>>>(dst, ldd, rows, cols);
   RQ_CHECK_LAUNCH();
+  count_launch();
 }
 
 void transpose(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows,
@@ -299,6 +308,7 @@ void transpose(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t
   dim3 grid((unsigned)((rows + 31) / 32), (unsigned)((cols + 31) / 32));
   transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(src, lds, dst, ldd, rows, cols);
   RQ_CHECK_LAUNCH();
+  count_launch();
 }
 
 void scatter_cols(const double* src, int64_t lds, const int64_t* perm, double* dst,
@@ -307,6 +317,7 @@ void scatter_cols(const double* src, int64_t lds, const int64_t* perm, double* d
   scatter_cols_kernel<<<grid_for(rows * cols, 148), 256, 0, s>>>(src, lds, perm, dst, ldd,
                                                                   rows, cols);
   RQ_CHECK_LAUNCH();
+  count_launch();
 }
 
 void t_factor(Handle& h, const double* Y, int64_t ldy, int64_t mm, int64_t nb,
@@ -320,6 +331,7 @@ void t_factor(Handle& h, const double* Y, int64_t ldy, int64_t mm, int64_t nb,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   t_recurrence_kernel<<<1, 256, smem, s>>>(G, nb, tau, (int)nb, T, ldt);
   RQ_CHECK_LAUNCH();
+  count_launch();
 }
 
 }  // namespace rq
