@@ -62,29 +62,34 @@ __global__ void __launch_bounds__(kPanThreads, 1) panel_kernel(PanArgs a) {
   double* rowj = dsum + bw;                // [bw]
   double* wsh = rowj + bw;                 // [bw]
   double* taus = wsh + bw;                 // [bw]
-  double* betas = taus + bw;               // [bw]
+  double* tvrow = taus + bw;               // [rpb]  tau * v_r for my rows
+  double* xnext = tvrow + a.rpb;           // [rpb]  updated column j+1
   __shared__ double s_sc[4];
   __shared__ int s_usable;
   unsigned int epoch = 0;
   const int stride = 2 * bw;
+  const int64_t ncols = imin64(bw, a.mm);
 
-  // load my row slab (column-major, ld = ldl)
-  for (int c = 0; c < bw; ++c)
-    for (int r = tid; r < nrow; r += kPanThreads)
+  // ---- load my row slab (coalesced down each column, many loads in flight)
+  {
+    const int total = nrow * bw;
+#pragma unroll 8
+    for (int e = tid; e < total; e += kPanThreads) {
+      const int c = e / nrow, r = e - c * nrow;
       loc[(size_t)c * ldl + r] = a.P[(size_t)c * a.ldp + r0 + r];
-  if (tid == 0) s_usable = bw;
+    }
+  }
+  if (tid == 0) s_usable = (int)ncols;
   __syncthreads();
 
-  // partials of column jn over my rows r > jn, plus row jn if I own it
-  auto publish = [&](int jn) {
-    const int par = jn & 1;
-    double* out = a.pub + ((size_t)par * Q + me) * stride;
-    const double* xcol = loc + (size_t)jn * ldl;
+  // publish the partials of column jn over my rows r > jn (+ row jn if owned)
+  auto publish = [&](int jn, const double* xc) {
+    double* out = a.pub + ((size_t)(jn & 1) * Q + me) * stride;
     const int rstart = (int)imax64(0, (int64_t)jn + 1 - r0);
     for (int c = jn + tc; c < bw; c += cs) {
       const double* col = loc + (size_t)c * ldl;
       double d = 0.0;
-      for (int r = rstart + tg; r < nrow; r += groups) d = __fma_rn(xcol[r], col[r], d);
+      for (int r = rstart + tg; r < nrow; r += groups) d = __fma_rn(xc[r], col[r], d);
       part[tg * bw + c] = d;
     }
     __syncthreads();
@@ -98,24 +103,35 @@ __global__ void __launch_bounds__(kPanThreads, 1) panel_kernel(PanArgs a) {
       const int lr = (int)(jn - r0);
       for (int c = jn + tid; c < bw; c += kPanThreads) out[bw + c] = loc[(size_t)c * ldl + lr];
     }
-    __syncthreads();
   };
 
-  const int64_t ncols = imin64(bw, a.mm);
   int64_t l2 = 0, l2b = 0;
-  if (ncols > 0) publish(0);
+  if (ncols > 0) publish(0, loc);
   for (int j = 0; j < ncols; ++j) {
     grid_barrier(a.bar, epoch);
-    const int par = j & 1;
+    const double* pb = a.pub + (size_t)(j & 1) * Q * stride;
     const int owner = (int)(j / a.rpb);
-    // reduce partials in fixed q order (identical in every CTA)
-    for (int c = j + tid; c < bw; c += kPanThreads) {
-      double d = 0.0;
-      for (int q = 0; q < Q; ++q) d = __dadd_rn(d, a.pub[((size_t)par * Q + q) * stride + c]);
-      dsum[c] = d;
-      rowj[c] = a.pub[((size_t)par * Q + owner) * stride + bw + c];
+    // (1) reduce the Q partials: thread (c, g) sums its q-chunk in order,
+    //     then the chunks are combined in order (identical in every CTA)
+    {
+      const int qlo = (int)((int64_t)tg * Q / groups), qhi = (int)((int64_t)(tg + 1) * Q / groups);
+      for (int c = j + tc; c < bw; c += cs) {
+        double d = 0.0;
+#pragma unroll 8
+        for (int q = qlo; q < qhi; ++q) d = __dadd_rn(d, pb[(size_t)q * stride + c]);
+        part[tg * bw + c] = d;
+        if (tg == 0) rowj[c] = pb[(size_t)owner * stride + bw + c];
+      }
     }
     __syncthreads();
+    if (tg == 0)
+      for (int c = j + tc; c < bw; c += cs) {
+        double d = part[c];
+        for (int g = 1; g < groups; ++g) d = __dadd_rn(d, part[g * bw + c]);
+        dsum[c] = d;
+      }
+    __syncthreads();
+    // (2) reflector scalars (kernels.py:35-44), identical in every CTA
     if (tid == 0) {
       const double alpha = rowj[j];
       const double norm = sqrt(__fma_rn(alpha, alpha, dsum[j]));
@@ -127,8 +143,7 @@ __global__ void __launch_bounds__(kPanThreads, 1) panel_kernel(PanArgs a) {
       }
       s_sc[0] = beta; s_sc[1] = tau; s_sc[2] = den; s_sc[3] = norm;
       taus[j] = tau;
-      betas[j] = beta;
-      if (s_usable == bw && fabs(beta) <= a.tol) s_usable = j;  // _panel_rank
+      if (s_usable == ncols && fabs(beta) <= a.tol) s_usable = j;  // _panel_rank
       if (me == 0) {
         const int64_t cols = bw - j - 1;
         if (tau != 0.0 && cols > 0) {
@@ -138,35 +153,68 @@ __global__ void __launch_bounds__(kPanThreads, 1) panel_kernel(PanArgs a) {
       }
     }
     __syncthreads();
-    const double tau = s_sc[1], den = s_sc[2];
+    const double beta = s_sc[0], tau = s_sc[1], den = s_sc[2];
     const bool zero = s_sc[3] == 0.0;
-    // w_c = v^T P[:,c] = P[j,c] + (sum_{r>j} x_r P[r,c]) / (alpha - beta)
+    // (3) w_c = v^T P[:,c] = P[j,c] + (sum_{r>j} x_r P[r,c]) / (alpha - beta);
+    //     v_r = x_r / (alpha - beta) once per row (kernels.py:42), column j
+    //     becomes beta on the diagonal and v below it
     for (int c = j + 1 + tid; c < bw; c += kPanThreads)
       wsh[c] = zero ? rowj[c] : __dadd_rn(rowj[c], __ddiv_rn(dsum[c], den));
-    __syncthreads();
-    const double* xcol = loc + (size_t)j * ldl;
     const int rj = (int)imax64(0, (int64_t)j - r0);  // first local row >= j
-    if (tau != 0.0) {
-      for (int c = j + 1 + tc; c < bw; c += cs) {
-        double* col = loc + (size_t)c * ldl;
-        const double w = wsh[c];
-        for (int r = rj + tg; r < nrow; r += groups) {
-          const int64_t gr = r0 + r;
-          const double v = (gr == j) ? 1.0 : __ddiv_rn(xcol[r], den);
-          col[r] = __dsub_rn(col[r], __dmul_rn(__dmul_rn(tau, v), w));
-        }
+    {
+      double* xj = loc + (size_t)j * ldl;
+      for (int r = rj + tid; r < nrow; r += kPanThreads) {
+        const bool diag = r0 + r == j;
+        const double v = diag ? 1.0 : (zero ? xj[r] : __ddiv_rn(xj[r], den));
+        tvrow[r] = __dmul_rn(tau, v);
+        xj[r] = diag ? beta : v;
       }
     }
     __syncthreads();
-    // column j: beta on the diagonal, v below it (scaled reflector)
-    for (int r = rj + tid; r < nrow; r += kPanThreads) {
-      const int64_t gr = r0 + r;
-      double* x = loc + (size_t)j * ldl + r;
-      if (gr == j) *x = s_sc[0];
-      else if (!zero) *x = __ddiv_rn(*x, den);
+    const bool more = j + 1 < ncols;
+    // (4) updated column j+1 first (it feeds the next partials)
+    if (more) {
+      const double w1 = wsh[j + 1];
+      double* x1 = loc + (size_t)(j + 1) * ldl;
+      for (int r = rj + tid; r < nrow; r += kPanThreads) {
+        const double nv = tau != 0.0 ? __dsub_rn(x1[r], __dmul_rn(tvrow[r], w1)) : x1[r];
+        x1[r] = nv;
+        xnext[r] = nv;
+      }
     }
     __syncthreads();
-    if (j + 1 < ncols) publish(j + 1);
+    // (5) fused trailing update of columns > j+1 and the partials of step j+1
+    if (more) {
+      const int rs1 = (int)imax64(0, (int64_t)j + 2 - r0);  // rows > j+1
+      for (int c = j + 1 + tc; c < bw; c += cs) {
+        double* col = loc + (size_t)c * ldl;
+        double d = 0.0;
+        if (c == j + 1) {
+          for (int r = rs1 + tg; r < nrow; r += groups) d = __fma_rn(xnext[r], xnext[r], d);
+        } else {
+          const double w = wsh[c];
+          for (int r = rj + tg; r < nrow; r += groups) {
+            const double nv = tau != 0.0 ? __dsub_rn(col[r], __dmul_rn(tvrow[r], w)) : col[r];
+            col[r] = nv;
+            if (r >= rs1) d = __fma_rn(xnext[r], nv, d);
+          }
+        }
+        part[tg * bw + c] = d;
+      }
+      __syncthreads();
+      double* out = a.pub + ((size_t)((j + 1) & 1) * Q + me) * stride;
+      if (tg == 0)
+        for (int c = j + 1 + tc; c < bw; c += cs) {
+          double d = part[c];
+          for (int g = 1; g < groups; ++g) d = __dadd_rn(d, part[g * bw + c]);
+          out[c] = d;
+        }
+      if (j + 1 >= r0 && j + 1 < r0 + nrow) {
+        const int lr = (int)(j + 1 - r0);
+        for (int c = j + 1 + tid; c < bw; c += kPanThreads) out[bw + c] = loc[(size_t)c * ldl + lr];
+      }
+    }
+    __syncthreads();
   }
 
   // ---- commit
@@ -186,8 +234,11 @@ __global__ void __launch_bounds__(kPanThreads, 1) panel_kernel(PanArgs a) {
     }
   }
   if (ncommit == 0) return;  // uniform across the grid
-  for (int c = 0; c < ncommit; ++c) {
-    for (int r = tid; r < nrow; r += kPanThreads) {
+  {
+    const int total = nrow * ncommit;
+#pragma unroll 4
+    for (int e = tid; e < total; e += kPanThreads) {
+      const int c = e / nrow, r = e - c * nrow;
       const int64_t gr = r0 + r;
       const double val = loc[(size_t)c * ldl + r];
       a.Y[(size_t)c * a.ldy + gr] = gr < c ? 0.0 : (gr == c ? 1.0 : val);
@@ -198,58 +249,63 @@ __global__ void __launch_bounds__(kPanThreads, 1) panel_kernel(PanArgs a) {
     for (int c = tid; c < ncommit; c += kPanThreads) a.tau[c] = taus[c];
   if (a.T == nullptr) return;
 
-  // ---- T factor (kernels.py:139-147): G = Y^T Y (strict upper), then the
-  // forward column recurrence T[:j,j] = -tau_j T[:j,:j] G[:j,j]
+  // ---- T factor (kernels.py:139-147): G = Y^T Y (strict upper) from the
+  // per-CTA partials, then T[:j,j] = -tau_j T[:j,:j] G[:j,j]
   const int nc = ncommit;
-  double* gq = a.gram + (size_t)me * bw * bw;
-  for (int e = tid; e < nc * nc; e += kPanThreads) {
-    const int i = e % nc, j = e / nc;
-    if (i >= j) continue;
-    double g = 0.0;
+  const int npair = nc * (nc - 1) / 2;
+  double* gq = a.gram + (size_t)me * npair;
+  for (int e = tid; e < npair; e += kPanThreads) {
+    // pair index e -> (i, j), i < j, column-major over the strict upper triangle
+    int j = (int)((1.0 + sqrt(1.0 + 8.0 * e)) * 0.5);
+    while (j * (j - 1) / 2 > e) --j;
+    while ((j + 1) * j / 2 <= e) ++j;
+    const int i = e - j * (j - 1) / 2;
     const int rs = (int)imax64(0, (int64_t)j - r0);  // rows >= j carry both
+    const double* yi = loc + (size_t)i * ldl;
+    const double* yj = loc + (size_t)j * ldl;
+    double g = 0.0;
     for (int r = rs; r < nrow; ++r) {
-      const int64_t gr = r0 + r;
-      const double yi = gr == i ? 1.0 : loc[(size_t)i * ldl + r];
-      const double yj = gr == j ? 1.0 : loc[(size_t)j * ldl + r];
-      g = __fma_rn(yi, yj, g);
+      const double vj = (r0 + r == j) ? 1.0 : yj[r];
+      g = __fma_rn(yi[r], vj, g);
     }
-    gq[i + (size_t)j * bw] = g;
+    gq[e] = g;
   }
   grid_barrier(a.bar, epoch);
-  double* gfin = a.gram + (size_t)Q * bw * bw;
+  double* gfin = a.gram + (size_t)Q * npair;
   {
-    const int total = nc * nc;
-    const int per = (total + Q - 1) / Q;
-    for (int e = me * per + tid; e < min(total, (me + 1) * per); e += kPanThreads) {
-      const int i = e % nc, j = e / nc;
-      if (i >= j) continue;
+    const int per = (npair + Q - 1) / Q;
+    const int lo = me * per, hi = min(npair, lo + per);
+    for (int e = lo + tid; e < hi; e += kPanThreads) {
       double g = 0.0;
-      for (int q = 0; q < Q; ++q) g = __dadd_rn(g, a.gram[(size_t)q * bw * bw + i + (size_t)j * bw]);
-      gfin[i + (size_t)j * bw] = g;
+#pragma unroll 8
+      for (int q = 0; q < Q; ++q) g = __dadd_rn(g, a.gram[(size_t)q * npair + e]);
+      gfin[e] = g;
     }
   }
   grid_barrier(a.bar, epoch);
   if (me != 0) return;
-  double* Tsh = part;  // reuse: [bw*bw] would not fit for big bw; write T directly
-  (void)Tsh;
+  const bool tsm = a.use_smem && ldl >= nc;
+  double* Tw = tsm ? loc : a.T;          // T workspace, column-major
+  const int ldtw = tsm ? ldl : (int)a.ldt;
+  for (int e = tid; e < nc * nc; e += kPanThreads) Tw[(e % nc) + (size_t)(e / nc) * ldtw] = 0.0;
+  __syncthreads();
   for (int j = 0; j < nc; ++j) {
-    // T[:j, j] = -tau_j * (T[:j,:j] @ g), g = G[:j, j]
+    const double* gcol = gfin + j * (j - 1) / 2;  // G[0:j, j]
     for (int i = tid; i < j; i += kPanThreads) {
       double t = 0.0;
-      for (int l = i; l < j; ++l)
-        t = __fma_rn(a.T[i + (size_t)l * a.ldt], gfin[l + (size_t)j * bw], t);
+      for (int l = i; l < j; ++l) t = __fma_rn(Tw[i + (size_t)l * ldtw], gcol[l], t);
       wsh[i] = t;
     }
     __syncthreads();
-    for (int i = tid; i < nc; i += kPanThreads) {
-      double v;
-      if (i < j) v = __dmul_rn(-taus[j], wsh[i]);
-      else if (i == j) v = taus[j];
-      else v = 0.0;
-      a.T[i + (size_t)j * a.ldt] = v;
-    }
+    for (int i = tid; i < j; i += kPanThreads) Tw[i + (size_t)j * ldtw] = __dmul_rn(-taus[j], wsh[i]);
+    if (tid == 0) Tw[j + (size_t)j * ldtw] = taus[j];
     __syncthreads();
   }
+  if (tsm)
+    for (int e = tid; e < nc * nc; e += kPanThreads) {
+      const int i = e % nc, j = e / nc;
+      a.T[i + (size_t)j * a.ldt] = Tw[i + (size_t)j * ldtw];
+    }
 }
 
 }  // namespace
@@ -267,7 +323,7 @@ void panel_qr(Handle& h, int64_t mm, int64_t bw, const double* P, int64_t ldp,
   while (cs < bw && cs < kPanThreads) cs <<= 1;
   const int groups = kPanThreads / cs;
   const int ldl = rpb | 1;
-  const size_t aux = ((size_t)groups * bw + 5 * (size_t)bw + 8) * 8;
+  const size_t aux = ((size_t)groups * bw + 5 * (size_t)bw + 2 * (size_t)rpb + 8) * 8;
   const size_t store = (size_t)ldl * bw * 8;
   const bool use_smem = store + aux <= h.smem_optin - 2048;
   const size_t smem = (use_smem ? store : 0) + aux;
@@ -279,7 +335,7 @@ void panel_qr(Handle& h, int64_t mm, int64_t bw, const double* P, int64_t ldp,
   a.st = st;
   a.bar = (unsigned int*)h.buf("pan_bar", 64, s);
   a.pub = (double*)h.buf("pan_pub", (size_t)2 * Q * 2 * bw * 8, s);
-  a.gram = out.T ? (double*)h.buf("pan_gram", (size_t)(Q + 1) * bw * bw * 8, s) : nullptr;
+  a.gram = out.T ? (double*)h.buf("pan_gram", (size_t)(Q + 1) * bw * bw * 4 + 64, s) : nullptr;
   a.gstore = use_smem ? nullptr : (double*)h.buf("pan_gstore", (size_t)Q * rpb * bw * 8, s);
   a.rpb = rpb; a.ldl = use_smem ? ldl : rpb; a.use_smem = use_smem ? 1 : 0; a.cs = cs;
   RQ_CUDA(cudaMemsetAsync(a.bar, 0, 64, s));

@@ -44,7 +44,8 @@ struct SelArgs {
 
 struct Cand {
   double val;
-  int pos;
+  int pos;   // logical position (tie-break: lowest wins)
+  int idx;   // local column (publish) or owner CTA (global reduce)
 };
 RQ_DEV bool better(const Cand& a, const Cand& b) {
   return a.val > b.val || (a.val == b.val && a.pos < b.pos);
@@ -55,6 +56,7 @@ RQ_DEV Cand warp_best(Cand c) {
     Cand o;
     o.val = __shfl_xor_sync(0xffffffffu, c.val, off);
     o.pos = __shfl_xor_sync(0xffffffffu, c.pos, off);
+    o.idx = __shfl_xor_sync(0xffffffffu, c.idx, off);
     if (better(o, c)) c = o;
   }
   return c;
@@ -64,12 +66,23 @@ RQ_DEV double warp_sum(double v) {
   for (int off = 16; off; off >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
   return v;
 }
+// sum over an aligned group of 8 lanes; every lane of the group gets the same value
+RQ_DEV double group8_sum(double v, unsigned mask) {
+#pragma unroll
+  for (int off = 4; off; off >>= 1) v = __dadd_rn(v, __shfl_xor_sync(mask, v, off, 8));
+  return v;
+}
+
+constexpr int kNoPos = 0x7fffffff;
 
 __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
   if (aborted(a.st)) return;
   extern __shared__ __align__(16) double sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = kSelThreads / 32;
+  constexpr int NG = kSelThreads / 8;  // 8-lane column groups
+  const int grp = tid >> 3, gl = tid & 7;
+  const unsigned gmask = 0xffu << (lane & 24);  // the 8 lanes of my group
   const int P = gridDim.x, me = blockIdx.x;
   const int ell = a.ell, ldl = a.ldl;
   const int c0 = me * a.cpb;
@@ -79,24 +92,27 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
   double* meta = a.use_smem ? sm + (size_t)a.cpb * ldl : sm;
   double* nrm = meta;                 // [cpb]
   double* orig = nrm + a.cpb;         // [cpb]
-  double* xb = orig + a.cpb;          // [ell] winner column
+  double* xb = orig + a.cpb;          // [ell] pivot column
   double* vb = xb + ell;              // [ell] v
   double* tvb = vb + ell;             // [ell] tau*v
-  double* wv = tvb + ell;             // [NW] scratch
+  double* wv = tvb + ell;             // [NW + 8] scratch
   int* pos = (int*)(wv + NW + 8);     // [cpb]
-  int* redpos = pos + a.cpb;          // [NW]
-  double* redval = wv;                // reuse [NW]
+  __shared__ Cand s_red[NW];
   __shared__ double s_sc[8];
-  __shared__ int s_ic[8];
-  __shared__ int s_lc[2];      // local column of the candidate published per parity
-  __shared__ int s_owner[NW];
+  __shared__ Cand s_win;
+  __shared__ int s_lc[2];             // local column of the candidate published per parity
+  __shared__ double s_sq[160];
 
   unsigned int epoch = 0;
 
   // ---- load my columns, initial norms (pairwise, bit-identical to numpy)
-  for (int e = tid; e < ncol * ell; e += kSelThreads) {
-    const int c = e / ell, i = e % ell;
-    store[(size_t)c * ldl + i] = a.B[(size_t)(c0 + c) * a.ldb + i];
+  {
+    const int total = ncol * ell;
+#pragma unroll 4
+    for (int e = tid; e < total; e += kSelThreads) {
+      const int c = e / ell, i = e - c * ell;
+      store[(size_t)c * ldl + i] = a.B[(size_t)(c0 + c) * a.ldb + i];
+    }
   }
   __syncthreads();
   double mysq = 0.0;  // fixed-order per-thread partial of ||B||_F^2
@@ -108,7 +124,6 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
     pos[c] = c0 + c;
     mysq = __dadd_rn(mysq, sq);
   }
-  // CTA partial of ||B||^2 (fixed tree) -> pubsq
   {
     double v = warp_sum(mysq);
     if (lane == 0) wv[warp] = v;
@@ -118,52 +133,46 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
       for (int w = 0; w < NW; ++w) t = __dadd_rn(t, wv[w]);
       a.pubsq[me] = t;
     }
-    __syncthreads();
   }
 
-  // local argmax over active columns with position >= jstart; publishes the
-  // candidate (value, position, column data) into parity slot `par`
+  // local argmax over active columns (position >= jstart); publishes the
+  // candidate (value, position) and its column into parity slot `par`
   auto publish = [&](int jstart, int par) {
-    Cand best{-1.0, 0x7fffffff};
+    Cand best{-1.0, kNoPos, -1};
     for (int c = tid; c < ncol; c += kSelThreads) {
       if (pos[c] >= jstart) {
-        Cand cc{nrm[c], pos[c]};
+        Cand cc{nrm[c], pos[c], c};
         if (better(cc, best)) best = cc;
       }
     }
     best = warp_best(best);
-    if (lane == 0) { redval[warp] = best.val; redpos[warp] = best.pos; }
+    if (lane == 0) s_red[warp] = best;
     __syncthreads();
-    if (tid == 0) {
-      Cand b{-1.0, 0x7fffffff};
-      for (int w = 0; w < NW; ++w) {
-        Cand cc{redval[w], redpos[w]};
-        if (better(cc, b)) b = cc;
+    if (warp == 0) {
+      Cand b = lane < NW ? s_red[lane] : Cand{-1.0, kNoPos, -1};
+      b = warp_best(b);
+      if (lane == 0) {
+        s_lc[par] = b.idx;
+        a.pubval[par * P + me] = b.val;
+        a.pubpos[par * P + me] = b.pos;
       }
-      int lc = -1;
-      if (b.pos != 0x7fffffff)
-        for (int c = 0; c < ncol; ++c)
-          if (pos[c] == b.pos) { lc = c; break; }
-      s_ic[0] = lc;
-      s_lc[par] = lc;
-      a.pubval[par * P + me] = b.val;
-      a.pubpos[par * P + me] = b.pos;
     }
     __syncthreads();
-    const int lc = s_ic[0];
+    const int lc = s_lc[par];
     if (lc >= 0)
       for (int i = tid; i < ell; i += kSelThreads)
         a.pubcol[((size_t)par * P + me) * ell + i] = store[(size_t)lc * ldl + i];
-    __syncthreads();
   };
 
   publish(0, 0);
   grid_barrier(a.bar, epoch);
 
-  // tol = eps * ||B||_F  (randomized.py:98)
+  // tol = eps * ||B||_F  (randomized.py:98), same summation order everywhere
+  for (int q = tid; q < P; q += kSelThreads) s_sq[q] = a.pubsq[q];
+  __syncthreads();
   if (tid == 0) {
     double t = 0.0;
-    for (int q = 0; q < P; ++q) t = __dadd_rn(t, a.pubsq[q]);
+    for (int q = 0; q < P; ++q) t = __dadd_rn(t, s_sq[q]);
     s_sc[0] = kEps * sqrt(t);
   }
   __syncthreads();
@@ -173,52 +182,36 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
   int64_t l2 = 0, l2b = 0;
   for (int j = 0; j < a.want; ++j) {
     const int par = j & 1;
-    // ---- global argmax over the P candidates (order independent)
+    // ---- global argmax over the P candidates (total order -> identical everywhere)
     {
-      Cand best{-1.0, 0x7fffffff};
-      int bq = -1;
+      Cand best{-1.0, kNoPos, -1};
       for (int q = tid; q < P; q += kSelThreads) {
-        Cand cc{a.pubval[par * P + q], a.pubpos[par * P + q]};
-        if (cc.pos != 0x7fffffff && better(cc, best)) { best = cc; bq = q; }
+        Cand cc{a.pubval[par * P + q], a.pubpos[par * P + q], q};
+        if (cc.pos != kNoPos && better(cc, best)) best = cc;
       }
-      Cand w = warp_best(best);
-      // owner of the warp winner
-      const unsigned hit = __ballot_sync(0xffffffffu, best.pos == w.pos && bq >= 0);
-      int wq = __shfl_sync(0xffffffffu, bq, hit ? __ffs(hit) - 1 : 0);
-      if (lane == 0) {
-        redval[warp] = w.val;
-        redpos[warp] = w.pos;
-        s_owner[warp] = hit ? wq : -1;
-      }
+      best = warp_best(best);
+      if (lane == 0) s_red[warp] = best;
       __syncthreads();
-      if (tid == 0) {
-        Cand b{-1.0, 0x7fffffff};
-        int bo = -1;
-        for (int ww = 0; ww < NW; ++ww) {
-          Cand cc{redval[ww], redpos[ww]};
-          if (s_owner[ww] >= 0 && better(cc, b)) { b = cc; bo = s_owner[ww]; }
-        }
-        s_sc[1] = b.val;
-        s_ic[0] = b.pos;
-        s_ic[1] = bo;
+      if (warp == 0) {
+        Cand b = lane < NW ? s_red[lane] : Cand{-1.0, kNoPos, -1};
+        b = warp_best(b);
+        if (lane == 0) s_win = b;
       }
       __syncthreads();
     }
-    const double bval = s_sc[1];
-    const int p = s_ic[0], owner = s_ic[1];
-    if (owner < 0 || !(bval > tol)) {  // max trailing norm <= tol: halt (qrcp.py:69-71)
+    const Cand win = s_win;
+    const int p = win.pos, owner = win.idx;
+    if (owner < 0 || !(win.val > tol)) {  // max trailing norm <= tol: halt (qrcp.py:69-71)
       got = j;
       break;
     }
     // ---- fetch the pivot column, relabel positions (swap j <-> p)
     for (int i = tid; i < ell; i += kSelThreads)
       xb[i] = a.pubcol[((size_t)par * P + owner) * ell + i];
-    // the pivot column's local index was recorded when it was published
     const int lc_piv = s_lc[par];
-    for (int c = tid; c < ncol; c += kSelThreads) {
+    for (int c = tid; c < ncol; c += kSelThreads)
       if (pos[c] == j && p != j) pos[c] = p;
-    }
-    __syncthreads();  // xb complete before warp 0 forms the reflector
+    __syncthreads();
     // ---- reflector from x[j:] (kernels.py:26-44), identical in every CTA
     if (warp == 0) {
       double sq = 0.0;
@@ -244,58 +237,53 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
       vb[i] = v;
       tvb[i] = __dmul_rn(tau, v);
     }
-    __syncthreads();
     if (owner == me) {
-      const int lc = lc_piv;
-      if (tid == 0) pos[lc] = j;
+      if (tid == 0) pos[lc_piv] = j;
       // pivot column: rows < j keep R, row j = beta, below = 0 (qrcp.py:80-81)
       for (int i = j + tid; i < ell; i += kSelThreads)
-        store[(size_t)lc * ldl + i] = (i == j) ? beta : 0.0;
+        store[(size_t)lc_piv * ldl + i] = (i == j) ? beta : 0.0;
     }
-    if (me == 0) {
-      if (tid == 0) {
-        a.piv[j] = p;
-        if (a.taus) a.taus[j] = tau;
-        const int64_t cols = (int64_t)a.nt - j - 1;
-        if (tau != 0.0 && cols > 0) {
-          l2 += 4LL * (ell - j) * cols;
-          l2b += 16LL * (ell - j) * cols;
-        }
+    if (me == 0 && tid == 0) {
+      a.piv[j] = p;
+      if (a.taus) a.taus[j] = tau;
+      const int64_t cols = (int64_t)a.nt - j - 1;
+      if (tau != 0.0 && cols > 0) {
+        l2 += 4LL * (ell - j) * cols;
+        l2b += 16LL * (ell - j) * cols;
       }
-      if (a.Ys)
-        for (int i = tid; i < ell; i += kSelThreads)
-          a.Ys[(size_t)j * a.ldys + i] = i < j ? 0.0 : vb[i];
     }
     __syncthreads();
-    // ---- apply H_j to my active columns (pos > j), then downdate
-    for (int c = warp; c < ncol; c += NW) {
-      if (pos[c] <= j) continue;
+    if (me == 0 && a.Ys)
+      for (int i = tid; i < ell; i += kSelThreads)
+        a.Ys[(size_t)j * a.ldys + i] = i < j ? 0.0 : vb[i];
+    // ---- apply H_j to my active columns (pos > j) and downdate their norms;
+    //      one 8-lane group per column
+    for (int c = grp; c < ncol; c += NG) {
+      if (pos[c] <= j) continue;  // uniform within the group
       double* col = store + (size_t)c * ldl;
       if (tau != 0.0) {
         double d = 0.0;
-        for (int i = j + lane; i < ell; i += 32) d = __fma_rn(vb[i], col[i], d);
-        const double w = warp_sum(d);
-        for (int i = j + lane; i < ell; i += 32) col[i] = __dsub_rn(col[i], __dmul_rn(tvb[i], w));
+        for (int i = j + gl; i < ell; i += 8) d = __fma_rn(vb[i], col[i], d);
+        const double w = group8_sum(d, gmask);
+        for (int i = j + gl; i < ell; i += 8) col[i] = __dsub_rn(col[i], __dmul_rn(tvb[i], w));
       }
-      __syncwarp();
       if (j + 1 < a.nt) {
         // NormTracker.downdate with row j of the updated sample (kernels.py:222-233)
+        __syncwarp(gmask);
         const double row = col[j];
         const double nv = nrm[c];
         double nsq = __dsub_rn(__dmul_rn(nv, nv), __dmul_rn(row, row));
         nsq = nsq > 0.0 ? nsq : 0.0;
-        const bool unsafe = nsq < __dmul_rn(kGuard, orig[c]);
-        if (!unsafe) {
-          if (lane == 0) nrm[c] = sqrt(nsq);
+        if (!(nsq < __dmul_rn(kGuard, orig[c]))) {
+          if (gl == 0) nrm[c] = sqrt(nsq);
         } else {
           double sq = 0.0;
-          for (int i = j + 1 + lane; i < ell; i += 32) sq = __fma_rn(col[i], col[i], sq);
-          sq = warp_sum(sq);
+          for (int i = j + 1 + gl; i < ell; i += 8) sq = __fma_rn(col[i], col[i], sq);
+          sq = group8_sum(sq, gmask);
           const double fresh = sqrt(sq);
-          if (lane == 0) { nrm[c] = fresh; orig[c] = __dmul_rn(fresh, fresh); }
+          if (gl == 0) { nrm[c] = fresh; orig[c] = __dmul_rn(fresh, fresh); }
         }
       }
-      __syncwarp();
     }
     __syncthreads();
     publish(j + 1, par ^ 1);
@@ -303,9 +291,12 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
   }
 
   // ---- write the transformed sample in pivoted order
-  for (int e = tid; e < ncol * ell; e += kSelThreads) {
-    const int c = e / ell, i = e % ell;
-    a.S[(size_t)pos[c] * a.lds + i] = store[(size_t)c * ldl + i];
+  {
+    const int total = ncol * ell;
+    for (int e = tid; e < total; e += kSelThreads) {
+      const int c = e / ell, i = e - c * ell;
+      a.S[(size_t)pos[c] * a.lds + i] = store[(size_t)c * ldl + i];
+    }
   }
   if (me == 0 && tid == 0) {
     a.st->got = got;
@@ -334,6 +325,7 @@ void select_pivots(Handle& h, int64_t ell, int64_t nt, int64_t want, const doubl
   P = (int)((nt + cpb - 1) / cpb);
   const int ldl = (int)(ell | 1);
   const size_t meta = (size_t)(2 * cpb + 3 * ell + 8 + 8) * 8 + (size_t)(cpb + 8) * 4 + 64;
+  if (P > 160) throw InvalidArg("select: too many CTAs");
   const size_t store = (size_t)cpb * ldl * 8;
   const bool use_smem = store + meta <= h.smem_optin - 2048;
   const size_t smem = (use_smem ? store : 0) + meta;

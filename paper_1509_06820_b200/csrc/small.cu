@@ -68,61 +68,101 @@ __global__ void __launch_bounds__(kSuThreads) sample_update_kernel(
   for (int i = b; i < ell; ++i) out[i] = s12[i];
 }
 
+// Register-resident variant for b in {16, 32, 64}: thread per column, the
+// solve vector lives in registers, R11 and S11 are staged in shared memory
+// (broadcast reads).  X = R11^{-1} R12 by back substitution with the
+// reciprocal diagonal (OpenBLAS dtrsm, behind np.linalg.solve, also scales by
+// the inverted diagonal), then B1 = S12 - S11 X.
+template <int B>
+__global__ void __launch_bounds__(128) sample_update_reg_kernel(
+    int ell, int64_t n2, const double* __restrict__ S, int64_t lds,
+    const double* __restrict__ R11, const double* __restrict__ R12, int64_t ldr, double thresh,
+    double* __restrict__ Bn, int64_t ldb, Status* st, int abort_on_degenerate, int64_t i0) {
+  if (aborted(st)) return;
+  extern __shared__ __align__(16) double dyn[];
+  double* r11 = dyn;              // r11[l + i*B] = R11[l, i]
+  double* s11 = dyn + B * B;      // s11[i + l*B] = S11[i, l]
+  double* rinv = dyn + 2 * B * B;
+  __shared__ int s_bad;
+  const int tid = threadIdx.x;
+  if (tid == 0) s_bad = 0;
+  __syncthreads();
+  for (int j = tid; j < B; j += blockDim.x) {
+    const double d = R11[j + (size_t)j * ldr];
+    if (fabs(d) < thresh) s_bad = 1;
+    rinv[j] = 1.0 / d;
+  }
+  for (int e = tid; e < B * B; e += blockDim.x) {
+    const int i = e % B, l = e / B;
+    r11[e] = R11[i + (size_t)l * ldr];
+    s11[e] = S[i + (size_t)l * lds];
+  }
+  __syncthreads();
+  if (s_bad) {
+    if (blockIdx.x == 0 && tid == 0) {
+      st->degenerate = 1;
+      if (abort_on_degenerate) {
+        st->abort_i0 = i0;
+        __threadfence();
+        st->abort = kAbortDegenerate;
+      }
+    }
+    return;
+  }
+  if (blockIdx.x == 0 && tid == 0) st->degenerate = 0;
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + tid;
+  if (c >= n2) return;
+  double x[B];
+  const double* rc = R12 + (size_t)c * ldr;
+#pragma unroll
+  for (int i = 0; i < B; ++i) x[i] = rc[i];
+#pragma unroll
+  for (int i = B - 1; i >= 0; --i) {
+    x[i] = __dmul_rn(x[i], rinv[i]);
+#pragma unroll
+    for (int l = 0; l < i; ++l) x[l] = __fma_rn(-r11[l + i * B], x[i], x[l]);
+  }
+  const double* s12 = S + (size_t)(B + c) * lds;
+  double* out = Bn + (size_t)c * ldb;
+#pragma unroll
+  for (int i = 0; i < B; ++i) {
+    double acc = 0.0;
+#pragma unroll
+    for (int l = i; l < B; ++l) acc = __fma_rn(s11[i + l * B], x[l], acc);
+    out[i] = __dsub_rn(s12[i], acc);
+  }
+  for (int i = B; i < ell; ++i) out[i] = s12[i];
+}
+
 // ---------------------------------------------------------------- K6
-__global__ void swap_kernel(const int64_t* __restrict__ piv, int64_t i0, SwapTargets t,
-                            Status* st, int64_t m_rows) {
+// Swap replay as a permutation gather: the ordered swaps (i0+j, i0+piv[j])
+// (randomized.py:138-147) only touch positions {j} U {piv[j]}; the plan
+// kernel replays them on a position->source map (and on perm + the swap log),
+// then every touched column is gathered into scratch and scattered back, each
+// row/column in parallel.  Equivalent to the sequential swaps.
+__global__ void swap_plan_kernel(const int64_t* __restrict__ piv, int64_t i0, SwapTargets t,
+                                 Status* st, int* idx, int* plan_src) {
   if (aborted(st)) return;
   const int got = (int)st->got;
-  const int which = blockIdx.y;
-  if (which == 0) {  // full columns of work (R rows included)
-    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < t.m;
-         r += (int64_t)gridDim.x * blockDim.x) {
-      for (int j = 0; j < got; ++j) {
-        const int64_t ga = i0 + j, gc = i0 + piv[j];
-        if (ga == gc) continue;
-        double* pa = t.work + r + ga * t.ldw;
-        double* pc = t.work + r + gc * t.ldw;
-        const double va = *pa;
-        *pa = *pc;
-        *pc = va;
-      }
-    }
-  } else if (which == 1 && t.Wf) {  // W rows follow A's columns
-    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < t.wf_cols;
-         c += (int64_t)gridDim.x * blockDim.x) {
-      for (int j = 0; j < got; ++j) {
-        const int64_t ga = i0 + j, gc = i0 + piv[j];
-        if (ga == gc) continue;
-        double* pa = t.Wf + ga + c * t.ldwf;
-        double* pc = t.Wf + gc + c * t.ldwf;
-        const double va = *pa;
-        *pa = *pc;
-        *pc = va;
-      }
-    }
-  } else if (which == 2 && t.Rf) {  // R columns (R.T rows)
-    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < t.rf_rows;
-         r += (int64_t)gridDim.x * blockDim.x) {
-      for (int j = 0; j < got; ++j) {
-        const int64_t ga = i0 + j, gc = i0 + piv[j];
-        if (ga == gc) continue;
-        double* pa = t.Rf + r + ga * t.ldrf;
-        double* pc = t.Rf + r + gc * t.ldrf;
-        const double va = *pa;
-        *pa = *pc;
-        *pc = va;
-      }
-    }
-  } else if (which == 3 && blockIdx.x == 0 && threadIdx.x == 0) {  // perm + swap log
+  for (int e = threadIdx.x; e < got; e += blockDim.x) {
+    idx[e] = e;
+    idx[piv[e]] = (int)piv[e];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
     int64_t n = st->nswaps;
     for (int j = 0; j < got; ++j) {
-      const int64_t ga = i0 + j, gc = i0 + piv[j];
+      const int p = (int)piv[j];
+      const int64_t ga = i0 + j, gc = i0 + p;
       if (n < t.log_cap) {
         t.log[2 * n] = ga;
         t.log[2 * n + 1] = gc;
       }
       ++n;
-      if (ga != gc) {
+      if (p != j) {
+        const int tmp = idx[j];
+        idx[j] = idx[p];
+        idx[p] = tmp;
         const int64_t v = t.perm[ga];
         t.perm[ga] = t.perm[gc];
         t.perm[gc] = v;
@@ -130,6 +170,43 @@ __global__ void swap_kernel(const int64_t* __restrict__ piv, int64_t i0, SwapTar
     }
     st->nswaps = n;
   }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 2 * got; e += blockDim.x) {
+    const int q = e < got ? e : (int)piv[e - got];
+    const int src = idx[q];
+    // a position listed twice (as some j and as some piv[k]) is moved once
+    const bool dup = e >= got && q < got;
+    plan_src[e] = (src == q || dup) ? -1 : src;
+  }
+}
+
+__global__ void swap_move_kernel(const int64_t* __restrict__ piv, int64_t i0, SwapTargets t,
+                                 const Status* st, const int* __restrict__ plan_src,
+                                 double* scratch, int64_t ldsc, double* wsc, double* rsc,
+                                 int to_scratch) {
+  if (aborted(st)) return;
+  const int got = (int)st->got;
+  const int e = blockIdx.y;
+  if (e >= 2 * got) return;
+  const int src = plan_src[e];
+  if (src < 0) return;
+  const int q = e < got ? e : (int)piv[e - got];
+  const int64_t col = i0 + (to_scratch ? src : q);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < t.m; r += stride) {
+    if (to_scratch) scratch[r + e * ldsc] = t.work[r + col * t.ldw];
+    else t.work[r + col * t.ldw] = scratch[r + e * ldsc];
+  }
+  if (t.Wf)
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < t.wf_cols; c += stride) {
+      if (to_scratch) wsc[c + e * t.wf_cols] = t.Wf[col + c * t.ldwf];
+      else t.Wf[col + c * t.ldwf] = wsc[c + e * t.wf_cols];
+    }
+  if (t.Rf)
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < t.rf_rows; r += stride) {
+      if (to_scratch) rsc[r + e * t.rf_rows] = t.Rf[r + col * t.ldrf];
+      else t.Rf[r + col * t.ldrf] = rsc[r + e * t.rf_rows];
+    }
 }
 
 // ---------------------------------------------------------------- K10
@@ -240,6 +317,31 @@ void sample_update(Handle& h, int64_t ell, int64_t b, int64_t n2, const double* 
                    const double* R11, const double* R12, int64_t ldr, double frob,
                    double* Bnew, int64_t ldb, Status* st, bool abort_on_degenerate, int64_t i0,
                    cudaStream_t s) {
+  if (b == 16 || b == 32 || b == 64) {
+    const int blocks = (int)std::max<int64_t>(1, (n2 + 127) / 128);
+    ProfScope prof(h, kProfSampleUpd, 3.0 * b * b * n2, 8.0 * (2 * ell * n2 + b * b), s);
+    count_launch();
+    const double th = kEps34 * frob;
+    const int ab = abort_on_degenerate ? 1 : 0;
+    const size_t dsm = (size_t)(2 * b * b + b) * 8;
+    static bool attr64 = false;
+    if (!attr64) {
+      RQ_CUDA(cudaFuncSetAttribute(sample_update_reg_kernel<64>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024));
+      attr64 = true;
+    }
+    if (b == 16)
+      sample_update_reg_kernel<16><<<blocks, 128, dsm, s>>>((int)ell, n2, S, lds, R11, R12, ldr,
+                                                            th, Bnew, ldb, st, ab, i0);
+    else if (b == 32)
+      sample_update_reg_kernel<32><<<blocks, 128, dsm, s>>>((int)ell, n2, S, lds, R11, R12, ldr,
+                                                            th, Bnew, ldb, st, ab, i0);
+    else
+      sample_update_reg_kernel<64><<<blocks, 128, dsm, s>>>((int)ell, n2, S, lds, R11, R12, ldr,
+                                                            th, Bnew, ldb, st, ab, i0);
+    RQ_CHECK_LAUNCH();
+    return;
+  }
   const size_t smem = ((size_t)b * b + (size_t)b * kSuThreads) * 8;
   static size_t attr = 0;
   if (smem > attr) {
@@ -260,13 +362,26 @@ void sample_update(Handle& h, int64_t ell, int64_t b, int64_t n2, const double* 
 
 void apply_swaps(Handle& h, const int64_t* piv, int64_t got_max, int64_t i0,
                  const SwapTargets& t, Status* st, cudaStream_t s) {
-  (void)got_max;
-  const int64_t mx = std::max<int64_t>(std::max<int64_t>(t.m, 1), std::max<int64_t>(t.Wf ? t.wf_cols : 0, t.Rf ? t.rf_rows : 0));
-  dim3 grid((unsigned)grid_for(mx, h.num_sms), 4);
+  const int64_t ne = 2 * got_max;
+  int* plan = (int*)h.buf("swap_plan", (size_t)ne * 4 + 64, s);
+  double* sc = (double*)h.buf("swap_scratch", (size_t)ne * t.m * 8 + 64, s);
+  double* wsc = t.Wf ? (double*)h.buf("swap_wsc", (size_t)ne * t.wf_cols * 8 + 64, s) : nullptr;
+  double* rsc = t.Rf ? (double*)h.buf("swap_rsc", (size_t)ne * t.rf_rows * 8 + 64, s) : nullptr;
   ProfScope prof(h, kProfSwap, 0.0, 32.0 * got_max * t.m, s);
-  count_launch();
-  swap_kernel<<<grid, 256, 0, s>>>(piv, i0, t, st, t.m);
+  // position -> source map over the trailing columns (only touched entries
+  // are ever read); sized for n - i0 <= 2^22 columns
+  int* pmap = (int*)h.buf("swap_pmap", (size_t)4 << 22, s);
+  swap_plan_kernel<<<1, 256, 0, s>>>(piv, i0, t, st, pmap, plan);
   RQ_CHECK_LAUNCH();
+  const int64_t mx = std::max<int64_t>(std::max<int64_t>(t.m, 1),
+                                       std::max<int64_t>(t.Wf ? t.wf_cols : 0, t.Rf ? t.rf_rows : 0));
+  const unsigned gx = (unsigned)std::min<int64_t>((mx + 255) / 256, 64);
+  dim3 grid(gx, (unsigned)ne);
+  swap_move_kernel<<<grid, 256, 0, s>>>(piv, i0, t, st, plan, sc, t.m, wsc, rsc, 1);
+  RQ_CHECK_LAUNCH();
+  swap_move_kernel<<<grid, 256, 0, s>>>(piv, i0, t, st, plan, sc, t.m, wsc, rsc, 0);
+  RQ_CHECK_LAUNCH();
+  count_launch(3);
 }
 
 void frob_norm(Handle& h, const double* A, int64_t m, int64_t n, int64_t lda, double* out,
