@@ -141,42 +141,54 @@ __global__ void __launch_bounds__(128) sample_update_reg_kernel(
 // then every touched column is gathered into scratch and scattered back, each
 // row/column in parallel.  Equivalent to the sequential swaps.
 __global__ void swap_plan_kernel(const int64_t* __restrict__ piv, int64_t i0, SwapTargets t,
-                                 Status* st, int* idx, int* plan_src) {
+                                 Status* st, int* plan_src) {
   if (aborted(st)) return;
   const int got = (int)st->got;
+  extern __shared__ int ssw[];
+  int* pv = ssw;               // [got]      piv
+  int* slotb = pv + got;       // [got]      slot of position piv[j]
+  int* src = slotb + got;      // [2 got]    source position currently at each slot
+  // slots: position q < got -> slot q; position q >= got -> got + (first k with piv[k] == q)
+  for (int e = threadIdx.x; e < got; e += blockDim.x) pv[e] = (int)piv[e];
+  __syncthreads();
   for (int e = threadIdx.x; e < got; e += blockDim.x) {
-    idx[e] = e;
-    idx[piv[e]] = (int)piv[e];
+    const int q = pv[e];
+    int sl;
+    if (q < got) {
+      sl = q;
+    } else {
+      int k = e;
+      for (int kk = 0; kk < e; ++kk)
+        if (pv[kk] == q) { k = kk; break; }
+      sl = got + k;
+    }
+    slotb[e] = sl;
+    src[e] = e;
+    src[got + e] = q;
+    if (st->nswaps + e < t.log_cap) {  // swap log: stores only
+      t.log[2 * (st->nswaps + e)] = i0 + e;
+      t.log[2 * (st->nswaps + e) + 1] = i0 + q;
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    int64_t n = st->nswaps;
     for (int j = 0; j < got; ++j) {
-      const int p = (int)piv[j];
-      const int64_t ga = i0 + j, gc = i0 + p;
-      if (n < t.log_cap) {
-        t.log[2 * n] = ga;
-        t.log[2 * n + 1] = gc;
-      }
-      ++n;
-      if (p != j) {
-        const int tmp = idx[j];
-        idx[j] = idx[p];
-        idx[p] = tmp;
-        const int64_t v = t.perm[ga];
-        t.perm[ga] = t.perm[gc];
-        t.perm[gc] = v;
+      const int b = slotb[j];
+      if (b != j) {
+        const int tmp = src[j];
+        src[j] = src[b];
+        src[b] = tmp;
       }
     }
-    st->nswaps = n;
+    st->nswaps += got;
   }
   __syncthreads();
   for (int e = threadIdx.x; e < 2 * got; e += blockDim.x) {
-    const int q = e < got ? e : (int)piv[e - got];
-    const int src = idx[q];
-    // a position listed twice (as some j and as some piv[k]) is moved once
-    const bool dup = e >= got && q < got;
-    plan_src[e] = (src == q || dup) ? -1 : src;
+    // slot e holds position q(e); duplicate slots (got + k whose position is
+    // < got, or not the first occurrence) are never used -> -1
+    const int q = e < got ? e : pv[e - got];
+    const bool live = e < got || (q >= got && slotb[e - got] == e);
+    plan_src[e] = (live && src[e] != q) ? src[e] : -1;
   }
 }
 
@@ -196,6 +208,10 @@ __global__ void swap_move_kernel(const int64_t* __restrict__ piv, int64_t i0, Sw
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < t.m; r += stride) {
     if (to_scratch) scratch[r + e * ldsc] = t.work[r + col * t.ldw];
     else t.work[r + col * t.ldw] = scratch[r + e * ldsc];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // Permutation.forward follows the columns
+    if (to_scratch) ((int64_t*)(scratch + 2 * got * ldsc))[e] = t.perm[col];
+    else t.perm[col] = ((const int64_t*)(scratch + 2 * got * ldsc))[e];
   }
   if (t.Wf)
     for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < t.wf_cols; c += stride) {
@@ -364,14 +380,11 @@ void apply_swaps(Handle& h, const int64_t* piv, int64_t got_max, int64_t i0,
                  const SwapTargets& t, Status* st, cudaStream_t s) {
   const int64_t ne = 2 * got_max;
   int* plan = (int*)h.buf("swap_plan", (size_t)ne * 4 + 64, s);
-  double* sc = (double*)h.buf("swap_scratch", (size_t)ne * t.m * 8 + 64, s);
+  double* sc = (double*)h.buf("swap_scratch", (size_t)ne * t.m * 8 + (size_t)ne * 8 + 64, s);
   double* wsc = t.Wf ? (double*)h.buf("swap_wsc", (size_t)ne * t.wf_cols * 8 + 64, s) : nullptr;
   double* rsc = t.Rf ? (double*)h.buf("swap_rsc", (size_t)ne * t.rf_rows * 8 + 64, s) : nullptr;
   ProfScope prof(h, kProfSwap, 0.0, 32.0 * got_max * t.m, s);
-  // position -> source map over the trailing columns (only touched entries
-  // are ever read); sized for n - i0 <= 2^22 columns
-  int* pmap = (int*)h.buf("swap_pmap", (size_t)4 << 22, s);
-  swap_plan_kernel<<<1, 256, 0, s>>>(piv, i0, t, st, pmap, plan);
+  swap_plan_kernel<<<1, 256, (size_t)4 * got_max * 4, s>>>(piv, i0, t, st, plan);
   RQ_CHECK_LAUNCH();
   const int64_t mx = std::max<int64_t>(std::max<int64_t>(t.m, 1),
                                        std::max<int64_t>(t.Wf ? t.wf_cols : 0, t.Rf ? t.rf_rows : 0));
