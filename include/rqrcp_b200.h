@@ -171,6 +171,11 @@ int rq_frob_norm(rq_handle_t h, const double* A, int64_t m, int64_t n, int64_t l
 
 /* ---------------------------------------------------------------- instrumentation */
 
+/* tuning knobs: "force_select" / "force_panel" (0 = size heuristic, 1 = grid
+ * cooperative variant, 2 = single-cluster variant), "select_cluster_max_cols",
+ * "panel_cluster_max_rows" (size thresholds of the heuristic) */
+int rq_set_option(rq_handle_t h, const char* name, int64_t value);
+
 /* total kernel launches issued by this library since load (all handles) */
 int64_t rq_launch_count(void);
 

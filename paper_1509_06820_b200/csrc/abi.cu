@@ -247,6 +247,19 @@ int rq_frob_norm(rq_handle_t h, const double* A, int64_t m, int64_t n, int64_t l
 
 int64_t rq_launch_count(void) { return rq::launch_count(); }
 
+int rq_set_option(rq_handle_t h, const char* name, int64_t value) {
+  return guarded([&] {
+    need(name != nullptr, "null option name");
+    rq::Handle& hh = H(h);
+    const std::string n(name);
+    if (n == "force_select") hh.force_select = (int)value;
+    else if (n == "force_panel") hh.force_panel = (int)value;
+    else if (n == "select_cluster_max_cols") hh.select_cluster_max_cols = value;
+    else if (n == "panel_cluster_max_rows") hh.panel_cluster_max_rows = value;
+    else throw rq::InvalidArg("unknown option " + n);
+  });
+}
+
 int rq_profile_enable(rq_handle_t h, int on) {
   return guarded([&] { H(h).profiling = on != 0; });
 }

@@ -83,6 +83,13 @@ class Handle {
   void* buf(const std::string& name, size_t bytes, cudaStream_t s);
   void* host_pinned(const std::string& name, size_t bytes, cudaStream_t s);
 
+  // kernel-variant overrides (0 = size heuristic, 1 = grid, 2 = cluster)
+  int force_select = 0, force_panel = 0;
+  // size heuristics: cluster variant when the work per step is small enough
+  // (crossovers measured on B200: tools/variant_sweep.py, profiles/r01_variant_sweep.jsonl)
+  int64_t select_cluster_max_cols = 1024;   // nt threshold
+  int64_t panel_cluster_max_rows = 3072;    // mm threshold (bw <= 64 only)
+
   // profiler
   bool profiling = false;
   ProfStat stats[kProfNum];
@@ -127,6 +134,11 @@ void select_pivots(Handle& h, int64_t ell, int64_t nt, int64_t want, const doubl
                    int64_t ldb, const SelectOut& out, Status* st, bool abort_on_short,
                    int64_t i0, cudaStream_t s);
 
+// grid-cooperative variant (all SMs, one grid barrier per step) for wide samples
+void select_pivots_grid(Handle& h, int64_t ell, int64_t nt, int64_t want, const double* B,
+                        int64_t ldb, const SelectOut& out, Status* st, bool abort_on_short,
+                        int64_t i0, cudaStream_t s);
+
 struct PanelOut {
   double* Rdst; int64_t ldr; int64_t rrows;   // transformed panel rows [0, rrows)
   double* Y; int64_t ldy;                      // unit lower reflectors (mm x bw)
@@ -141,6 +153,10 @@ enum PanelPolicy { kPanelCommitIfFull = 0, kPanelCommitUsable = 1, kPanelCommitA
 void panel_qr(Handle& h, int64_t mm, int64_t bw, const double* P, int64_t ldp,
               const PanelOut& out, double tol, PanelPolicy policy, bool raise_abort, Status* st,
               int64_t i0, cudaStream_t s);
+
+void panel_qr_grid(Handle& h, int64_t mm, int64_t bw, const double* P, int64_t ldp,
+                   const PanelOut& out, double tol, PanelPolicy policy, bool raise_abort,
+                   Status* st, int64_t i0, cudaStream_t s);
 
 // B_new = [S12 - S11 R11^{-1} R12; S22] (randomized.py:107-135).  Writes
 // Status.degenerate; with abort_on_degenerate also sets Status.abort.

@@ -1,27 +1,21 @@
-// K4: pivot-block selection = `want` greedy steps of column-pivoted
+// K4 (grid variant, wide samples): pivot-block selection = `want` greedy steps of column-pivoted
 // Householder QR on the small (b+p) x nt Gaussian sample, in one persistent
 // cooperative kernel (randomized.py:85-104 -> qrcp.py:63-84, NormTracker
 // kernels.py:196-233, form/apply_reflector kernels.py:26-56).
 //
-// Layout: the sample's columns are dealt out to the P <= 16 CTAs of ONE
-// thread-block cluster in contiguous chunks and stay resident in shared
-// memory (columns beyond the shared-memory budget spill to global/L2).
-// Columns never move: a swap only relabels logical positions, so a step costs
-// one cluster barrier (~0.23 us on B200):
-//   publish local best (norm, position) + that column's data in own smem
-//   -> cluster barrier -> every CTA reads the P candidates over DSMEM and
-//      reduces them identically
+// Layout: the sample's columns are dealt out to P CTAs in contiguous chunks
+// and stay resident in shared memory (global/L2 fallback when a chunk does
+// not fit).  Columns never move: a swap only relabels logical positions, so
+// a step costs one grid barrier:
+//   publish local best (norm, position) + that column's data
+//   -> barrier -> every CTA reduces the P candidates identically
 //   -> forms the reflector redundantly (bit-identical in every CTA)
 //   -> applies it to its own active columns, downdates their norms with the
 //      sqrt(eps) recompute guard, and publishes its next candidate.
 // Ties break to the lowest logical position (np.argmax first-max semantics).
 // Initial norms use numpy's pairwise summation, so they are bit-identical to
 // np.linalg.norm(B, axis=0).
-#include <cooperative_groups.h>
-
 #include "runtime.hpp"
-
-namespace cg = cooperative_groups;
 
 namespace rq {
 
@@ -29,9 +23,7 @@ namespace {
 
 constexpr int kSelThreads = 256;
 
-constexpr int kMaxCluster = 16;
-
-struct SelArgs {
+struct SelGridArgs {
   int ell, nt, want;
   int abort_on_short;
   int64_t i0;
@@ -41,8 +33,13 @@ struct SelArgs {
   double* Ys; int64_t ldys;
   double* taus;
   Status* st;
-  double* gstore;   // spill columns [P][cpb - ncs][ldl]
-  int cpb, ldl, ncs;
+  unsigned int* bar;
+  double* pubval;   // [2][P]
+  int* pubpos;      // [2][P]
+  double* pubcol;   // [2][P][ell]
+  double* pubsq;    // [P]
+  double* gstore;   // fallback column store
+  int cpb, ldl, use_smem;
 };
 
 struct Cand {
@@ -78,39 +75,35 @@ RQ_DEV double group8_sum(double v, unsigned mask) {
 
 constexpr int kNoPos = 0x7fffffff;
 
-__global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
+__global__ void __launch_bounds__(kSelThreads, 1) select_grid_kernel(SelGridArgs a) {
   if (aborted(a.st)) return;
-  cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(16) double sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = kSelThreads / 32;
   constexpr int NG = kSelThreads / 8;  // 8-lane column groups
   const int grp = tid >> 3, gl = tid & 7;
   const unsigned gmask = 0xffu << (lane & 24);  // the 8 lanes of my group
-  const int P = (int)cluster.num_blocks(), me = (int)cluster.block_rank();
-  const int ell = a.ell, ldl = a.ldl, ncs = a.ncs;
+  const int P = gridDim.x, me = blockIdx.x;
+  const int ell = a.ell, ldl = a.ldl;
   const int c0 = me * a.cpb;
   const int ncol = max(0, min(a.nt - c0, a.cpb));
-  double* gsp = a.gstore ? a.gstore + (size_t)me * (a.cpb - ncs) * ldl : nullptr;
-  auto colp = [&](int c) -> double* {
-    return c < ncs ? sm + (size_t)c * ldl : gsp + (size_t)(c - ncs) * ldl;
-  };
-  double* meta = sm + (size_t)ncs * ldl;
+
+  double* store = a.use_smem ? sm : a.gstore + (size_t)me * a.cpb * ldl;
+  double* meta = a.use_smem ? sm + (size_t)a.cpb * ldl : sm;
   double* nrm = meta;                 // [cpb]
   double* orig = nrm + a.cpb;         // [cpb]
   double* xb = orig + a.cpb;          // [ell] pivot column
   double* vb = xb + ell;              // [ell] v
   double* tvb = vb + ell;             // [ell] tau*v
-  double* ccol = tvb + ell;           // [2][ell] published candidate column (DSMEM)
-  double* wv = ccol + 2 * ell;        // [NW + 8] scratch
+  double* wv = tvb + ell;             // [NW + 8] scratch
   int* pos = (int*)(wv + NW + 8);     // [cpb]
   __shared__ Cand s_red[NW];
   __shared__ double s_sc[8];
   __shared__ Cand s_win;
-  __shared__ int s_lc[2];             // local column of the published candidate
-  __shared__ double s_cval[2];        // published candidate (DSMEM)
-  __shared__ int s_cpos[2];
-  __shared__ double s_sq;             // published ||B_local||^2 (DSMEM)
+  __shared__ int s_lc[2];             // local column of the candidate published per parity
+  __shared__ double s_sq[160];
+
+  unsigned int epoch = 0;
 
   // ---- load my columns, initial norms (pairwise, bit-identical to numpy)
   {
@@ -118,13 +111,13 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
 #pragma unroll 4
     for (int e = tid; e < total; e += kSelThreads) {
       const int c = e / ell, i = e - c * ell;
-      colp(c)[i] = a.B[(size_t)(c0 + c) * a.ldb + i];
+      store[(size_t)c * ldl + i] = a.B[(size_t)(c0 + c) * a.ldb + i];
     }
   }
   __syncthreads();
   double mysq = 0.0;  // fixed-order per-thread partial of ||B||_F^2
   for (int c = tid; c < ncol; c += kSelThreads) {
-    const double sq = pairwise_sumsq(colp(c), ell, 1);
+    const double sq = pairwise_sumsq(store + (size_t)c * ldl, ell, 1);
     const double nv = sqrt(sq);
     nrm[c] = nv;
     orig[c] = __dmul_rn(nv, nv);
@@ -138,7 +131,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
     if (tid == 0) {
       double t = 0.0;
       for (int w = 0; w < NW; ++w) t = __dadd_rn(t, wv[w]);
-      s_sq = t;
+      a.pubsq[me] = t;
     }
   }
 
@@ -160,25 +153,26 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
       b = warp_best(b);
       if (lane == 0) {
         s_lc[par] = b.idx;
-        s_cval[par] = b.val;
-        s_cpos[par] = b.pos;
+        a.pubval[par * P + me] = b.val;
+        a.pubpos[par * P + me] = b.pos;
       }
     }
     __syncthreads();
     const int lc = s_lc[par];
-    if (lc >= 0) {
-      const double* src = colp(lc);
-      for (int i = tid; i < ell; i += kSelThreads) ccol[par * ell + i] = src[i];
-    }
+    if (lc >= 0)
+      for (int i = tid; i < ell; i += kSelThreads)
+        a.pubcol[((size_t)par * P + me) * ell + i] = store[(size_t)lc * ldl + i];
   };
 
   publish(0, 0);
-  cluster.sync();
+  grid_barrier(a.bar, epoch);
 
   // tol = eps * ||B||_F  (randomized.py:98), same summation order everywhere
+  for (int q = tid; q < P; q += kSelThreads) s_sq[q] = a.pubsq[q];
+  __syncthreads();
   if (tid == 0) {
     double t = 0.0;
-    for (int q = 0; q < P; ++q) t = __dadd_rn(t, *cluster.map_shared_rank(&s_sq, q));
+    for (int q = 0; q < P; ++q) t = __dadd_rn(t, s_sq[q]);
     s_sc[0] = kEps * sqrt(t);
   }
   __syncthreads();
@@ -188,29 +182,32 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
   int64_t l2 = 0, l2b = 0;
   for (int j = 0; j < a.want; ++j) {
     const int par = j & 1;
-    // ---- cluster-wide argmax over the P candidates (total order -> identical everywhere)
-    if (warp == 0) {
-      Cand b{-1.0, kNoPos, -1};
-      if (lane < P) {
-        const double v = cluster.map_shared_rank(s_cval, lane)[par];
-        const int p = cluster.map_shared_rank(s_cpos, lane)[par];
-        if (p != kNoPos) b = Cand{v, p, lane};
+    // ---- global argmax over the P candidates (total order -> identical everywhere)
+    {
+      Cand best{-1.0, kNoPos, -1};
+      for (int q = tid; q < P; q += kSelThreads) {
+        Cand cc{a.pubval[par * P + q], a.pubpos[par * P + q], q};
+        if (cc.pos != kNoPos && better(cc, best)) best = cc;
       }
-      b = warp_best(b);
-      if (lane == 0) s_win = b;
+      best = warp_best(best);
+      if (lane == 0) s_red[warp] = best;
+      __syncthreads();
+      if (warp == 0) {
+        Cand b = lane < NW ? s_red[lane] : Cand{-1.0, kNoPos, -1};
+        b = warp_best(b);
+        if (lane == 0) s_win = b;
+      }
+      __syncthreads();
     }
-    __syncthreads();
     const Cand win = s_win;
     const int p = win.pos, owner = win.idx;
     if (owner < 0 || !(win.val > tol)) {  // max trailing norm <= tol: halt (qrcp.py:69-71)
       got = j;
       break;
     }
-    // ---- fetch the pivot column over DSMEM, relabel positions (swap j <-> p)
-    {
-      const double* oc = cluster.map_shared_rank(ccol, owner) + par * ell;
-      for (int i = tid; i < ell; i += kSelThreads) xb[i] = oc[i];
-    }
+    // ---- fetch the pivot column, relabel positions (swap j <-> p)
+    for (int i = tid; i < ell; i += kSelThreads)
+      xb[i] = a.pubcol[((size_t)par * P + owner) * ell + i];
     const int lc_piv = s_lc[par];
     for (int c = tid; c < ncol; c += kSelThreads)
       if (pos[c] == j && p != j) pos[c] = p;
@@ -243,8 +240,8 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
     if (owner == me) {
       if (tid == 0) pos[lc_piv] = j;
       // pivot column: rows < j keep R, row j = beta, below = 0 (qrcp.py:80-81)
-      double* pc = colp(lc_piv);
-      for (int i = j + tid; i < ell; i += kSelThreads) pc[i] = (i == j) ? beta : 0.0;
+      for (int i = j + tid; i < ell; i += kSelThreads)
+        store[(size_t)lc_piv * ldl + i] = (i == j) ? beta : 0.0;
     }
     if (me == 0 && tid == 0) {
       a.piv[j] = p;
@@ -263,7 +260,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
     //      one 8-lane group per column
     for (int c = grp; c < ncol; c += NG) {
       if (pos[c] <= j) continue;  // uniform within the group
-      double* col = colp(c);
+      double* col = store + (size_t)c * ldl;
       if (tau != 0.0) {
         double d = 0.0;
         for (int i = j + gl; i < ell; i += 8) d = __fma_rn(vb[i], col[i], d);
@@ -290,7 +287,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
     }
     __syncthreads();
     publish(j + 1, par ^ 1);
-    cluster.sync();
+    grid_barrier(a.bar, epoch);
   }
 
   // ---- write the transformed sample in pivoted order
@@ -298,7 +295,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
     const int total = ncol * ell;
     for (int e = tid; e < total; e += kSelThreads) {
       const int c = e / ell, i = e - c * ell;
-      a.S[(size_t)pos[c] * a.lds + i] = colp(c)[i];
+      a.S[(size_t)pos[c] * a.lds + i] = store[(size_t)c * ldl + i];
     }
   }
   if (me == 0 && tid == 0) {
@@ -311,34 +308,28 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
       a.st->abort = kAbortShortSample;
     }
   }
-  cluster.sync();  // keep shared memory alive until every peer is done reading it
 }
 
 }  // namespace
 
-void select_pivots(Handle& h, int64_t ell, int64_t nt, int64_t want, const double* B,
+void select_pivots_grid(Handle& h, int64_t ell, int64_t nt, int64_t want, const double* B,
                    int64_t ldb, const SelectOut& out, Status* st, bool abort_on_short,
                    int64_t i0, cudaStream_t s) {
   if (want < 1 || want > std::min(ell, nt))
     throw InvalidArg("cannot select " + std::to_string(want) + " pivots from a " +
                      std::to_string(ell) + " x " + std::to_string(nt) + " sample");
-  const bool use_grid = h.force_select == 1 ||
-                        (h.force_select == 0 && nt > h.select_cluster_max_cols);
-  if (use_grid) {
-    select_pivots_grid(h, ell, nt, want, B, ldb, out, st, abort_on_short, i0, s);
-    return;
-  }
-  // cluster of P <= 16 CTAs, >= 32 columns each
-  int P = 1;
-  while (P < kMaxCluster && (int64_t)P * 32 < nt) P <<= 1;
+  // CTA count: >= 32 columns per CTA, at most one CTA per SM
+  int P = (int)std::min<int64_t>(h.num_sms, (nt + 31) / 32);
+  P = std::max(P, 1);
   const int cpb = (int)((nt + P - 1) / P);
+  P = (int)((nt + cpb - 1) / cpb);
   const int ldl = (int)(ell | 1);
-  const size_t meta = (size_t)(2 * cpb + 5 * ell + 8 + 8 + 8) * 8 + (size_t)(cpb + 8) * 4 + 256;
-  if (meta > h.smem_optin - 2048) throw InvalidArg("select: sample too large");
-  const size_t colbytes = (size_t)ldl * 8;
-  const int ncs = (int)std::min<size_t>(cpb, (h.smem_optin - 2048 - meta) / colbytes);
-  const size_t smem = (size_t)ncs * colbytes + meta;
-  SelArgs a{};
+  const size_t meta = (size_t)(2 * cpb + 3 * ell + 8 + 8) * 8 + (size_t)(cpb + 8) * 4 + 64;
+  if (P > 160) throw InvalidArg("select: too many CTAs");
+  const size_t store = (size_t)cpb * ldl * 8;
+  const bool use_smem = store + meta <= h.smem_optin - 2048;
+  const size_t smem = (use_smem ? store : 0) + meta;
+  SelGridArgs a{};
   a.ell = (int)ell; a.nt = (int)nt; a.want = (int)want;
   a.abort_on_short = abort_on_short ? 1 : 0;
   a.i0 = i0;
@@ -346,35 +337,25 @@ void select_pivots(Handle& h, int64_t ell, int64_t nt, int64_t want, const doubl
   a.S = out.S; a.lds = out.lds; a.piv = out.piv; a.Ys = out.Ys; a.ldys = out.ldys;
   a.taus = out.taus;
   a.st = st;
-  a.gstore = ncs < cpb ? (double*)h.buf("sel_gstore", (size_t)P * (cpb - ncs) * colbytes, s)
-                       : nullptr;
-  a.cpb = cpb; a.ldl = ldl; a.ncs = ncs;
-  static bool attr_init = false;
+  a.bar = (unsigned int*)h.buf("selg_bar", 64, s);
+  a.pubval = (double*)h.buf("selg_pubval", (size_t)2 * P * 8, s);
+  a.pubpos = (int*)h.buf("selg_pubpos", (size_t)2 * P * 4, s);
+  a.pubcol = (double*)h.buf("selg_pubcol", (size_t)2 * P * ell * 8, s);
+  a.pubsq = (double*)h.buf("selg_pubsq", (size_t)P * 8, s);
+  a.gstore = use_smem ? nullptr : (double*)h.buf("selg_gstore", (size_t)P * store, s);
+  a.cpb = cpb; a.ldl = ldl; a.use_smem = use_smem ? 1 : 0;
+  RQ_CUDA(cudaMemsetAsync(a.bar, 0, 64, s));
   static size_t attr = 0;
-  if (!attr_init) {
-    RQ_CUDA(cudaFuncSetAttribute(select_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    attr_init = true;
-  }
   if (smem > attr) {
-    RQ_CUDA(cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    RQ_CUDA(cudaFuncSetAttribute(select_grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)std::max<size_t>(smem, 48 * 1024)));
     attr = std::max<size_t>(smem, 48 * 1024);
   }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(P);
-  cfg.blockDim = dim3(kSelThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attrs[1];
-  attrs[0].id = cudaLaunchAttributeClusterDimension;
-  attrs[0].val.clusterDim.x = P;
-  attrs[0].val.clusterDim.y = 1;
-  attrs[0].val.clusterDim.z = 1;
-  cfg.attrs = attrs;
-  cfg.numAttrs = 1;
+  void* args[] = {&a};
   ProfScope prof(h, kProfSelect, 4.0 * ell * nt * want, 16.0 * ell * nt, s);
   count_launch();
-  RQ_CUDA(cudaLaunchKernelEx(&cfg, select_kernel, a));
+  RQ_CUDA(cudaLaunchCooperativeKernel((void*)select_grid_kernel, dim3(P), dim3(kSelThreads), args,
+                                      smem, s));
 }
 
 }  // namespace rq
