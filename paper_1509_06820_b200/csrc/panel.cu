@@ -1,24 +1,25 @@
-// K5: panel Householder QR + _panel_rank + T factor in ONE thread-block
-// cluster (qrcp.py:206-219 panel_householder; randomized.py:150-155
-// _panel_rank; kernels.py:139-147 build_t_matrix).
+// K5: panel Householder QR + _panel_rank (qrcp.py:206-219 panel_householder;
+// randomized.py:150-155 _panel_rank).  The T factor (kernels.py:139-147) is
+// built afterwards by t_factor() from a DMMA Gram GEMM.
 //
-// The mm x bw panel is split by rows over the Q <= 16 CTAs of a cluster and
-// kept in shared memory (global/L2 fallback when a row slab does not fit).
-// Per column j every CTA publishes, in its own shared memory, the partial
-// inner products d_c = sum_{r>j} P[r,j] P[r,c] over its rows (d_j is the
-// partial squared norm; the owner of row j also publishes that row), then a
-// cluster barrier (~0.23 us on B200, 5x cheaper than a grid barrier), then
-// every CTA reads the Q partial vectors over DSMEM and reduces them in the
-// same fixed order -- so beta, tau and w are bit-identical in every CTA -- and
-// updates its rows:
+// The mm x bw panel is split by rows over Q CTAs; every thread OWNS whole
+// rows (row-major shared-memory slab, odd leading dimension, rows past the
+// budget spill to L2), so one pass per column both applies the reflector and
+// forms the next column's partial inner products without any cross-thread
+// hand-off:
 //   P[r,c] -= (tau v_r) w_c,   v_r = P[r,j] / (alpha - beta)   (kernels.py:42,52)
-// fused with the partials of column j+1 (one pass over the slab per column).
-// Reflector convention is the reference's: beta = -sign(alpha)||x||,
+//   d_c    += P'[r,j+1] P'[r,c]      (r > j+1)
+// The partial vectors are reduced within a warp by a 31-shuffle transpose
+// reduction, across warps in shared memory, and across CTAs by the exchange:
+// either one thread-block cluster (Q <= 16, DSMEM + cluster barrier ~0.23 us)
+// or a cooperative grid (Q <= 64, L2 buffers + grid barrier ~1.2 us).  Every
+// CTA reduces the Q partials in the same fixed order, so alpha, beta, tau and
+// w are bit-identical everywhere.  Per column: one exchange + two block
+// barriers.  Reflector convention is the reference's: beta = -sign(alpha)||x||,
 // sign(0) = +1, a nonzero column is always reflected, a zero column gives
 // tau = 0.  v is kept below the diagonal until the commit, which writes R
-// (zeros below the diagonal) and the unit-lower Y only when the policy
-// allows it (speculative path: all columns usable, else Status.abort).
-// Using 16 SMs also leaves the rest of the GPU free for concurrent GEMMs.
+// (zeros below the diagonal) and unit-lower Y only when the policy allows it
+// (speculative path: all columns usable, else Status.abort).
 #include <cooperative_groups.h>
 
 #include "runtime.hpp"
@@ -32,6 +33,9 @@ namespace {
 constexpr int kPanThreads = 256;
 constexpr int kMaxBw = 256;
 constexpr int kMaxCluster = 16;
+constexpr int kMaxGrid = 64;
+constexpr int kRowsPerThread = 4;   // rpb <= 1024
+constexpr int kChunk = 32;          // columns per register chunk
 
 struct PanArgs {
   int64_t mm;
@@ -40,113 +44,168 @@ struct PanArgs {
   double* Rdst; int64_t ldr; int64_t rrows;
   double* Y; int64_t ldy;
   double* tau;
-  double* T; int64_t ldt;
   double tol;
   int policy;
   int raise_abort;
   int64_t i0;
   Status* st;
-  double* gstore;     // spill columns (global/L2), [Q][bw - ncs][ldl]
-  int rpb, ldl, ncs, cs;  // ncs = leading columns kept in shared memory
+  double* gstore;          // spill rows [Q][rpb - nrs][ldl]
+  int rpb, ldl, nrs;       // rows per CTA, row stride (odd), rows kept in smem
+  // grid exchange
+  unsigned int* bar;
+  double* gpub;            // [2][Q][2*bw]
 };
 
+// 32 per-lane values -> lane l holds the warp sum of column l (31 shuffles,
+// fixed combination order)
+RQ_DEV double warp_transpose_sum(double (&d)[kChunk]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    const bool up = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < off; ++i) {
+      const double keep = up ? d[i + off] : d[i];
+      const double give = up ? d[i] : d[i + off];
+      const double got = __shfl_xor_sync(0xffffffffu, give, off);
+      d[i] = up ? __dadd_rn(got, keep) : __dadd_rn(keep, got);
+    }
+  }
+  return d[0];
+}
+
+template <bool kCluster>
 __global__ void __launch_bounds__(kPanThreads, 1) panel_kernel(PanArgs a) {
   if (aborted(a.st)) return;
-  cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(16) double sm[];
-  const int tid = threadIdx.x;
-  const int Q = (int)cluster.num_blocks(), me = (int)cluster.block_rank();
-  const int bw = a.bw, cs = a.cs, groups = kPanThreads / cs;
-  const int tc = tid % cs, tg = tid / cs;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = kPanThreads / 32;
+  int Q, me;
+  if constexpr (kCluster) {
+    Q = (int)cg::this_cluster().num_blocks();
+    me = (int)cg::this_cluster().block_rank();
+  } else {
+    Q = gridDim.x;
+    me = blockIdx.x;
+  }
+  const int bw = a.bw, ldl = a.ldl, nrs = a.nrs;
   const int64_t r0 = (int64_t)me * a.rpb;
   const int nrow = (int)imax64(0, imin64(a.mm - r0, a.rpb));
-  const int ldl = a.ldl;
-  const int npair = bw * (bw - 1) / 2;
-  const int ncs = a.ncs;
-  double* gsp = a.gstore ? a.gstore + (size_t)me * (bw - ncs) * ldl : nullptr;
-  // column c of my row slab: shared memory for c < ncs, else the L2 spill
-  auto colp = [&](int c) -> double* {
-    return c < ncs ? sm + (size_t)c * ldl : gsp + (size_t)(c - ncs) * ldl;
+  double* gsp = a.gstore ? a.gstore + (size_t)me * (a.rpb - nrs) * ldl : nullptr;
+  auto rowp = [&](int r) -> double* {
+    return r < nrs ? sm + (size_t)r * ldl : gsp + (size_t)(r - nrs) * ldl;
   };
-  double* aux = sm + (size_t)ncs * ldl;
-  double* xpub = aux;                      // [2][2*bw] DSMEM-published partials + row
-  double* part = xpub + 4 * bw;            // [groups][bw]
-  double* dsum = part + groups * bw;       // [bw]
-  double* rowj = dsum + bw;                // [bw]
-  double* wsh = rowj + bw;                 // [bw]
-  double* taus = wsh + bw;                 // [bw]
-  double* tvrow = taus + bw;               // [rpb]  tau * v_r for my rows
-  double* xnext = tvrow + a.rpb;           // [rpb]  updated column j+1
-  double* gpart = xnext + a.rpb;           // [npair] Gram partial
-  double* gfin = gpart + npair;            // [npair] reduced Gram (rank 0)
-  __shared__ double s_sc[4];
+  double* aux = sm + (size_t)nrs * ldl;
+  double* xpub = aux;                  // [2][2*bw] partials + owner row (cluster exchange)
+  double* wpart = xpub + 4 * bw;       // [NW][bw] per-warp partial sums
+  double* dsum = wpart + NW * bw;      // [bw]
+  double* rowj = dsum + bw;            // [bw]
+  double* taus = rowj + bw;            // [bw]
   __shared__ int s_usable;
+  unsigned int epoch = 0;
   const int stride = 2 * bw;
   const int64_t ncols = imin64(bw, a.mm);
+  auto xsync = [&]() {
+    if constexpr (kCluster) cg::this_cluster().sync();
+    else grid_barrier(a.bar, epoch);
+  };
+  auto pub_out = [&](int par) -> double* {
+    if constexpr (kCluster) return xpub + (size_t)par * stride;
+    else return a.gpub + ((size_t)par * Q + me) * stride;
+  };
 
-  // ---- load my row slab (coalesced down each column, many loads in flight)
+  // ---- load my rows (coalesced down each global column)
   {
     const int total = nrow * bw;
 #pragma unroll 8
     for (int e = tid; e < total; e += kPanThreads) {
       const int c = e / nrow, r = e - c * nrow;
-      colp(c)[r] = a.P[(size_t)c * a.ldp + r0 + r];
+      rowp(r)[c] = a.P[(size_t)c * a.ldp + r0 + r];
     }
   }
   if (tid == 0) s_usable = (int)ncols;
   __syncthreads();
 
-  // partials of column 0 over my rows r > 0 (+ row 0 if owned) -> xpub[0]
-  {
-    const int rstart = r0 == 0 ? 1 : 0;
-    const double* x0 = colp(0);
-    for (int c = tc; c < bw; c += cs) {
-      const double* col = colp(c);
-      double d = 0.0;
-      for (int r = rstart + tg; r < nrow; r += groups) d = __fma_rn(x0[r], col[r], d);
-      part[tg * bw + c] = d;
-    }
+  // partial vector for column jn (rows > jn): per-thread registers, warp
+  // transpose-reduce, per-warp slots, then the block sum and the owner row
+  auto finish_partials = [&](int jn) {
     __syncthreads();
-    if (tg == 0)
-      for (int c = tc; c < bw; c += cs) {
-        double d = part[c];
-        for (int g = 1; g < groups; ++g) d = __dadd_rn(d, part[g * bw + c]);
-        xpub[c] = d;
+    double* out = pub_out(jn & 1);
+    for (int c = jn + tid; c < bw; c += kPanThreads) {
+      double d = wpart[c];
+      for (int w = 1; w < NW; ++w) d = __dadd_rn(d, wpart[w * bw + c]);
+      out[c] = d;
+    }
+    if (jn >= r0 && jn < r0 + nrow) {
+      const double* rr = rowp((int)(jn - r0));
+      for (int c = jn + tid; c < bw; c += kPanThreads) out[bw + c] = rr[c];
+    }
+  };
+
+  // initial partials of column 0
+  for (int cb = 0; cb < bw; cb += kChunk) {
+    double d[kChunk];
+#pragma unroll
+    for (int i = 0; i < kChunk; ++i) d[i] = 0.0;
+#pragma unroll
+    for (int k = 0; k < kRowsPerThread; ++k) {
+      const int r = tid + k * kPanThreads;
+      if (r < nrow && r0 + r > 0) {
+        const double* rr = rowp(r);
+        const double x = rr[0];
+#pragma unroll
+        for (int i = 0; i < kChunk; ++i)
+          if (cb + i < bw) d[i] = __fma_rn(x, rr[cb + i], d[i]);
       }
-    if (r0 == 0 && nrow > 0)
-      for (int c = tid; c < bw; c += kPanThreads) xpub[bw + c] = colp(c)[0];
+    }
+    const double s = warp_transpose_sum(d);
+    if (cb + lane < bw) wpart[warp * bw + cb + lane] = s;
   }
+  finish_partials(0);
 
   int64_t l2 = 0, l2b = 0;
   for (int j = 0; j < ncols; ++j) {
-    cluster.sync();
+    xsync();
     const int par = j & 1;
     const int owner = (int)(j / a.rpb);
-    // (1) reduce the Q partial vectors over DSMEM in fixed q order
+    // (A) fixed-order reduction of the Q partial vectors
     for (int c = j + tid; c < bw; c += kPanThreads) {
-      double v[kMaxCluster];
-#pragma unroll
-      for (int q = 0; q < kMaxCluster; ++q)
-        if (q < Q) v[q] = cluster.map_shared_rank(xpub, q)[par * stride + c];
       double d = 0.0;
+      if constexpr (kCluster) {
+        double v[kMaxCluster];
 #pragma unroll
-      for (int q = 0; q < kMaxCluster; ++q)
-        if (q < Q) d = __dadd_rn(d, v[q]);
+        for (int q = 0; q < kMaxCluster; ++q)
+          if (q < Q) v[q] = cg::this_cluster().map_shared_rank(xpub, q)[par * stride + c];
+#pragma unroll
+        for (int q = 0; q < kMaxCluster; ++q)
+          if (q < Q) d = __dadd_rn(d, v[q]);
+        rowj[c] = cg::this_cluster().map_shared_rank(xpub, owner)[par * stride + bw + c];
+      } else {
+        const double* g = a.gpub + (size_t)par * Q * stride + c;
+        double v[kMaxGrid];
+#pragma unroll
+        for (int q = 0; q < kMaxGrid; ++q)
+          if (q < Q) v[q] = g[(size_t)q * stride];
+#pragma unroll
+        for (int q = 0; q < kMaxGrid; ++q)
+          if (q < Q) d = __dadd_rn(d, v[q]);
+        rowj[c] = a.gpub[((size_t)par * Q + owner) * stride + bw + c];
+      }
       dsum[c] = d;
-      rowj[c] = cluster.map_shared_rank(xpub, owner)[par * stride + bw + c];
     }
     __syncthreads();
-    // (2) reflector scalars (kernels.py:35-44), identical in every CTA
+    // (B) reflector scalars (kernels.py:35-44), computed redundantly by every thread
+    const double alpha = rowj[j];
+    const double norm = sqrt(__fma_rn(alpha, alpha, dsum[j]));
+    double beta = 0.0, tau = 0.0, den = 1.0;
+    const bool zero = norm == 0.0;
+    if (!zero) {
+      beta = alpha >= 0.0 ? -norm : norm;
+      den = __dsub_rn(alpha, beta);
+      tau = __ddiv_rn(__dsub_rn(beta, alpha), beta);
+    }
+    const double rinv = zero ? 0.0 : 1.0 / den;
     if (tid == 0) {
-      const double alpha = rowj[j];
-      const double norm = sqrt(__fma_rn(alpha, alpha, dsum[j]));
-      double beta = 0.0, tau = 0.0, den = 1.0;
-      if (norm != 0.0) {
-        beta = alpha >= 0.0 ? -norm : norm;
-        den = __dsub_rn(alpha, beta);
-        tau = __ddiv_rn(__dsub_rn(beta, alpha), beta);
-      }
-      s_sc[0] = beta; s_sc[1] = tau; s_sc[2] = den; s_sc[3] = norm;
       taus[j] = tau;
       if (s_usable == ncols && fabs(beta) <= a.tol) s_usable = j;  // _panel_rank
       if (me == 0) {
@@ -157,68 +216,55 @@ __global__ void __launch_bounds__(kPanThreads, 1) panel_kernel(PanArgs a) {
         }
       }
     }
-    __syncthreads();
-    const double beta = s_sc[0], tau = s_sc[1], den = s_sc[2];
-    const bool zero = s_sc[3] == 0.0;
-    // (3) w_c = P[j,c] + (sum_{r>j} x_r P[r,c]) / (alpha - beta); v_r once per row
-    for (int c = j + 1 + tid; c < bw; c += kPanThreads)
-      wsh[c] = zero ? rowj[c] : __dadd_rn(rowj[c], __ddiv_rn(dsum[c], den));
-    const int rj = (int)imax64(0, (int64_t)j - r0);  // first local row >= j
-    {
-      double* xj = colp(j);
-      for (int r = rj + tid; r < nrow; r += kPanThreads) {
+    const bool more = j + 1 < ncols;
+    // (C) one pass over my rows: v, update of columns > j (w_c = P[j,c] +
+    //     (sum_{r>j} x_r P[r,c]) / (alpha - beta)), partials of column j+1
+    double tvr[kRowsPerThread];
+#pragma unroll
+    for (int k = 0; k < kRowsPerThread; ++k) {
+      const int r = tid + k * kPanThreads;
+      tvr[k] = 0.0;
+      if (r < nrow && r0 + r >= j) {
+        double* rr = rowp(r);
         const bool diag = r0 + r == j;
-        const double v = diag ? 1.0 : (zero ? xj[r] : __ddiv_rn(xj[r], den));
-        tvrow[r] = __dmul_rn(tau, v);
-        xj[r] = diag ? beta : v;
+        const double v = diag ? 1.0 : (zero ? rr[j] : __ddiv_rn(rr[j], den));
+        tvr[k] = __dmul_rn(tau, v);
+        rr[j] = diag ? beta : v;
       }
     }
-    __syncthreads();
-    if (j + 1 >= ncols) break;
-    // (4) updated column j+1 first (it feeds the next partials)
-    {
-      const double w1 = wsh[j + 1];
-      double* x1 = colp(j + 1);
-      for (int r = rj + tid; r < nrow; r += kPanThreads) {
-        const double nv = tau != 0.0 ? __dsub_rn(x1[r], __dmul_rn(tvrow[r], w1)) : x1[r];
-        x1[r] = nv;
-        xnext[r] = nv;
-      }
-    }
-    __syncthreads();
-    // (5) fused trailing update of columns > j+1 and the partials of step j+1
-    {
-      const int rs1 = (int)imax64(0, (int64_t)j + 2 - r0);  // rows > j+1
-      for (int c = j + 1 + tc; c < bw; c += cs) {
-        double* col = colp(c);
-        double d = 0.0;
-        if (c == j + 1) {
-          for (int r = rs1 + tg; r < nrow; r += groups) d = __fma_rn(xnext[r], xnext[r], d);
-        } else {
-          const double w = wsh[c];
-          for (int r = rj + tg; r < nrow; r += groups) {
-            const double nv = tau != 0.0 ? __dsub_rn(col[r], __dmul_rn(tvrow[r], w)) : col[r];
-            col[r] = nv;
-            if (r >= rs1) d = __fma_rn(xnext[r], nv, d);
+    if (!more) break;
+    const double w1 = __fma_rn(dsum[j + 1], rinv, rowj[j + 1]);
+    for (int cb = j + 1; cb < bw; cb += kChunk) {
+      double d[kChunk];
+#pragma unroll
+      for (int i = 0; i < kChunk; ++i) d[i] = 0.0;
+#pragma unroll
+      for (int k = 0; k < kRowsPerThread; ++k) {
+        const int r = tid + k * kPanThreads;
+        if (r < nrow && r0 + r >= j) {
+          double* rr = rowp(r);
+          const double tv = tvr[k];
+          // updated x' = P'[r, j+1] (needed for every chunk's partials)
+          const double x1 = tau != 0.0 ? __dsub_rn(rr[j + 1], __dmul_rn(tv, w1)) : rr[j + 1];
+          const bool below = r0 + r > j + 1;
+#pragma unroll
+          for (int i = 0; i < kChunk; ++i) {
+            const int c = cb + i;
+            if (c < bw) {
+              double nv = rr[c];
+              if (tau != 0.0) nv = __dsub_rn(nv, __dmul_rn(tv, __fma_rn(dsum[c], rinv, rowj[c])));
+              rr[c] = nv;
+              if (below) d[i] = __fma_rn(x1, nv, d[i]);
+            }
           }
         }
-        part[tg * bw + c] = d;
       }
-      __syncthreads();
-      double* out = xpub + (size_t)((j + 1) & 1) * stride;
-      if (tg == 0)
-        for (int c = j + 1 + tc; c < bw; c += cs) {
-          double d = part[c];
-          for (int g = 1; g < groups; ++g) d = __dadd_rn(d, part[g * bw + c]);
-          out[c] = d;
-        }
-      if (j + 1 >= r0 && j + 1 < r0 + nrow) {
-        const int lr = (int)(j + 1 - r0);
-        for (int c = j + 1 + tid; c < bw; c += kPanThreads) out[bw + c] = colp(c)[lr];
-      }
+      const double s = warp_transpose_sum(d);
+      if (cb + lane < bw) wpart[warp * bw + cb + lane] = s;
     }
+    finish_partials(j + 1);
   }
-  cluster.sync();  // every CTA is done reading the others' partials
+  xsync();  // every CTA is done reading the others' partials
 
   // ---- commit
   const int usable = s_usable;
@@ -236,76 +282,20 @@ __global__ void __launch_bounds__(kPanThreads, 1) panel_kernel(PanArgs a) {
       a.st->abort = kAbortPanelRank;
     }
   }
-  if (ncommit == 0) return;  // uniform across the cluster
-  {
+  if (ncommit > 0) {
     const int total = nrow * ncommit;
 #pragma unroll 4
     for (int e = tid; e < total; e += kPanThreads) {
       const int c = e / nrow, r = e - c * nrow;
       const int64_t gr = r0 + r;
-      const double val = colp(c)[r];
+      const double val = rowp(r)[c];
       a.Y[(size_t)c * a.ldy + gr] = gr < c ? 0.0 : (gr == c ? 1.0 : val);
       if (gr < a.rrows) a.Rdst[(size_t)c * a.ldr + gr] = gr <= c ? val : 0.0;
     }
+    if (me == 0)
+      for (int c = tid; c < ncommit; c += kPanThreads) a.tau[c] = taus[c];
   }
-  if (me == 0)
-    for (int c = tid; c < ncommit; c += kPanThreads) a.tau[c] = taus[c];
-  if (a.T == nullptr) return;
-
-  // ---- T factor (kernels.py:139-147): Gram G = Y^T Y (strict upper) from
-  // per-CTA partials reduced over DSMEM, then on rank 0
-  // T[:j,j] = -tau_j T[:j,:j] G[:j,j]
-  const int nc = ncommit;
-  const int np = nc * (nc - 1) / 2;
-  for (int e = tid; e < np; e += kPanThreads) {
-    int j = (int)((1.0 + sqrt(1.0 + 8.0 * e)) * 0.5);
-    while (j * (j - 1) / 2 > e) --j;
-    while ((j + 1) * j / 2 <= e) ++j;
-    const int i = e - j * (j - 1) / 2;
-    const int rs = (int)imax64(0, (int64_t)j - r0);  // rows >= j carry both
-    const double* yi = colp(i);
-    const double* yj = colp(j);
-    double g = 0.0;
-    for (int r = rs; r < nrow; ++r) g = __fma_rn(yi[r], (r0 + r == j) ? 1.0 : yj[r], g);
-    gpart[e] = g;
-  }
-  cluster.sync();
-  {
-    // this CTA reduces a slice of the pair list into rank 0's gfin
-    const int per = (np + Q - 1) / Q;
-    const int lo = me * per, hi = min(np, lo + per);
-    double* g0 = cluster.map_shared_rank(gfin, 0);
-    for (int e = lo + tid; e < hi; e += kPanThreads) {
-      double g = 0.0;
-      for (int q = 0; q < Q; ++q) g = __dadd_rn(g, cluster.map_shared_rank(gpart, q)[e]);
-      g0[e] = g;
-    }
-  }
-  cluster.sync();
-  if (me != 0) return;
-  // T workspace in the (now free) shared column store when it is big enough
-  const bool tsm = (int64_t)ncs * ldl >= (int64_t)nc * nc;
-  double* Tw = tsm ? sm : a.T;
-  const int ldtw = tsm ? nc : (int)a.ldt;
-  for (int e = tid; e < nc * nc; e += kPanThreads) Tw[(e % nc) + (size_t)(e / nc) * ldtw] = 0.0;
-  __syncthreads();
-  for (int j = 0; j < nc; ++j) {
-    const double* gcol = gfin + j * (j - 1) / 2;  // G[0:j, j]
-    for (int i = tid; i < j; i += kPanThreads) {
-      double t = 0.0;
-      for (int l = i; l < j; ++l) t = __fma_rn(Tw[i + (size_t)l * ldtw], gcol[l], t);
-      wsh[i] = t;
-    }
-    __syncthreads();
-    for (int i = tid; i < j; i += kPanThreads) Tw[i + (size_t)j * ldtw] = __dmul_rn(-taus[j], wsh[i]);
-    if (tid == 0) Tw[j + (size_t)j * ldtw] = taus[j];
-    __syncthreads();
-  }
-  if (tsm)
-    for (int e = tid; e < nc * nc; e += kPanThreads) {
-      const int i = e % nc, j = e / nc;
-      a.T[i + (size_t)j * a.ldt] = Tw[i + (size_t)j * ldtw];
-    }
+  if constexpr (kCluster) cg::this_cluster().sync();  // peers' DSMEM reads are done
 }
 
 }  // namespace
@@ -315,61 +305,82 @@ void panel_qr(Handle& h, int64_t mm, int64_t bw, const double* P, int64_t ldp,
               int64_t i0, cudaStream_t s) {
   if (bw < 1 || bw > kMaxBw) throw InvalidArg("panel width must be in [1, 256]");
   if (mm < 1) throw InvalidArg("panel needs at least one row");
-  const bool use_grid = h.force_panel == 1 ||
-                        (h.force_panel == 0 && (mm > h.panel_cluster_max_rows || bw > 64));
-  if (use_grid) {
-    panel_qr_grid(h, mm, bw, P, ldp, out, tol, policy, raise_abort, st, i0, s);
-    return;
-  }
+  const bool grid = h.force_panel == 1 || (h.force_panel == 0 && mm > h.panel_cluster_max_rows);
   int Q = 1;
-  while (Q < kMaxCluster && (int64_t)Q * 128 < mm) Q <<= 1;
+  if (grid) {
+    Q = (int)std::min<int64_t>(kMaxGrid, (mm + 127) / 128);
+    Q = std::max(Q, 1);
+  } else {
+    while (Q < kMaxCluster && (int64_t)Q * 128 < mm) Q <<= 1;
+  }
   const int rpb = (int)((mm + Q - 1) / Q);
-  int cs = 1;
-  while (cs < bw && cs < kPanThreads) cs <<= 1;
-  const int groups = kPanThreads / cs;
-  const int ldl = rpb | 1;
-  const size_t npair = (size_t)bw * (bw - 1) / 2;
-  const size_t aux = ((size_t)4 * bw + (size_t)groups * bw + 5 * (size_t)bw + 2 * (size_t)rpb +
-                      2 * npair + 8) * 8;
-  if (aux > h.smem_optin - 2048) throw InvalidArg("panel too wide for shared memory");
-  const size_t colbytes = (size_t)ldl * 8;
-  const int ncs = (int)std::min<size_t>(bw, (h.smem_optin - 2048 - aux) / colbytes);
-  const size_t smem = (size_t)ncs * colbytes + aux;
+  if (rpb > kRowsPerThread * kPanThreads) throw InvalidArg("panel too tall for the kernel");
+  const int ldl = (int)(bw | 1);
+  const size_t aux = ((size_t)4 * bw + (size_t)(kPanThreads / 32) * bw + 3 * (size_t)bw + 8) * 8;
+  if (aux > h.smem_optin - 4096) throw InvalidArg("panel too wide for shared memory");
+  const size_t rowbytes = (size_t)ldl * 8;
+  const int nrs = (int)std::min<size_t>(rpb, (h.smem_optin - 4096 - aux) / rowbytes);
+  const size_t smem = (size_t)nrs * rowbytes + aux;
   PanArgs a{};
   a.mm = mm; a.bw = (int)bw; a.P = P; a.ldp = ldp;
   a.Rdst = out.Rdst; a.ldr = out.ldr; a.rrows = out.rrows;
-  a.Y = out.Y; a.ldy = out.ldy; a.tau = out.tau; a.T = out.T; a.ldt = out.ldt;
+  a.Y = out.Y; a.ldy = out.ldy; a.tau = out.tau;
   a.tol = tol; a.policy = (int)policy; a.raise_abort = raise_abort ? 1 : 0; a.i0 = i0;
   a.st = st;
-  a.gstore = ncs < bw ? (double*)h.buf("pan_gstore", (size_t)Q * (bw - ncs) * colbytes, s)
-                      : nullptr;
-  a.rpb = rpb; a.ldl = ldl; a.ncs = ncs; a.cs = cs;
-  static bool attr_init = false;
-  static size_t attr = 0;
-  if (!attr_init) {
-    RQ_CUDA(cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    attr_init = true;
+  a.gstore = nrs < rpb ? (double*)h.buf("pan_gstore", (size_t)Q * (rpb - nrs) * rowbytes, s)
+                       : nullptr;
+  a.rpb = rpb; a.ldl = ldl; a.nrs = nrs;
+  {
+    ProfScope prof(h, kProfPanel, 2.0 * mm * bw * bw, 16.0 * mm * bw, s);
+    count_launch();
+    if (grid) {
+      a.bar = (unsigned int*)h.buf("pan_bar", 64, s);
+      a.gpub = (double*)h.buf("pan_gpub", (size_t)2 * Q * 2 * bw * 8, s);
+      RQ_CUDA(cudaMemsetAsync(a.bar, 0, 64, s));
+      static size_t attr = 0;
+      if (smem > attr) {
+        RQ_CUDA(cudaFuncSetAttribute(panel_kernel<false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)std::max<size_t>(smem, 48 * 1024)));
+        attr = std::max<size_t>(smem, 48 * 1024);
+      }
+      void* args[] = {&a};
+      RQ_CUDA(cudaLaunchCooperativeKernel((void*)panel_kernel<false>, dim3(Q), dim3(kPanThreads),
+                                          args, smem, s));
+    } else {
+      static bool attr_init = false;
+      static size_t attr = 0;
+      if (!attr_init) {
+        RQ_CUDA(cudaFuncSetAttribute(panel_kernel<true>,
+                                     cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        attr_init = true;
+      }
+      if (smem > attr) {
+        RQ_CUDA(cudaFuncSetAttribute(panel_kernel<true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)std::max<size_t>(smem, 48 * 1024)));
+        attr = std::max<size_t>(smem, 48 * 1024);
+      }
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(Q);
+      cfg.blockDim = dim3(kPanThreads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = s;
+      cudaLaunchAttribute attrs[1];
+      attrs[0].id = cudaLaunchAttributeClusterDimension;
+      attrs[0].val.clusterDim.x = Q;
+      attrs[0].val.clusterDim.y = 1;
+      attrs[0].val.clusterDim.z = 1;
+      cfg.attrs = attrs;
+      cfg.numAttrs = 1;
+      RQ_CUDA(cudaLaunchKernelEx(&cfg, panel_kernel<true>, a));
+    }
   }
-  if (smem > attr) {
-    RQ_CUDA(cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)std::max<size_t>(smem, 48 * 1024)));
-    attr = std::max<size_t>(smem, 48 * 1024);
+  if (out.T != nullptr) {
+    // T factor of the committed columns (kernels.py:139-147); after a failed
+    // speculative commit the Status predicate turns this into a no-op
+    t_factor(h, out.Y, out.ldy, mm, bw, out.tau, out.T, out.ldt, s, st);
   }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(Q);
-  cfg.blockDim = dim3(kPanThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attrs[1];
-  attrs[0].id = cudaLaunchAttributeClusterDimension;
-  attrs[0].val.clusterDim.x = Q;
-  attrs[0].val.clusterDim.y = 1;
-  attrs[0].val.clusterDim.z = 1;
-  cfg.attrs = attrs;
-  cfg.numAttrs = 1;
-  ProfScope prof(h, kProfPanel, 2.0 * mm * bw * bw, 16.0 * mm * bw, s);
-  count_launch();
-  RQ_CUDA(cudaLaunchKernelEx(&cfg, panel_kernel, a));
 }
 
 }  // namespace rq

@@ -134,11 +134,6 @@ void select_pivots(Handle& h, int64_t ell, int64_t nt, int64_t want, const doubl
                    int64_t ldb, const SelectOut& out, Status* st, bool abort_on_short,
                    int64_t i0, cudaStream_t s);
 
-// grid-cooperative variant (all SMs, one grid barrier per step) for wide samples
-void select_pivots_grid(Handle& h, int64_t ell, int64_t nt, int64_t want, const double* B,
-                        int64_t ldb, const SelectOut& out, Status* st, bool abort_on_short,
-                        int64_t i0, cudaStream_t s);
-
 struct PanelOut {
   double* Rdst; int64_t ldr; int64_t rrows;   // transformed panel rows [0, rrows)
   double* Y; int64_t ldy;                      // unit lower reflectors (mm x bw)
@@ -153,10 +148,6 @@ enum PanelPolicy { kPanelCommitIfFull = 0, kPanelCommitUsable = 1, kPanelCommitA
 void panel_qr(Handle& h, int64_t mm, int64_t bw, const double* P, int64_t ldp,
               const PanelOut& out, double tol, PanelPolicy policy, bool raise_abort, Status* st,
               int64_t i0, cudaStream_t s);
-
-void panel_qr_grid(Handle& h, int64_t mm, int64_t bw, const double* P, int64_t ldp,
-                   const PanelOut& out, double tol, PanelPolicy policy, bool raise_abort,
-                   Status* st, int64_t i0, cudaStream_t s);
 
 // B_new = [S12 - S11 R11^{-1} R12; S22] (randomized.py:107-135).  Writes
 // Status.degenerate; with abort_on_degenerate also sets Status.abort.
@@ -190,6 +181,7 @@ void scatter_cols(const double* src, int64_t lds, const int64_t* perm, double* d
 void set_identity(double* dst, int64_t ldd, int64_t rows, int64_t cols, cudaStream_t s);
 // full T factor of Y (mm x nb) from its Gram matrix (kernels.py:139-147)
 void t_factor(Handle& h, const double* Y, int64_t ldy, int64_t mm, int64_t nb,
-              const double* tau, double* T, int64_t ldt, cudaStream_t s);
+              const double* tau, double* T, int64_t ldt, cudaStream_t s,
+              const Status* st = nullptr);
 
 }  // namespace rq

@@ -1,20 +1,23 @@
 // K4: pivot-block selection = `want` greedy steps of column-pivoted
 // Householder QR on the small (b+p) x nt Gaussian sample, in one persistent
-// cooperative kernel (randomized.py:85-104 -> qrcp.py:63-84, NormTracker
+// kernel (randomized.py:85-104 -> qrcp.py:63-84, NormTracker
 // kernels.py:196-233, form/apply_reflector kernels.py:26-56).
 //
-// Layout: the sample's columns are dealt out to the P <= 16 CTAs of ONE
-// thread-block cluster in contiguous chunks and stay resident in shared
-// memory (columns beyond the shared-memory budget spill to global/L2).
-// Columns never move: a swap only relabels logical positions, so a step costs
-// one cluster barrier (~0.23 us on B200):
-//   publish local best (norm, position) + that column's data in own smem
-//   -> cluster barrier -> every CTA reads the P candidates over DSMEM and
-//      reduces them identically
-//   -> forms the reflector redundantly (bit-identical in every CTA)
-//   -> applies it to its own active columns, downdates their norms with the
-//      sqrt(eps) recompute guard, and publishes its next candidate.
-// Ties break to the lowest logical position (np.argmax first-max semantics).
+// Layout: the sample's columns are dealt out to P CTAs in contiguous chunks,
+// one column per thread, resident in shared memory (columns past the budget
+// spill to global/L2).  Columns never move: a swap only relabels logical
+// positions.  One step costs one exchange + one block barrier:
+//   exchange: every CTA publishes its local best (norm, position) and that
+//     column; then either a cluster barrier with DSMEM reads (P <= 16 CTAs of
+//     one thread-block cluster, small samples) or a grid barrier with
+//     L2-resident buffers (all SMs, wide samples)
+//   every WARP then redundantly reduces the P candidates (total order:
+//     larger norm, then lower position = np.argmax first-max), fetches the
+//     pivot column and forms the reflector -- identical bits everywhere, no
+//     block barrier needed
+//   every thread applies H_j to its own column, downdates its norm with the
+//     sqrt(eps) recompute guard, and the block argmax publishes the next
+//     candidate.
 // Initial norms use numpy's pairwise summation, so they are bit-identical to
 // np.linalg.norm(B, axis=0).
 #include <cooperative_groups.h>
@@ -28,8 +31,8 @@ namespace rq {
 namespace {
 
 constexpr int kSelThreads = 256;
-
 constexpr int kMaxCluster = 16;
+constexpr int kNoPos = 0x7fffffff;
 
 struct SelArgs {
   int ell, nt, want;
@@ -43,12 +46,18 @@ struct SelArgs {
   Status* st;
   double* gstore;   // spill columns [P][cpb - ncs][ldl]
   int cpb, ldl, ncs;
+  // grid exchange (global/L2)
+  unsigned int* bar;
+  double* gval;     // [2][P]
+  int* gpos;        // [2][P]
+  double* gcol;     // [2][P][ell]
+  double* gsq;      // [P]
 };
 
 struct Cand {
   double val;
   int pos;   // logical position (tie-break: lowest wins)
-  int idx;   // local column (publish) or owner CTA (global reduce)
+  int idx;   // local column (publish) or owner CTA (reduce)
 };
 RQ_DEV bool better(const Cand& a, const Cand& b) {
   return a.val > b.val || (a.val == b.val && a.pos < b.pos);
@@ -69,25 +78,21 @@ RQ_DEV double warp_sum(double v) {
   for (int off = 16; off; off >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
   return v;
 }
-// sum over an aligned group of 8 lanes; every lane of the group gets the same value
-RQ_DEV double group8_sum(double v, unsigned mask) {
-#pragma unroll
-  for (int off = 4; off; off >>= 1) v = __dadd_rn(v, __shfl_xor_sync(mask, v, off, 8));
-  return v;
-}
 
-constexpr int kNoPos = 0x7fffffff;
-
+template <bool kCluster>
 __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
   if (aborted(a.st)) return;
-  cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(16) double sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = kSelThreads / 32;
-  constexpr int NG = kSelThreads / 8;  // 8-lane column groups
-  const int grp = tid >> 3, gl = tid & 7;
-  const unsigned gmask = 0xffu << (lane & 24);  // the 8 lanes of my group
-  const int P = (int)cluster.num_blocks(), me = (int)cluster.block_rank();
+  int P, me;
+  if constexpr (kCluster) {
+    P = (int)cg::this_cluster().num_blocks();
+    me = (int)cg::this_cluster().block_rank();
+  } else {
+    P = gridDim.x;
+    me = blockIdx.x;
+  }
   const int ell = a.ell, ldl = a.ldl, ncs = a.ncs;
   const int c0 = me * a.cpb;
   const int ncol = max(0, min(a.nt - c0, a.cpb));
@@ -96,23 +101,24 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
     return c < ncs ? sm + (size_t)c * ldl : gsp + (size_t)(c - ncs) * ldl;
   };
   double* meta = sm + (size_t)ncs * ldl;
-  double* nrm = meta;                 // [cpb]
-  double* orig = nrm + a.cpb;         // [cpb]
-  double* xb = orig + a.cpb;          // [ell] pivot column
-  double* vb = xb + ell;              // [ell] v
-  double* tvb = vb + ell;             // [ell] tau*v
-  double* ccol = tvb + ell;           // [2][ell] published candidate column (DSMEM)
-  double* wv = ccol + 2 * ell;        // [NW + 8] scratch
-  int* pos = (int*)(wv + NW + 8);     // [cpb]
+  double* vw = meta;                         // [NW][2][ell] per-warp v and tau*v
+  double* ccol = vw + (size_t)NW * 2 * ell;  // [2][ell] published candidate column (cluster)
   __shared__ Cand s_red[NW];
-  __shared__ double s_sc[8];
-  __shared__ Cand s_win;
-  __shared__ int s_lc[2];             // local column of the published candidate
-  __shared__ double s_cval[2];        // published candidate (DSMEM)
+  __shared__ int s_lc[2];
+  __shared__ double s_cval[2];
   __shared__ int s_cpos[2];
-  __shared__ double s_sq;             // published ||B_local||^2 (DSMEM)
+  __shared__ double s_sq;
+  unsigned int epoch = 0;
 
-  // ---- load my columns, initial norms (pairwise, bit-identical to numpy)
+  auto xsync = [&]() {
+    if constexpr (kCluster) cg::this_cluster().sync();
+    else grid_barrier(a.bar, epoch);
+  };
+
+  // ---- per-thread column state (thread t owns local columns t, t+256, ...)
+  constexpr int kMaxOwn = 4;  // cpb <= 1024
+  double nrm[kMaxOwn], orig[kMaxOwn];
+  int pos[kMaxOwn];
   {
     const int total = ncol * ell;
 #pragma unroll 4
@@ -122,130 +128,150 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
     }
   }
   __syncthreads();
-  double mysq = 0.0;  // fixed-order per-thread partial of ||B||_F^2
-  for (int c = tid; c < ncol; c += kSelThreads) {
-    const double sq = pairwise_sumsq(colp(c), ell, 1);
-    const double nv = sqrt(sq);
-    nrm[c] = nv;
-    orig[c] = __dmul_rn(nv, nv);
-    pos[c] = c0 + c;
-    mysq = __dadd_rn(mysq, sq);
+  double mysq = 0.0;
+#pragma unroll
+  for (int k = 0; k < kMaxOwn; ++k) {
+    const int c = tid + k * kSelThreads;
+    pos[k] = kNoPos;
+    nrm[k] = -1.0;
+    orig[k] = 0.0;
+    if (c < ncol) {
+      const double sq = pairwise_sumsq(colp(c), ell, 1);
+      const double nv = sqrt(sq);
+      nrm[k] = nv;
+      orig[k] = __dmul_rn(nv, nv);
+      pos[k] = c0 + c;
+      mysq = __dadd_rn(mysq, sq);
+    }
   }
+  // CTA partial of ||B||^2 in a fixed order
   {
-    double v = warp_sum(mysq);
-    if (lane == 0) wv[warp] = v;
+    const double v = warp_sum(mysq);
+    if (lane == 0) s_red[warp].val = v;
     __syncthreads();
     if (tid == 0) {
       double t = 0.0;
-      for (int w = 0; w < NW; ++w) t = __dadd_rn(t, wv[w]);
+      for (int w = 0; w < NW; ++w) t = __dadd_rn(t, s_red[w].val);
       s_sq = t;
+      if constexpr (!kCluster) a.gsq[me] = t;
     }
+    __syncthreads();
   }
 
-  // local argmax over active columns (position >= jstart); publishes the
-  // candidate (value, position) and its column into parity slot `par`
+  // block argmax over my active columns -> publish slot `par`
   auto publish = [&](int jstart, int par) {
     Cand best{-1.0, kNoPos, -1};
-    for (int c = tid; c < ncol; c += kSelThreads) {
-      if (pos[c] >= jstart) {
-        Cand cc{nrm[c], pos[c], c};
+#pragma unroll
+    for (int k = 0; k < kMaxOwn; ++k)
+      if (pos[k] != kNoPos && pos[k] >= jstart) {
+        Cand cc{nrm[k], pos[k], tid + k * kSelThreads};
         if (better(cc, best)) best = cc;
       }
-    }
     best = warp_best(best);
     if (lane == 0) s_red[warp] = best;
     __syncthreads();
     if (warp == 0) {
       Cand b = lane < NW ? s_red[lane] : Cand{-1.0, kNoPos, -1};
       b = warp_best(b);
+      const int lc = b.idx;
       if (lane == 0) {
-        s_lc[par] = b.idx;
-        s_cval[par] = b.val;
-        s_cpos[par] = b.pos;
+        s_lc[par] = lc;
+        if constexpr (kCluster) {
+          s_cval[par] = b.val;
+          s_cpos[par] = b.pos;
+        } else {
+          a.gval[par * P + me] = b.val;
+          a.gpos[par * P + me] = b.pos;
+        }
       }
-    }
-    __syncthreads();
-    const int lc = s_lc[par];
-    if (lc >= 0) {
-      const double* src = colp(lc);
-      for (int i = tid; i < ell; i += kSelThreads) ccol[par * ell + i] = src[i];
+      if (lc >= 0) {
+        const double* src = colp(lc);
+        double* dst = kCluster ? ccol + par * ell : a.gcol + ((size_t)par * P + me) * ell;
+        for (int i = lane; i < ell; i += 32) dst[i] = src[i];
+      }
     }
   };
 
   publish(0, 0);
-  cluster.sync();
-
-  // tol = eps * ||B||_F  (randomized.py:98), same summation order everywhere
-  if (tid == 0) {
+  xsync();
+  double tol;
+  {
+    __shared__ double s_all[160];
+    for (int q = tid; q < P; q += kSelThreads) {
+      if constexpr (kCluster) s_all[q] = *cg::this_cluster().map_shared_rank(&s_sq, q);
+      else s_all[q] = a.gsq[q];
+    }
+    __syncthreads();
     double t = 0.0;
-    for (int q = 0; q < P; ++q) t = __dadd_rn(t, *cluster.map_shared_rank(&s_sq, q));
-    s_sc[0] = kEps * sqrt(t);
+    for (int q = 0; q < P; ++q) t = __dadd_rn(t, s_all[q]);
+    tol = kEps * sqrt(t);  // randomized.py:98, same summation order everywhere
   }
-  __syncthreads();
-  const double tol = s_sc[0];
 
   int got = a.want;
   int64_t l2 = 0, l2b = 0;
+  double* myv = vw + (size_t)warp * 2 * ell;
+  double* mytv = myv + ell;
   for (int j = 0; j < a.want; ++j) {
     const int par = j & 1;
-    // ---- cluster-wide argmax over the P candidates (total order -> identical everywhere)
-    if (warp == 0) {
-      Cand b{-1.0, kNoPos, -1};
-      if (lane < P) {
-        const double v = cluster.map_shared_rank(s_cval, lane)[par];
-        const int p = cluster.map_shared_rank(s_cpos, lane)[par];
-        if (p != kNoPos) b = Cand{v, p, lane};
+    // ---- every warp: winner among the P candidates (order independent)
+    Cand win{-1.0, kNoPos, -1};
+    for (int q = lane; q < P; q += 32) {
+      double v;
+      int p;
+      if constexpr (kCluster) {
+        v = cg::this_cluster().map_shared_rank(s_cval, q)[par];
+        p = cg::this_cluster().map_shared_rank(s_cpos, q)[par];
+      } else {
+        v = a.gval[par * P + q];
+        p = a.gpos[par * P + q];
       }
-      b = warp_best(b);
-      if (lane == 0) s_win = b;
+      Cand cc{v, p, q};
+      if (p != kNoPos && better(cc, win)) win = cc;
     }
-    __syncthreads();
-    const Cand win = s_win;
+    win = warp_best(win);
     const int p = win.pos, owner = win.idx;
     if (owner < 0 || !(win.val > tol)) {  // max trailing norm <= tol: halt (qrcp.py:69-71)
       got = j;
       break;
     }
-    // ---- fetch the pivot column over DSMEM, relabel positions (swap j <-> p)
-    {
-      const double* oc = cluster.map_shared_rank(ccol, owner) + par * ell;
-      for (int i = tid; i < ell; i += kSelThreads) xb[i] = oc[i];
+    // ---- every warp: pivot column -> reflector (kernels.py:26-44), own copy of v
+    const double* xc;
+    if constexpr (kCluster) xc = cg::this_cluster().map_shared_rank(ccol, owner) + par * ell;
+    else xc = a.gcol + ((size_t)par * P + owner) * ell;
+    double xv[5];  // ell <= 160
+    double sq = 0.0;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const int i = lane + 32 * k;
+      xv[k] = i < ell ? xc[i] : 0.0;
+      if (i >= j && i < ell) sq = __fma_rn(xv[k], xv[k], sq);
     }
-    const int lc_piv = s_lc[par];
-    for (int c = tid; c < ncol; c += kSelThreads)
-      if (pos[c] == j && p != j) pos[c] = p;
-    __syncthreads();
-    // ---- reflector from x[j:] (kernels.py:26-44), identical in every CTA
-    if (warp == 0) {
-      double sq = 0.0;
-      for (int i = j + lane; i < ell; i += 32) sq = __fma_rn(xb[i], xb[i], sq);
-      sq = warp_sum(sq);
-      if (lane == 0) {
-        const double norm = sqrt(sq);
-        const double alpha = xb[j];
-        double beta = 0.0, tau = 0.0, den = 1.0;
-        if (norm != 0.0) {
-          beta = alpha >= 0.0 ? -norm : norm;
-          den = __dsub_rn(alpha, beta);
-          tau = __ddiv_rn(__dsub_rn(beta, alpha), beta);
-        }
-        s_sc[2] = beta; s_sc[3] = tau; s_sc[4] = den; s_sc[5] = norm;
+    sq = warp_sum(sq);
+    double alpha = 0.0;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const double t = __shfl_sync(0xffffffffu, xv[k], j & 31);
+      if ((j >> 5) == k) alpha = t;
+    }
+    const double norm = sqrt(sq);
+    double beta = 0.0, tau = 0.0, den = 1.0;
+    const bool zero = norm == 0.0;
+    if (!zero) {
+      beta = alpha >= 0.0 ? -norm : norm;
+      den = __dsub_rn(alpha, beta);
+      tau = __ddiv_rn(__dsub_rn(beta, alpha), beta);
+    }
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const int i = lane + 32 * k;
+      if (i >= j && i < ell) {
+        const double v = (i == j) ? 1.0 : (zero ? xv[k] : __ddiv_rn(xv[k], den));
+        myv[i] = v;
+        mytv[i] = __dmul_rn(tau, v);
       }
     }
-    __syncthreads();
-    const double beta = s_sc[2], tau = s_sc[3], den = s_sc[4];
-    const bool zero = s_sc[5] == 0.0;
-    for (int i = j + tid; i < ell; i += kSelThreads) {
-      const double v = (i == j) ? 1.0 : (zero ? xb[i] : __ddiv_rn(xb[i], den));
-      vb[i] = v;
-      tvb[i] = __dmul_rn(tau, v);
-    }
-    if (owner == me) {
-      if (tid == 0) pos[lc_piv] = j;
-      // pivot column: rows < j keep R, row j = beta, below = 0 (qrcp.py:80-81)
-      double* pc = colp(lc_piv);
-      for (int i = j + tid; i < ell; i += kSelThreads) pc[i] = (i == j) ? beta : 0.0;
-    }
+    __syncwarp();
+    const int lc_piv = s_lc[par];
     if (me == 0 && tid == 0) {
       a.piv[j] = p;
       if (a.taus) a.taus[j] = tau;
@@ -255,51 +281,64 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
         l2b += 16LL * (ell - j) * cols;
       }
     }
-    __syncthreads();
-    if (me == 0 && a.Ys)
-      for (int i = tid; i < ell; i += kSelThreads)
-        a.Ys[(size_t)j * a.ldys + i] = i < j ? 0.0 : vb[i];
-    // ---- apply H_j to my active columns (pos > j) and downdate their norms;
-    //      one 8-lane group per column
-    for (int c = grp; c < ncol; c += NG) {
-      if (pos[c] <= j) continue;  // uniform within the group
+    if (me == 0 && a.Ys && warp == 0)
+      for (int i = lane; i < ell; i += 32) a.Ys[(size_t)j * a.ldys + i] = i < j ? 0.0 : myv[i];
+    // ---- my columns: relabel (swap j <-> p), pivot column, apply H_j, downdate
+#pragma unroll
+    for (int k = 0; k < kMaxOwn; ++k) {
+      const int c = tid + k * kSelThreads;
+      if (pos[k] == kNoPos) continue;
+      if (owner == me && c == lc_piv) {
+        // pivot column: rows < j keep R, row j = beta, below = 0 (qrcp.py:80-81)
+        double* col = colp(c);
+        for (int i = j; i < ell; ++i) col[i] = (i == j) ? beta : 0.0;
+        pos[k] = j;
+        continue;
+      }
+      if (pos[k] == j && p != j) pos[k] = p;
+      if (pos[k] <= j) continue;
       double* col = colp(c);
       if (tau != 0.0) {
-        double d = 0.0;
-        for (int i = j + gl; i < ell; i += 8) d = __fma_rn(vb[i], col[i], d);
-        const double w = group8_sum(d, gmask);
-        for (int i = j + gl; i < ell; i += 8) col[i] = __dsub_rn(col[i], __dmul_rn(tvb[i], w));
+        double d0 = 0.0, d1 = 0.0;
+        int i = j;
+        for (; i + 1 < ell; i += 2) {
+          d0 = __fma_rn(myv[i], col[i], d0);
+          d1 = __fma_rn(myv[i + 1], col[i + 1], d1);
+        }
+        if (i < ell) d0 = __fma_rn(myv[i], col[i], d0);
+        const double w = __dadd_rn(d0, d1);
+#pragma unroll 4
+        for (int r = j; r < ell; ++r) col[r] = __dsub_rn(col[r], __dmul_rn(mytv[r], w));
       }
       if (j + 1 < a.nt) {
         // NormTracker.downdate with row j of the updated sample (kernels.py:222-233)
-        __syncwarp(gmask);
         const double row = col[j];
-        const double nv = nrm[c];
+        const double nv = nrm[k];
         double nsq = __dsub_rn(__dmul_rn(nv, nv), __dmul_rn(row, row));
         nsq = nsq > 0.0 ? nsq : 0.0;
-        if (!(nsq < __dmul_rn(kGuard, orig[c]))) {
-          if (gl == 0) nrm[c] = sqrt(nsq);
+        if (!(nsq < __dmul_rn(kGuard, orig[k]))) {
+          nrm[k] = sqrt(nsq);
         } else {
-          double sq = 0.0;
-          for (int i = j + 1 + gl; i < ell; i += 8) sq = __fma_rn(col[i], col[i], sq);
-          sq = group8_sum(sq, gmask);
-          const double fresh = sqrt(sq);
-          if (gl == 0) { nrm[c] = fresh; orig[c] = __dmul_rn(fresh, fresh); }
+          double s0 = 0.0;
+          for (int r = j + 1; r < ell; ++r) s0 = __fma_rn(col[r], col[r], s0);
+          const double fresh = sqrt(s0);
+          nrm[k] = fresh;
+          orig[k] = __dmul_rn(fresh, fresh);
         }
       }
     }
-    __syncthreads();
     publish(j + 1, par ^ 1);
-    cluster.sync();
+    xsync();
   }
 
-  // ---- write the transformed sample in pivoted order
-  {
-    const int total = ncol * ell;
-    for (int e = tid; e < total; e += kSelThreads) {
-      const int c = e / ell, i = e - c * ell;
-      a.S[(size_t)pos[c] * a.lds + i] = colp(c)[i];
-    }
+  // ---- write the transformed sample in pivoted order (thread per column)
+#pragma unroll
+  for (int k = 0; k < kMaxOwn; ++k) {
+    const int c = tid + k * kSelThreads;
+    if (pos[k] == kNoPos) continue;
+    const double* col = colp(c);
+    double* dst = a.S + (size_t)pos[k] * a.lds;
+    for (int i = 0; i < ell; ++i) dst[i] = col[i];
   }
   if (me == 0 && tid == 0) {
     a.st->got = got;
@@ -311,7 +350,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
       a.st->abort = kAbortShortSample;
     }
   }
-  cluster.sync();  // keep shared memory alive until every peer is done reading it
+  if constexpr (kCluster) cg::this_cluster().sync();  // peers may still read my smem
 }
 
 }  // namespace
@@ -322,21 +361,25 @@ void select_pivots(Handle& h, int64_t ell, int64_t nt, int64_t want, const doubl
   if (want < 1 || want > std::min(ell, nt))
     throw InvalidArg("cannot select " + std::to_string(want) + " pivots from a " +
                      std::to_string(ell) + " x " + std::to_string(nt) + " sample");
-  const bool use_grid = h.force_select == 1 ||
-                        (h.force_select == 0 && nt > h.select_cluster_max_cols);
-  if (use_grid) {
-    select_pivots_grid(h, ell, nt, want, B, ldb, out, st, abort_on_short, i0, s);
-    return;
+  if (ell > 160) throw InvalidArg("sample rows > 160 not supported by the pivot kernel");
+  const bool grid = h.force_select == 1 ||
+                    (h.force_select == 0 && nt > h.select_cluster_max_cols);
+  int P;
+  if (grid) {
+    P = (int)std::min<int64_t>(std::min(h.num_sms, 160), (nt + 31) / 32);
+    P = std::max(P, 1);
+    const int cpb = (int)((nt + P - 1) / P);
+    P = (int)((nt + cpb - 1) / cpb);
+  } else {
+    P = 1;
+    while (P < kMaxCluster && (int64_t)P * 64 < nt) P <<= 1;
   }
-  // cluster of P <= 16 CTAs, >= 32 columns each
-  int P = 1;
-  while (P < kMaxCluster && (int64_t)P * 32 < nt) P <<= 1;
   const int cpb = (int)((nt + P - 1) / P);
+  if (cpb > 4 * kSelThreads) throw InvalidArg("sample too wide for the pivot kernel");
   const int ldl = (int)(ell | 1);
-  const size_t meta = (size_t)(2 * cpb + 5 * ell + 8 + 8 + 8) * 8 + (size_t)(cpb + 8) * 4 + 256;
-  if (meta > h.smem_optin - 2048) throw InvalidArg("select: sample too large");
+  const size_t meta = ((size_t)(kSelThreads / 32) * 2 * ell + 2 * ell + 16) * 8 + 256;
   const size_t colbytes = (size_t)ldl * 8;
-  const int ncs = (int)std::min<size_t>(cpb, (h.smem_optin - 2048 - meta) / colbytes);
+  const int ncs = (int)std::min<size_t>(cpb, (h.smem_optin - 4096 - meta) / colbytes);
   const size_t smem = (size_t)ncs * colbytes + meta;
   SelArgs a{};
   a.ell = (int)ell; a.nt = (int)nt; a.want = (int)want;
@@ -349,14 +392,36 @@ void select_pivots(Handle& h, int64_t ell, int64_t nt, int64_t want, const doubl
   a.gstore = ncs < cpb ? (double*)h.buf("sel_gstore", (size_t)P * (cpb - ncs) * colbytes, s)
                        : nullptr;
   a.cpb = cpb; a.ldl = ldl; a.ncs = ncs;
+  ProfScope prof(h, kProfSelect, 4.0 * ell * nt * want, 16.0 * ell * nt, s);
+  count_launch();
+  if (grid) {
+    a.bar = (unsigned int*)h.buf("sel_bar", 64, s);
+    a.gval = (double*)h.buf("sel_gval", (size_t)2 * P * 8, s);
+    a.gpos = (int*)h.buf("sel_gpos", (size_t)2 * P * 4, s);
+    a.gcol = (double*)h.buf("sel_gcol", (size_t)2 * P * ell * 8, s);
+    a.gsq = (double*)h.buf("sel_gsq", (size_t)P * 8, s);
+    RQ_CUDA(cudaMemsetAsync(a.bar, 0, 64, s));
+    static size_t attr = 0;
+    if (smem > attr) {
+      RQ_CUDA(cudaFuncSetAttribute(select_kernel<false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)std::max<size_t>(smem, 48 * 1024)));
+      attr = std::max<size_t>(smem, 48 * 1024);
+    }
+    void* args[] = {&a};
+    RQ_CUDA(cudaLaunchCooperativeKernel((void*)select_kernel<false>, dim3(P), dim3(kSelThreads),
+                                        args, smem, s));
+    return;
+  }
   static bool attr_init = false;
   static size_t attr = 0;
   if (!attr_init) {
-    RQ_CUDA(cudaFuncSetAttribute(select_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    RQ_CUDA(cudaFuncSetAttribute(select_kernel<true>,
+                                 cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     attr_init = true;
   }
   if (smem > attr) {
-    RQ_CUDA(cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    RQ_CUDA(cudaFuncSetAttribute(select_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)std::max<size_t>(smem, 48 * 1024)));
     attr = std::max<size_t>(smem, 48 * 1024);
   }
@@ -372,9 +437,7 @@ void select_pivots(Handle& h, int64_t ell, int64_t nt, int64_t want, const doubl
   attrs[0].val.clusterDim.z = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
-  ProfScope prof(h, kProfSelect, 4.0 * ell * nt * want, 16.0 * ell * nt, s);
-  count_launch();
-  RQ_CUDA(cudaLaunchKernelEx(&cfg, select_kernel, a));
+  RQ_CUDA(cudaLaunchKernelEx(&cfg, select_kernel<true>, a));
 }
 
 }  // namespace rq

@@ -302,25 +302,35 @@ __global__ void scatter_cols_kernel(const double* src, int64_t lds, const int64_
     dst[r + perm[c] * ldd] = src[r + c * lds];
   }
 }
-// T recurrence from the Gram matrix G (nb x nb, upper part used)
-__global__ void t_recurrence_kernel(const double* G, int64_t ldg, const double* tau, int nb,
-                                    double* T, int64_t ldt) {
-  extern __shared__ double tmp[];
+// T recurrence from the Gram matrix G (nb x nb, upper part used):
+// T[:j, j] = -tau_j * (T[:j, :j] @ G[:j, j]), T[j, j] = tau_j (kernels.py:139-147).
+// T lives in shared memory while it is built (nb <= 128), else in place.
+__global__ void t_recurrence_kernel(const double* __restrict__ G, int64_t ldg,
+                                    const double* __restrict__ tau, int nb, double* T,
+                                    int64_t ldt, const Status* st) {
+  if (aborted(st)) return;
+  extern __shared__ double tsm[];
+  const bool in_smem = nb <= 128;
+  double* Tw = in_smem ? tsm : T;
+  const int64_t ldw = in_smem ? nb : ldt;
+  double* tmp = in_smem ? tsm + (size_t)nb * nb : tsm;
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) Tw[(e % nb) + (e / nb) * ldw] = 0.0;
+  __syncthreads();
   for (int j = 0; j < nb; ++j) {
+    const double tj = tau[j];
     for (int i = threadIdx.x; i < j; i += blockDim.x) {
       double t = 0.0;
-      for (int l = i; l < j; ++l) t = __fma_rn(T[i + (size_t)l * ldt], G[l + (size_t)j * ldg], t);
+      for (int l = i; l < j; ++l) t = __fma_rn(Tw[i + (size_t)l * ldw], G[l + (size_t)j * ldg], t);
       tmp[i] = t;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < nb; i += blockDim.x) {
-      double v = 0.0;
-      if (i < j) v = __dmul_rn(-tau[j], tmp[i]);
-      else if (i == j) v = tau[j];
-      T[i + (size_t)j * ldt] = v;
-    }
+    for (int i = threadIdx.x; i < j; i += blockDim.x) Tw[i + (size_t)j * ldw] = __dmul_rn(-tj, tmp[i]);
+    if (threadIdx.x == 0) Tw[j + (size_t)j * ldw] = tj;
     __syncthreads();
   }
+  if (in_smem)
+    for (int e = threadIdx.x; e < nb * nb; e += blockDim.x)
+      T[(e % nb) + (size_t)(e / nb) * ldt] = Tw[e];
 }
 
 int grid_for(int64_t total, int num_sms) {
@@ -449,15 +459,19 @@ void scatter_cols(const double* src, int64_t lds, const int64_t* perm, double* d
 }
 
 void t_factor(Handle& h, const double* Y, int64_t ldy, int64_t mm, int64_t nb,
-              const double* tau, double* T, int64_t ldt, cudaStream_t s) {
+              const double* tau, double* T, int64_t ldt, cudaStream_t s, const Status* st) {
   if (nb <= 0) return;
   double* G = (double*)h.buf("tf_gram", (size_t)nb * nb * 8, s);
-  gemm(h, true, false, nb, nb, mm, 1.0, Y, ldy, Y, ldy, 0.0, G, nb, s);
-  const size_t smem = (size_t)nb * 8;
-  if (smem > 48 * 1024)
-    RQ_CUDA(cudaFuncSetAttribute(t_recurrence_kernel,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  t_recurrence_kernel<<<1, 256, smem, s>>>(G, nb, tau, (int)nb, T, ldt);
+  gemm(h, true, false, nb, nb, mm, 1.0, Y, ldy, Y, ldy, 0.0, G, nb, s, st, kProfPanel);
+  const size_t smem = nb <= 128 ? ((size_t)nb * nb + nb) * 8 : (size_t)nb * 8;
+  static size_t attr = 0;
+  if (smem > attr) {
+    RQ_CUDA(cudaFuncSetAttribute(t_recurrence_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)std::max<size_t>(smem, 48 * 1024)));
+    attr = std::max<size_t>(smem, 48 * 1024);
+  }
+  ProfScope prof(h, kProfPanel, (double)nb * nb * nb / 3.0, 16.0 * nb * nb, s);
+  t_recurrence_kernel<<<1, 256, smem, s>>>(G, nb, tau, (int)nb, T, ldt, st);
   RQ_CHECK_LAUNCH();
   count_launch();
 }
