@@ -176,6 +176,9 @@ int rq_frob_norm(rq_handle_t h, const double* A, int64_t m, int64_t n, int64_t l
  * "panel_cluster_max_rows" (size thresholds of the heuristic) */
 int rq_set_option(rq_handle_t h, const char* name, int64_t value);
 
+/* debug: phase timers written by the kernels when "debug_timers" is set */
+int rq_debug_read(rq_handle_t h, int64_t* out, int n);
+
 /* total kernel launches issued by this library since load (all handles) */
 int64_t rq_launch_count(void);
 

@@ -70,6 +70,7 @@ SIGNATURES = {
     "rq_frob_norm": (C.c_int, [vp, dp, i64, i64, i64, dp, vp]),
     "rq_launch_count": (C.c_int64, []),
     "rq_set_option": (C.c_int, [vp, C.c_char_p, i64]),
+    "rq_debug_read": (C.c_int, [vp, C.POINTER(i64), C.c_int]),
     "rq_profile_enable": (C.c_int, [vp, C.c_int]),
     "rq_profile_reset": (C.c_int, [vp]),
     "rq_profile_read": (C.c_int, [vp, C.POINTER(i64), C.POINTER(f64), C.POINTER(f64),

@@ -256,7 +256,20 @@ int rq_set_option(rq_handle_t h, const char* name, int64_t value) {
     else if (n == "force_panel") hh.force_panel = (int)value;
     else if (n == "select_cluster_max_cols") hh.select_cluster_max_cols = value;
     else if (n == "panel_cluster_max_rows") hh.panel_cluster_max_rows = value;
+    else if (n == "debug_timers") {
+      hh.dbg = value ? (long long*)hh.buf("dbg_timers", 64 * 8, nullptr) : nullptr;
+      if (hh.dbg) RQ_CUDA(cudaMemset(hh.dbg, 0, 64 * 8));
+    }
     else throw rq::InvalidArg("unknown option " + n);
+  });
+}
+
+int rq_debug_read(rq_handle_t h, int64_t* out, int n) {
+  return guarded([&] {
+    rq::Handle& hh = H(h);
+    need(hh.dbg != nullptr, "debug timers not enabled");
+    RQ_CUDA(cudaDeviceSynchronize());
+    RQ_CUDA(cudaMemcpy(out, hh.dbg, (size_t)std::min(n, 64) * 8, cudaMemcpyDeviceToHost));
   });
 }
 

@@ -90,6 +90,8 @@ class Handle {
   int64_t select_cluster_max_cols = 1024;   // nt threshold
   int64_t panel_cluster_max_rows = 3072;    // mm threshold (bw <= 64 only)
 
+  long long* dbg = nullptr;  // optional device phase-timer buffer (debug)
+
   // profiler
   bool profiling = false;
   ProfStat stats[kProfNum];

@@ -30,7 +30,7 @@ namespace rq {
 
 namespace {
 
-constexpr int kSelThreads = 256;
+constexpr int kSelThreads = 512;
 constexpr int kMaxCluster = 16;
 constexpr int kNoPos = 0x7fffffff;
 
@@ -52,6 +52,7 @@ struct SelArgs {
   int* gpos;        // [2][P]
   double* gcol;     // [2][P][ell]
   double* gsq;      // [P]
+  long long* dbg;   // optional phase timers (CTA 0, thread 0): [8] cycles
 };
 
 struct Cand {
@@ -85,6 +86,9 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
   extern __shared__ __align__(16) double sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = kSelThreads / 32;
+  constexpr int NG = kSelThreads / 8;          // 8-lane column groups
+  const int grp = tid >> 3, gl = tid & 7;
+  const unsigned gmask = 0xffu << (lane & 24);  // my group's lanes
   int P, me;
   if constexpr (kCluster) {
     P = (int)cg::this_cluster().num_blocks();
@@ -102,12 +106,16 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
   };
   double* meta = sm + (size_t)ncs * ldl;
   double* vw = meta;                         // [NW][2][ell] per-warp v and tau*v
-  double* ccol = vw + (size_t)NW * 2 * ell;  // [2][ell] published candidate column (cluster)
+  double* ccol = vw + (size_t)NW * 2 * ell;  // [2][ell] my published candidate column
+  double* nrm = ccol + 2 * ell;              // [cpb]
+  double* orig = nrm + a.cpb;                // [cpb]
+  int* pos = (int*)(orig + a.cpb);           // [cpb]
   __shared__ Cand s_red[NW];
   __shared__ int s_lc[2];
-  __shared__ double s_cval[2];
-  __shared__ int s_cpos[2];
-  __shared__ double s_sq;
+  __shared__ double s_cval[2][kMaxCluster];  // candidates pushed by every peer (cluster)
+  __shared__ int s_cpos[2][kMaxCluster];
+  __shared__ double s_sq[kMaxCluster];
+  __shared__ double s_all[160];
   unsigned int epoch = 0;
 
   auto xsync = [&]() {
@@ -115,10 +123,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
     else grid_barrier(a.bar, epoch);
   };
 
-  // ---- per-thread column state (thread t owns local columns t, t+256, ...)
-  constexpr int kMaxOwn = 4;  // cpb <= 1024
-  double nrm[kMaxOwn], orig[kMaxOwn];
-  int pos[kMaxOwn];
+  // ---- load my columns; initial norms (pairwise, bit-identical to numpy)
   {
     const int total = ncol * ell;
 #pragma unroll 4
@@ -129,22 +134,14 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
   }
   __syncthreads();
   double mysq = 0.0;
-#pragma unroll
-  for (int k = 0; k < kMaxOwn; ++k) {
-    const int c = tid + k * kSelThreads;
-    pos[k] = kNoPos;
-    nrm[k] = -1.0;
-    orig[k] = 0.0;
-    if (c < ncol) {
-      const double sq = pairwise_sumsq(colp(c), ell, 1);
-      const double nv = sqrt(sq);
-      nrm[k] = nv;
-      orig[k] = __dmul_rn(nv, nv);
-      pos[k] = c0 + c;
-      mysq = __dadd_rn(mysq, sq);
-    }
+  for (int c = tid; c < ncol; c += kSelThreads) {
+    const double sq = pairwise_sumsq(colp(c), ell, 1);
+    const double nv = sqrt(sq);
+    nrm[c] = nv;
+    orig[c] = __dmul_rn(nv, nv);
+    pos[c] = c0 + c;
+    mysq = __dadd_rn(mysq, sq);
   }
-  // CTA partial of ||B||^2 in a fixed order
   {
     const double v = warp_sum(mysq);
     if (lane == 0) s_red[warp].val = v;
@@ -152,19 +149,20 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
     if (tid == 0) {
       double t = 0.0;
       for (int w = 0; w < NW; ++w) t = __dadd_rn(t, s_red[w].val);
-      s_sq = t;
-      if constexpr (!kCluster) a.gsq[me] = t;
+      if constexpr (kCluster) {
+        for (int q = 0; q < P; ++q) cg::this_cluster().map_shared_rank(s_sq, q)[me] = t;
+      } else {
+        a.gsq[me] = t;
+      }
     }
-    __syncthreads();
   }
 
-  // block argmax over my active columns -> publish slot `par`
+  // block argmax over my active columns -> publish into slot `par`
   auto publish = [&](int jstart, int par) {
     Cand best{-1.0, kNoPos, -1};
-#pragma unroll
-    for (int k = 0; k < kMaxOwn; ++k)
-      if (pos[k] != kNoPos && pos[k] >= jstart) {
-        Cand cc{nrm[k], pos[k], tid + k * kSelThreads};
+    for (int c = tid; c < ncol; c += kSelThreads)
+      if (pos[c] >= jstart) {
+        Cand cc{nrm[c], pos[c], c};
         if (better(cc, best)) best = cc;
       }
     best = warp_best(best);
@@ -174,16 +172,16 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
       Cand b = lane < NW ? s_red[lane] : Cand{-1.0, kNoPos, -1};
       b = warp_best(b);
       const int lc = b.idx;
-      if (lane == 0) {
-        s_lc[par] = lc;
-        if constexpr (kCluster) {
-          s_cval[par] = b.val;
-          s_cpos[par] = b.pos;
-        } else {
-          a.gval[par * P + me] = b.val;
-          a.gpos[par * P + me] = b.pos;
+      if constexpr (kCluster) {
+        if (lane < P) {  // push (value, position) into every peer's candidate table
+          cg::this_cluster().map_shared_rank(&s_cval[par][0], lane)[me] = b.val;
+          cg::this_cluster().map_shared_rank(&s_cpos[par][0], lane)[me] = b.pos;
         }
+      } else if (lane == 0) {
+        a.gval[par * P + me] = b.val;
+        a.gpos[par * P + me] = b.pos;
       }
+      if (lane == 0) s_lc[par] = lc;
       if (lc >= 0) {
         const double* src = colp(lc);
         double* dst = kCluster ? ccol + par * ell : a.gcol + ((size_t)par * P + me) * ell;
@@ -196,9 +194,8 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
   xsync();
   double tol;
   {
-    __shared__ double s_all[160];
     for (int q = tid; q < P; q += kSelThreads) {
-      if constexpr (kCluster) s_all[q] = *cg::this_cluster().map_shared_rank(&s_sq, q);
+      if constexpr (kCluster) s_all[q] = s_sq[q];
       else s_all[q] = a.gsq[q];
     }
     __syncthreads();
@@ -209,68 +206,96 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
 
   int got = a.want;
   int64_t l2 = 0, l2b = 0;
-  double* myv = vw + (size_t)warp * 2 * ell;
-  double* mytv = myv + ell;
+  long long tm[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tlast = clock64();
+  const bool timing = a.dbg != nullptr && me == 0 && tid == 0;
+  auto mark = [&](int k) {
+    if (timing) {
+      const long long t = clock64();
+      tm[k] += t - tlast;
+      tlast = t;
+    }
+  };
+  double* myv = vw;          // v and tau*v (written by warp 0)
+  double* mytv = vw + ell;
+  __shared__ double s_step[2];
+  __shared__ int s_stepi[2];
   for (int j = 0; j < a.want; ++j) {
     const int par = j & 1;
-    // ---- every warp: winner among the P candidates (order independent)
-    Cand win{-1.0, kNoPos, -1};
-    for (int q = lane; q < P; q += 32) {
-      double v;
-      int p;
-      if constexpr (kCluster) {
-        v = cg::this_cluster().map_shared_rank(s_cval, q)[par];
-        p = cg::this_cluster().map_shared_rank(s_cpos, q)[par];
-      } else {
-        v = a.gval[par * P + q];
-        p = a.gpos[par * P + q];
+    // ---- warp 0: winner among the P candidates (order independent) and the
+    //      reflector (kernels.py:26-44); the rest of the CTA waits at one barrier
+    if (warp == 0) {
+      Cand win{-1.0, kNoPos, -1};
+      for (int q = lane; q < P; q += 32) {
+        double v;
+        int p;
+        if constexpr (kCluster) {
+          v = s_cval[par][q];
+          p = s_cpos[par][q];
+        } else {
+          v = a.gval[par * P + q];
+          p = a.gpos[par * P + q];
+        }
+        Cand cc{v, p, q};
+        if (p != kNoPos && better(cc, win)) win = cc;
       }
-      Cand cc{v, p, q};
-      if (p != kNoPos && better(cc, win)) win = cc;
+      win = warp_best(win);
+      const bool halt = win.idx < 0 || !(win.val > tol);  // qrcp.py:69-71
+      if (!halt) {
+        const double* xc;
+        if constexpr (kCluster) xc = cg::this_cluster().map_shared_rank(ccol, win.idx) + par * ell;
+        else xc = a.gcol + ((size_t)par * P + win.idx) * ell;
+        double xv[5];  // ell <= 160
+        double sq = 0.0;
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+          const int i = lane + 32 * k;
+          xv[k] = i < ell ? xc[i] : 0.0;
+          if (i >= j && i < ell) sq = __fma_rn(xv[k], xv[k], sq);
+        }
+        sq = warp_sum(sq);
+        double alpha = 0.0;
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+          const double t = __shfl_sync(0xffffffffu, xv[k], j & 31);
+          if ((j >> 5) == k) alpha = t;
+        }
+        const double norm = sqrt(sq);
+        double beta = 0.0, tau = 0.0, den = 1.0;
+        const bool zero = norm == 0.0;
+        if (!zero) {
+          beta = alpha >= 0.0 ? -norm : norm;
+          den = __dsub_rn(alpha, beta);
+          tau = __ddiv_rn(__dsub_rn(beta, alpha), beta);
+        }
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+          const int i = lane + 32 * k;
+          if (i >= j && i < ell) {
+            const double v = (i == j) ? 1.0 : (zero ? xv[k] : __ddiv_rn(xv[k], den));
+            myv[i] = v;
+            mytv[i] = __dmul_rn(tau, v);
+          }
+        }
+        if (lane == 0) {
+          s_step[0] = beta;
+          s_step[1] = tau;
+        }
+      }
+      if (lane == 0) {
+        s_stepi[0] = halt ? -1 : win.idx;
+        s_stepi[1] = win.pos;
+      }
     }
-    win = warp_best(win);
-    const int p = win.pos, owner = win.idx;
-    if (owner < 0 || !(win.val > tol)) {  // max trailing norm <= tol: halt (qrcp.py:69-71)
+    __syncthreads();
+    mark(0);
+    const int owner = s_stepi[0], p = s_stepi[1];
+    if (owner < 0) {
       got = j;
       break;
     }
-    // ---- every warp: pivot column -> reflector (kernels.py:26-44), own copy of v
-    const double* xc;
-    if constexpr (kCluster) xc = cg::this_cluster().map_shared_rank(ccol, owner) + par * ell;
-    else xc = a.gcol + ((size_t)par * P + owner) * ell;
-    double xv[5];  // ell <= 160
-    double sq = 0.0;
-#pragma unroll
-    for (int k = 0; k < 5; ++k) {
-      const int i = lane + 32 * k;
-      xv[k] = i < ell ? xc[i] : 0.0;
-      if (i >= j && i < ell) sq = __fma_rn(xv[k], xv[k], sq);
-    }
-    sq = warp_sum(sq);
-    double alpha = 0.0;
-#pragma unroll
-    for (int k = 0; k < 5; ++k) {
-      const double t = __shfl_sync(0xffffffffu, xv[k], j & 31);
-      if ((j >> 5) == k) alpha = t;
-    }
-    const double norm = sqrt(sq);
-    double beta = 0.0, tau = 0.0, den = 1.0;
-    const bool zero = norm == 0.0;
-    if (!zero) {
-      beta = alpha >= 0.0 ? -norm : norm;
-      den = __dsub_rn(alpha, beta);
-      tau = __ddiv_rn(__dsub_rn(beta, alpha), beta);
-    }
-#pragma unroll
-    for (int k = 0; k < 5; ++k) {
-      const int i = lane + 32 * k;
-      if (i >= j && i < ell) {
-        const double v = (i == j) ? 1.0 : (zero ? xv[k] : __ddiv_rn(xv[k], den));
-        myv[i] = v;
-        mytv[i] = __dmul_rn(tau, v);
-      }
-    }
-    __syncwarp();
+    const double beta = s_step[0], tau = s_step[1];
+    mark(1);
     const int lc_piv = s_lc[par];
     if (me == 0 && tid == 0) {
       a.piv[j] = p;
@@ -283,62 +308,74 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
     }
     if (me == 0 && a.Ys && warp == 0)
       for (int i = lane; i < ell; i += 32) a.Ys[(size_t)j * a.ldys + i] = i < j ? 0.0 : myv[i];
-    // ---- my columns: relabel (swap j <-> p), pivot column, apply H_j, downdate
-#pragma unroll
-    for (int k = 0; k < kMaxOwn; ++k) {
-      const int c = tid + k * kSelThreads;
-      if (pos[k] == kNoPos) continue;
+    // ---- my columns, one 8-lane group per column: relabel (swap j <-> p),
+    //      pivot column, apply H_j, downdate
+    for (int c = grp; c < ncol; c += NG) {
+      double* col = colp(c);
+      int pc = pos[c];
       if (owner == me && c == lc_piv) {
         // pivot column: rows < j keep R, row j = beta, below = 0 (qrcp.py:80-81)
-        double* col = colp(c);
-        for (int i = j; i < ell; ++i) col[i] = (i == j) ? beta : 0.0;
-        pos[k] = j;
+        for (int i = j + gl; i < ell; i += 8) col[i] = (i == j) ? beta : 0.0;
+        if (gl == 0) pos[c] = j;
         continue;
       }
-      if (pos[k] == j && p != j) pos[k] = p;
-      if (pos[k] <= j) continue;
-      double* col = colp(c);
+      if (pc == j && p != j) {
+        pc = p;
+        if (gl == 0) pos[c] = p;
+      }
+      if (pc <= j) continue;
       if (tau != 0.0) {
         double d0 = 0.0, d1 = 0.0;
-        int i = j;
-        for (; i + 1 < ell; i += 2) {
+        int i = j + gl;
+        for (; i + 8 < ell; i += 16) {
           d0 = __fma_rn(myv[i], col[i], d0);
-          d1 = __fma_rn(myv[i + 1], col[i + 1], d1);
+          d1 = __fma_rn(myv[i + 8], col[i + 8], d1);
         }
         if (i < ell) d0 = __fma_rn(myv[i], col[i], d0);
-        const double w = __dadd_rn(d0, d1);
-#pragma unroll 4
-        for (int r = j; r < ell; ++r) col[r] = __dsub_rn(col[r], __dmul_rn(mytv[r], w));
+        double w = __dadd_rn(d0, d1);
+#pragma unroll
+        for (int off = 4; off; off >>= 1) w = __dadd_rn(w, __shfl_xor_sync(gmask, w, off, 8));
+#pragma unroll 2
+        for (int r = j + gl; r < ell; r += 8) col[r] = __dsub_rn(col[r], __dmul_rn(mytv[r], w));
       }
       if (j + 1 < a.nt) {
         // NormTracker.downdate with row j of the updated sample (kernels.py:222-233)
+        __syncwarp(gmask);
         const double row = col[j];
-        const double nv = nrm[k];
+        const double nv = nrm[c];
         double nsq = __dsub_rn(__dmul_rn(nv, nv), __dmul_rn(row, row));
         nsq = nsq > 0.0 ? nsq : 0.0;
-        if (!(nsq < __dmul_rn(kGuard, orig[k]))) {
-          nrm[k] = sqrt(nsq);
+        if (!(nsq < __dmul_rn(kGuard, orig[c]))) {
+          if (gl == 0) nrm[c] = sqrt(nsq);
         } else {
           double s0 = 0.0;
-          for (int r = j + 1; r < ell; ++r) s0 = __fma_rn(col[r], col[r], s0);
+          for (int r = j + 1 + gl; r < ell; r += 8) s0 = __fma_rn(col[r], col[r], s0);
+#pragma unroll
+          for (int off = 4; off; off >>= 1) s0 = __dadd_rn(s0, __shfl_xor_sync(gmask, s0, off, 8));
           const double fresh = sqrt(s0);
-          nrm[k] = fresh;
-          orig[k] = __dmul_rn(fresh, fresh);
+          if (gl == 0) {
+            nrm[c] = fresh;
+            orig[c] = __dmul_rn(fresh, fresh);
+          }
         }
       }
     }
+    mark(2);
     publish(j + 1, par ^ 1);
+    mark(3);
     xsync();
+    mark(4);
+  }
+  if (timing) {
+    for (int k = 0; k < 5; ++k) a.dbg[k] = tm[k];
+    a.dbg[7] = a.want;
   }
 
-  // ---- write the transformed sample in pivoted order (thread per column)
-#pragma unroll
-  for (int k = 0; k < kMaxOwn; ++k) {
-    const int c = tid + k * kSelThreads;
-    if (pos[k] == kNoPos) continue;
+  // ---- write the transformed sample in pivoted order (group per column)
+  for (int c = grp; c < ncol; c += NG) {
     const double* col = colp(c);
-    double* dst = a.S + (size_t)pos[k] * a.lds;
-    for (int i = 0; i < ell; ++i) dst[i] = col[i];
+    double* dst = a.S + (size_t)pos[c] * a.lds;
+    for (int i = gl; i < ell; i += 8) dst[i] = col[i];
   }
   if (me == 0 && tid == 0) {
     a.st->got = got;
@@ -375,9 +412,10 @@ void select_pivots(Handle& h, int64_t ell, int64_t nt, int64_t want, const doubl
     while (P < kMaxCluster && (int64_t)P * 64 < nt) P <<= 1;
   }
   const int cpb = (int)((nt + P - 1) / P);
-  if (cpb > 4 * kSelThreads) throw InvalidArg("sample too wide for the pivot kernel");
+  if (cpb > 8192) throw InvalidArg("sample too wide for the pivot kernel");
   const int ldl = (int)(ell | 1);
-  const size_t meta = ((size_t)(kSelThreads / 32) * 2 * ell + 2 * ell + 16) * 8 + 256;
+  const size_t meta = ((size_t)(kSelThreads / 32) * 2 * ell + 2 * ell + 2 * (size_t)cpb + 16) * 8 +
+                      (size_t)cpb * 4 + 256;
   const size_t colbytes = (size_t)ldl * 8;
   const int ncs = (int)std::min<size_t>(cpb, (h.smem_optin - 4096 - meta) / colbytes);
   const size_t smem = (size_t)ncs * colbytes + meta;
@@ -392,6 +430,7 @@ void select_pivots(Handle& h, int64_t ell, int64_t nt, int64_t want, const doubl
   a.gstore = ncs < cpb ? (double*)h.buf("sel_gstore", (size_t)P * (cpb - ncs) * colbytes, s)
                        : nullptr;
   a.cpb = cpb; a.ldl = ldl; a.ncs = ncs;
+  a.dbg = h.dbg;
   ProfScope prof(h, kProfSelect, 4.0 * ell * nt * want, 16.0 * ell * nt, s);
   count_launch();
   if (grid) {
