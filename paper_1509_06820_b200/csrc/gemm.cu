@@ -79,6 +79,10 @@ void gemm(Handle& h, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double a
           const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
           int64_t ldc, cudaStream_t s, const Status* st, int cat) {
   if (M <= 0 || N <= 0) return;
+  // rank-b trailing updates C -= Y X go to the persistent double-buffered kernel
+  if (!ta && !tb && alpha == -1.0 && beta == 1.0 && M >= 64 && N >= 64 && h.use_rank_update &&
+      rank_update(h, M, N, K, A, lda, B, ldb, C, ldc, s, st, cat))
+    return;
   // algorithmic traffic: read A, B (+ C when beta != 0), write C
   const double bytes = 8.0 * ((double)M * K + (double)K * N + (double)M * N * (beta != 0.0 ? 2 : 1));
   ProfScope prof(h, cat, 2.0 * (double)M * N * K, bytes, s);

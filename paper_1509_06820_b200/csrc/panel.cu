@@ -234,6 +234,17 @@ __global__ void __launch_bounds__(kPanThreads, 1) panel_kernel(PanArgs a) {
     }
     if (!more) break;
     const double w1 = __fma_rn(dsum[j + 1], rinv, rowj[j + 1]);
+    // updated x' = P'[r, j+1] of my rows, before any chunk rewrites column j+1
+    double x1r[kRowsPerThread];
+#pragma unroll
+    for (int k = 0; k < kRowsPerThread; ++k) {
+      const int r = tid + k * kPanThreads;
+      x1r[k] = 0.0;
+      if (r < nrow && r0 + r >= j) {
+        const double old = rowp(r)[j + 1];
+        x1r[k] = tau != 0.0 ? __dsub_rn(old, __dmul_rn(tvr[k], w1)) : old;
+      }
+    }
     for (int cb = j + 1; cb < bw; cb += kChunk) {
       double d[kChunk];
 #pragma unroll
@@ -244,8 +255,7 @@ __global__ void __launch_bounds__(kPanThreads, 1) panel_kernel(PanArgs a) {
         if (r < nrow && r0 + r >= j) {
           double* rr = rowp(r);
           const double tv = tvr[k];
-          // updated x' = P'[r, j+1] (needed for every chunk's partials)
-          const double x1 = tau != 0.0 ? __dsub_rn(rr[j + 1], __dmul_rn(tv, w1)) : rr[j + 1];
+          const double x1 = x1r[k];
           const bool below = r0 + r > j + 1;
 #pragma unroll
           for (int i = 0; i < kChunk; ++i) {

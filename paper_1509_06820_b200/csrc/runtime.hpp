@@ -90,6 +90,7 @@ class Handle {
   int64_t select_cluster_max_cols = 1024;   // nt threshold
   int64_t panel_cluster_max_rows = 3072;    // mm threshold (bw <= 64 only)
 
+  bool use_rank_update = true;
   long long* dbg = nullptr;  // optional device phase-timer buffer (debug)
 
   // profiler
@@ -122,6 +123,11 @@ class Handle {
 void gemm(Handle& h, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha,
           const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
           int64_t ldc, cudaStream_t s, const Status* st = nullptr, int cat = kProfSmallGemm);
+
+// persistent C -= Y X for K <= 64 (rank_update.cu); false if not applicable
+bool rank_update(Handle& h, int64_t M, int64_t N, int64_t K, const double* Y, int64_t ldy,
+                 const double* X, int64_t ldx, double* C, int64_t ldc, cudaStream_t s,
+                 const Status* st, int cat);
 
 // ------------------------------------------------------------------ kernels (small.cu, select.cu, panel.cu)
 struct SelectOut {

@@ -312,7 +312,10 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
     //      pivot column, apply H_j, downdate
     for (int c = grp; c < ncol; c += NG) {
       double* col = colp(c);
+      // read the column state before any lane of the group writes it
       int pc = pos[c];
+      const double nv = nrm[c], og = orig[c];
+      __syncwarp(gmask);
       if (owner == me && c == lc_piv) {
         // pivot column: rows < j keep R, row j = beta, below = 0 (qrcp.py:80-81)
         for (int i = j + gl; i < ell; i += 8) col[i] = (i == j) ? beta : 0.0;
@@ -342,10 +345,9 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
         // NormTracker.downdate with row j of the updated sample (kernels.py:222-233)
         __syncwarp(gmask);
         const double row = col[j];
-        const double nv = nrm[c];
         double nsq = __dsub_rn(__dmul_rn(nv, nv), __dmul_rn(row, row));
         nsq = nsq > 0.0 ? nsq : 0.0;
-        if (!(nsq < __dmul_rn(kGuard, orig[c]))) {
+        if (!(nsq < __dmul_rn(kGuard, og))) {
           if (gl == 0) nrm[c] = sqrt(nsq);
         } else {
           double s0 = 0.0;
@@ -360,6 +362,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
         }
       }
     }
+    __syncthreads();  // norms/positions written by the groups are read by publish
     mark(2);
     publish(j + 1, par ^ 1);
     mark(3);
@@ -371,6 +374,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
     a.dbg[7] = a.want;
   }
 
+  __syncthreads();
   // ---- write the transformed sample in pivoted order (group per column)
   for (int c = grp; c < ncol; c += NG) {
     const double* col = colp(c);
