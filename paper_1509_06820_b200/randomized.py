@@ -151,9 +151,9 @@ def package(out, host, trailing_update=True, truncated=False):
         trailing = out["work"][rank:, rank:] if trailing_update else None
     perm = out["perm"]
     if host:
+        # one D2H copy per output, layout kept (column-major), no host-side reshuffle
         cv = lambda t: None if t is None else t.cpu().numpy()  # noqa: E731
         Y, tau, R, W, trailing, perm = cv(Y), cv(tau), cv(R), cv(W), cv(trailing), cv(perm)
-        R = np.ascontiguousarray(R)
     else:
         R = R.clone()
         trailing = trailing.clone() if trailing is not None else None
