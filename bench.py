@@ -10,9 +10,10 @@ Householder QR flops (4n^3/3 full, 4kmn - 2k^2(m+n) + 4k^3/3 truncated).
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--config cfg1|cfg2|cfg3|cfg4|cfg5]
 
-Prints ONE JSON line on rank 0.  Under torchrun (N > 1) every rank factors its
-own replica (weak scaling; the column-block-cyclic sharded driver is not built
-yet -- DESIGN.md), timed between barriers, max over ranks.
+Prints ONE JSON line on rank 0.  Under torchrun (N > 1) the matrix is sharded
+column-block-cyclically over the ranks and factored by the NCCL driver
+(paper_1509_06820_b200/parallel.py; strong scaling), timed between barriers
+with CUDA events, max over ranks.
 """
 
 from __future__ import annotations
@@ -282,11 +283,29 @@ def main():
         torch.cuda.synchronize(dev)
 
     peak = fp64_peak() if rank == 0 else None
-    A = device_matrix(cfg["kind"], cfg["m"], cfg["n"], dev, seed=rank)
+    A = device_matrix(cfg["kind"], cfg["m"], cfg["n"], dev, seed=0 if world > 1 else rank)
     torch.cuda.synchronize(dev)
     lib = _abi.load_library()
     h = _abi.handle(local)
 
+    sharded = world > 1
+    if sharded:
+        # column-block-cyclic shards of ONE matrix over the ranks (strong scaling)
+        from paper_1509_06820_b200.parallel import BlockCyclic, rqrcp_sharded
+        layout = BlockCyclic(cfg["n"], cfg["block"], world)
+        idx = torch.as_tensor(layout.positions(rank), device=dev)
+        from paper_1509_06820_b200.device import fmat
+        A_loc = fmat(cfg["m"], int(idx.numel()), dev)
+        A_loc.copy_(A[:, idx])
+        del A
+        torch.cuda.empty_cache()
+        if cfg["driver"] != "rqrcp":
+            raise SystemExit("multi-GPU bench: only the RQRCP configs are sharded")
+        cfgP = P.RandomizedConfig(block=cfg["block"], padding=cfg["padding"], seed=0)
+
+        def run_ours(P_, cfg_, A_, _x):  # noqa: F811 - sharded step
+            return rqrcp_sharded(A_loc, cfg_["m"], cfg_["n"], cfg_["k"], cfgP, gather_r=False)
+        A = None
     for _ in range(args.warmup):
         f = run_ours(P, cfg, A, None)
     barrier()
@@ -317,7 +336,8 @@ def main():
     ms_max = float(t.item())
     ms_step = ms_max / args.steps
     flops_step = std_flops(cfg)
-    value = flops_step * world / (ms_step * 1e-3) / 1e9
+    # replicas: every rank factors its own matrix; sharded: one matrix over all ranks
+    value = flops_step * (1 if sharded else world) / (ms_step * 1e-3) / 1e9
     kernels = {}
     for i, nm in enumerate(_abi.PROF_NAMES):
         if L[i]:
@@ -341,10 +361,15 @@ def main():
                     "algorithmic_flops_per_launch": FL[i] / max(L[i], 1),
                     "avg_launch_us": MS[i] * 1e3 / max(L[i], 1)}
     res_counters = f.counters
+    if sharded:
+        from paper_1509_06820_b200.factorization import OpCounters
+        res_counters = OpCounters(gemm_flops=f.counters["gemm_flops"],
+                                  level2_flops=f.counters["level2_flops"],
+                                  resamples=f.counters["resamples"])
 
     # ---- end to end through the public API with host buffers
     e2e = None
-    if not args.no_e2e and rank == 0:
+    if not args.no_e2e and rank == 0 and not sharded:
         Ah = torch.empty((cfg["n"], cfg["m"]), dtype=torch.float64).pin_memory().t()
         Ah.copy_(A)
         Ahost = Ah.numpy()
@@ -375,13 +400,16 @@ def main():
             "metric": "RQRCP/TRQRCP FP64 GFLOP/s (standard QR flop count), % of FP64 peak",
             "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
             "config": {"workload": args.config, "desc": cfg["desc"], "m": cfg["m"], "n": cfg["n"],
                        "k": cfg["k"], "block": cfg["block"], "padding": cfg["padding"],
-                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                       "parallelism": (f"column-block-cyclic x{world} (NCCL)" if sharded
+                                       else "single GPU"),
                        "l2": "inputs larger than L2 (A is 8*m*n bytes)",
                        "input": "seeded numpy Gaussians; QR/products for the spectrum on GPU"},
             "pct_fp64_peak": (value / world / 1e3) / (peak["dmma_f64_tflops"] if peak else 37.2),
+            "pct_fp64_peak_note": "per GPU, of the measured DMMA peak",
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -1,0 +1,335 @@
+"""Column-block-cyclic multi-GPU RQRCP.
+
+Layout: global column position j lives on rank (j // b) % G at local index
+(j // (b G)) b + j % b, where b is the pivot block width.  Per block J
+(randomized.py:207-258 control flow, every branch decided identically on all
+ranks because every decision input is replicated and every kernel is
+deterministic):
+
+1. every rank holds the full ell x nt sample and runs the pivot-selection
+   kernel redundantly -> bitwise the same pivots everywhere;
+2. the swaps (i0+j, i0+piv[j]) become one net permutation of the touched
+   positions; columns whose source and destination ranks differ move with
+   point-to-point sends (``exchange_columns``);
+3. the owner of block-column J runs the panel kernel and broadcasts
+   (usable, Y, tau, T, R11);
+4. every rank updates ITS trailing columns: G = Y^T C, X = T^T G, C -= Y X;
+5. R12 (b x nt) is all-gathered in position order and every rank applies the
+   sample update redundantly (column-local math, replicated result).
+
+Data movement uses ``torch.distributed`` (NCCL over NVLink on GPUs; the
+exchange helpers are device-agnostic, so they are tested with gloo on CPU).
+The math runs in librqrcp_b200.so through the same C-ABI primitives as the
+single-GPU path.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+EPS = float(np.finfo(np.float64).eps)
+
+
+# ---------------------------------------------------------------- layout
+
+@dataclass(frozen=True)
+class BlockCyclic:
+    """Column-block-cyclic map of n column positions over `world` ranks."""
+
+    n: int
+    b: int
+    world: int
+
+    def owner(self, j: int) -> int:
+        return (j // self.b) % self.world
+
+    def local_index(self, j: int) -> int:
+        blk = j // self.b
+        return (blk // self.world) * self.b + j % self.b
+
+    def positions(self, rank: int) -> np.ndarray:
+        """Global positions held by `rank`, in local order."""
+        j = np.arange(self.n)
+        return j[(j // self.b) % self.world == rank]
+
+    def n_local(self, rank: int) -> int:
+        return int(self.positions(rank).size)
+
+    def first_local_at_or_after(self, rank: int, pos: int) -> int:
+        """Local index of the first column of `rank` whose position >= pos
+        (local columns are in increasing position order, so the tail from
+        here is contiguous)."""
+        p = self.positions(rank)
+        return int(np.searchsorted(p, pos))
+
+
+def shard(A: np.ndarray, layout: BlockCyclic, rank: int) -> np.ndarray:
+    """This rank's columns of A (host helper for setup and tests)."""
+    return np.asfortranarray(np.asarray(A)[:, layout.positions(rank)])
+
+
+# ---------------------------------------------------------------- swaps
+
+def swap_plan(piv, got: int, i0: int) -> list[tuple[int, int]]:
+    """Net effect of the ordered swaps (i0+j, i0+piv[j]), j < got
+    (randomized.py:138-147), as moves (dst_position, src_position) with
+    dst != src.  Applying every move simultaneously equals the sequence."""
+    cur: dict[int, int] = {}
+    for j in range(got):
+        a, c = i0 + j, i0 + int(piv[j])
+        if a == c:
+            continue
+        sa, sc = cur.get(a, a), cur.get(c, c)
+        cur[a], cur[c] = sc, sa
+    return [(d, s) for d, s in sorted(cur.items()) if d != s]
+
+
+def exchange_columns(local: torch.Tensor, layout: BlockCyclic, moves, rank: int,
+                     group=None) -> None:
+    """Apply a column permutation (dst <- src moves over global positions) to
+    the distributed matrix in place.  Columns whose source and destination
+    ranks differ are packed per peer and moved with one send/recv pair each."""
+    if not moves:
+        return
+    world = layout.world
+    li = layout.local_index
+    owner = layout.owner
+    # snapshot every source column this rank owns before anything is overwritten
+    mine_src = sorted({s for _, s in moves if owner(s) == rank})
+    snap = {s: local[:, li(s)].clone() for s in mine_src}
+    out_by_peer: dict[int, list[int]] = {}
+    in_by_peer: dict[int, list[tuple[int, int]]] = {}
+    for d, s in moves:
+        od, os_ = owner(d), owner(s)
+        if od == rank and os_ == rank:
+            local[:, li(d)] = snap[s]
+        elif os_ == rank:
+            out_by_peer.setdefault(od, []).append(s)
+        elif od == rank:
+            in_by_peer.setdefault(os_, []).append((d, s))
+    ops = []
+    sendbufs, recvbufs = [], []
+    for peer in range(world):
+        if peer == rank:
+            continue
+        if peer in out_by_peer:
+            buf = torch.stack([snap[s] for s in out_by_peer[peer]], dim=1).contiguous()
+            sendbufs.append(buf)
+            ops.append(dist.P2POp(dist.isend, buf, _grank(peer, group), group=group))
+        if peer in in_by_peer:
+            buf = torch.empty((local.shape[0], len(in_by_peer[peer])), dtype=local.dtype,
+                              device=local.device)
+            recvbufs.append((peer, buf))
+            ops.append(dist.P2POp(dist.irecv, buf, _grank(peer, group), group=group))
+    if ops:
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+    for peer, buf in recvbufs:
+        for col, (d, _s) in enumerate(in_by_peer[peer]):
+            local[:, li(d)] = buf[:, col]
+
+
+def _grank(r, group):
+    return r if group is None else dist.get_global_rank(group, r)
+
+
+# ---------------------------------------------------------------- gathers
+
+def allgather_positions(local_tail: torch.Tensor, layout: BlockCyclic, pos0: int, rank: int,
+                        group=None) -> torch.Tensor:
+    """All-gather every rank's columns with position >= pos0 (its contiguous
+    local tail) and assemble them in global position order: returns a
+    (rows x (n - pos0)) tensor on every rank."""
+    world = layout.world
+    rows = local_tail.shape[0]
+    counts = [int(np.sum(layout.positions(r) >= pos0)) for r in range(world)]
+    width = max(counts) if counts else 0
+    pad = torch.zeros((rows, width), dtype=local_tail.dtype, device=local_tail.device)
+    pad[:, : local_tail.shape[1]] = local_tail
+    flat = pad.t().contiguous()                      # (width x rows), one column per row
+    gathered = [torch.empty_like(flat) for _ in range(world)]
+    dist.all_gather(gathered, flat, group=group)
+    out = torch.empty((rows, layout.n - pos0), dtype=local_tail.dtype, device=local_tail.device)
+    for r in range(world):
+        p = layout.positions(r)
+        p = p[p >= pos0] - pos0
+        if p.size:
+            idx = torch.as_tensor(p, device=local_tail.device)
+            out[:, idx] = gathered[r][: p.size].t()
+    return out
+
+
+def broadcast(t: torch.Tensor, src: int, group=None) -> torch.Tensor:
+    dist.broadcast(t, _grank(src, group), group=group)
+    return t
+
+
+# ---------------------------------------------------------------- driver
+
+@dataclass
+class ShardedFactorization:
+    """Result of `rqrcp_sharded`: replicated reflectors/permutation, this
+    rank's R columns (``R_local``) and, when gathered, the full R."""
+
+    Y: torch.Tensor
+    tau: torch.Tensor
+    perm: np.ndarray
+    swaps: list
+    rank: int
+    R_local: torch.Tensor
+    R: torch.Tensor | None = None
+    layout: BlockCyclic | None = None
+    counters: dict = field(default_factory=dict)
+
+
+def rqrcp_sharded(A_local: torch.Tensor, m: int, n: int, k=None, config=None, group=None,
+                  gather_r: bool = True) -> ShardedFactorization:
+    """Full/partial RQRCP of the column-block-cyclic distributed A
+    (randomized.py:183-266 semantics) on the ranks of `group`, one GPU each."""
+    from . import primitives as K
+    from .device import fmat
+    from .randomized import RandomizedConfig, _validate_rank
+    from .rng import RngState, gaussian_matrix
+
+    config = config if config is not None else RandomizedConfig()
+    world = dist.get_world_size(group)
+    me = dist.get_rank(group)
+    b, ell = config.block, config.ell
+    layout = BlockCyclic(n, b, world)
+    k = _validate_rank(k, m, n)
+    if k == 0:
+        raise ValueError("rank must be >= 1")
+    if ell > m:
+        raise ValueError(f"sample rows {ell} exceed matrix rows {m}")
+    dev = A_local.device
+    nloc = layout.n_local(me)
+    work = fmat(m, nloc, dev)
+    work.copy_(A_local)
+    ss = (work * work).sum().reshape(1)
+    dist.all_reduce(ss, group=group)
+    frob = float(ss.sqrt().item())
+    tol = EPS * frob
+    rng = RngState(config.seed)
+    Y = fmat(m, k, dev, fill=0.0)
+    tau = torch.zeros(k, dtype=torch.float64, device=dev)
+    perm = np.arange(n)
+    swaps: list = []
+    ctr = {"gemm_flops": 0, "level2_flops": 0, "resamples": 0}
+
+    def sketch(i0: int) -> torch.Tensor:
+        om = torch.from_numpy(gaussian_matrix(rng, ell, m - i0)).to(dev)
+        lc = layout.first_local_at_or_after(me, i0)
+        local = K.gemm(_f(om), _f(work[i0:, lc:]))          # ell x local tail
+        ctr["gemm_flops"] += 2 * ell * (m - i0) * (n - i0)
+        return _f(allgather_positions(local, layout, i0, me, group))
+
+    B = sketch(0)
+    rank_out = k
+    i0 = 0
+    while i0 < k:
+        want = min(b, k - i0)
+        owner = layout.owner(i0)
+        resampled = False
+        while True:
+            S, piv, got, _, _, l2 = K.select_pivots(B, want)
+            ctr["level2_flops"] += l2
+            if got < want and not resampled:
+                B = sketch(i0)
+                ctr["resamples"] += 1
+                resampled = True
+                continue
+            if got == 0:
+                bw = 0
+                break
+            for j in range(got):
+                a, c = i0 + j, i0 + piv[j]
+                swaps.append((a, c))
+                if a != c:
+                    perm[[a, c]] = perm[[c, a]]
+            exchange_columns(work, layout, swap_plan(piv, got, i0), me, group)
+            meta = torch.zeros(1, dtype=torch.int64, device=dev)
+            lp = layout.local_index(i0)
+            if me == owner:
+                P = fmat(m - i0, got, dev)
+                P.copy_(work[i0:, lp:lp + got])
+                Yp, tp, T, usable, l2p = K.panel_qr(P, tol=tol, with_t=True)
+                meta[0] = usable
+                ctr["level2_flops"] += l2p
+            broadcast(meta, owner, group)
+            usable = int(meta.item())
+            if usable < got and not resampled:
+                B = sketch(i0)
+                ctr["resamples"] += 1
+                resampled = True
+                continue
+            bw = usable
+            if bw:
+                rows = max(m - i0, 2 * bw)
+                blk = fmat(rows, 2 * bw + 1, dev) if me != owner else None
+                if me == owner:
+                    work[i0:, lp:lp + bw] = P[:, :bw]
+                    Tb = K_t_factor(Yp[:, :bw], tp[:bw])
+                    blk = fmat(rows, 2 * bw + 1, dev, fill=0.0)
+                    blk[: m - i0, :bw] = Yp[:, :bw]
+                    blk[:bw, bw:2 * bw] = Tb
+                    blk[:bw, 2 * bw] = tp[:bw]
+                    blk[bw:2 * bw, bw:2 * bw] = P[:bw, :bw]      # R11 below T
+                broadcast(blk, owner, group)
+                Y[i0:, i0:i0 + bw] = blk[: m - i0, :bw]
+                tau[i0:i0 + bw] = blk[:bw, 2 * bw]
+                T = _f(blk[:bw, bw:2 * bw])
+                R11 = _f(blk[bw:2 * bw, bw:2 * bw])
+            break
+        if bw == 0:
+            rank_out = i0
+            break
+        # ---- block stages on my trailing columns (randomized.py:158-180)
+        nt2 = n - i0 - bw
+        lc = layout.first_local_at_or_after(me, i0 + bw)
+        Yb = _f(Y[i0:, i0:i0 + bw])
+        if nt2:
+            C = work[i0:, lc:]
+            if C.shape[1]:
+                G = K.gemm(Yb, _f(C), transa=True)
+                X = K.gemm(T, G, transa=True)
+                K.gemm(Yb, X, C, alpha=-1.0, beta=1.0)
+            mm = m - i0
+            ctr["gemm_flops"] += (2 * mm * bw * nt2 + bw * bw * nt2 + 2 * bw * bw * nt2
+                                  + (2 * (mm - bw) * bw * nt2 if i0 + bw < m else 0))
+        i0 += bw
+        if bw < want:
+            rank_out = i0
+            break
+        if i0 < k:
+            R12 = allgather_positions(_f(work[i0 - bw:i0, lc:]), layout, i0, me, group)
+            Bn, degenerate = K.sample_update(S, bw, R11, _f(R12), frob)
+            if degenerate:
+                B = sketch(i0)
+                ctr["resamples"] += 1
+            else:
+                B = Bn
+                ctr["gemm_flops"] += 3 * bw * bw * (n - i0)
+    R_local = work[:rank_out, :].clone()
+    R = _f(allgather_positions(R_local, layout, 0, me, group)) if gather_r else None
+    return ShardedFactorization(Y=Y[:, :rank_out], tau=tau[:rank_out], perm=perm, swaps=swaps,
+                                rank=rank_out, R_local=R_local, R=R, layout=layout,
+                                counters=ctr)
+
+
+def K_t_factor(Y, tau):
+    from .factorization import t_factor
+    return t_factor(Y, tau)
+
+
+def _f(t: torch.Tensor) -> torch.Tensor:
+    """Column-major copy (or view) of a 2-D tensor for the C-ABI."""
+    from .device import fmat, is_fortran
+    if is_fortran(t):
+        return t
+    out = fmat(t.shape[0], t.shape[1], t.device)
+    out.copy_(t)
+    return out

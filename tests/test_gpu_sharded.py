@@ -1,0 +1,50 @@
+"""The column-block-cyclic driver (paper_1509_06820_b200/parallel.py) on the
+B200 with a single-rank NCCL group must reproduce the native single-GPU
+driver: same pivots, same resamples, R to rounding."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from tests import _golden as G
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def group():
+    import torch
+    import torch.distributed as dist
+    if not dist.is_initialized():
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    yield None
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", ["rq_gauss_130x97_full", "rq_geom16_128_b8", "rq_gauss_60x45_k20",
+                                  "cfg1_rq_gauss_1000"])
+def test_sharded_world1_matches_native(group, name):
+    import torch
+    import paper_1509_06820_b200 as P
+    from paper_1509_06820_b200.parallel import rqrcp_sharded
+    rec = G.load(name)
+    A = G.matrix_of(rec)
+    cfg = P.RandomizedConfig(block=int(rec["block"]), padding=int(rec["padding"]),
+                             seed=int(rec["seed"]))
+    f = P.rqrcp(A, G.k_of(rec), cfg)
+    Ad = torch.from_numpy(np.asfortranarray(A)).cuda()
+    s = rqrcp_sharded(Ad, A.shape[0], A.shape[1], G.k_of(rec), cfg)
+    assert s.rank == f.rank
+    np.testing.assert_array_equal(s.perm, np.asarray(f.perm.forward))
+    assert s.counters["resamples"] == f.counters.resamples
+    R = s.R.cpu().numpy()
+    assert np.linalg.norm(R - f.R) <= 1e-12 * max(np.linalg.norm(f.R), 1e-300)
+    np.testing.assert_array_equal(np.array(s.swaps).reshape(-1, 2),
+                                  np.array(f.perm.swaps).reshape(-1, 2))
