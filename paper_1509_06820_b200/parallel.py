@@ -164,7 +164,12 @@ def allgather_positions(local_tail: torch.Tensor, layout: BlockCyclic, pos0: int
 
 
 def broadcast(t: torch.Tensor, src: int, group=None) -> torch.Tensor:
-    dist.broadcast(t, _grank(src, group), group=group)
+    """In-place broadcast; column-major matrices go through their (contiguous)
+    transposed view, which shares the storage."""
+    buf = t if t.is_contiguous() else t.t()
+    if not buf.is_contiguous():
+        raise ValueError("broadcast needs a dense row- or column-major tensor")
+    dist.broadcast(buf, _grank(src, group), group=group)
     return t
 
 
