@@ -54,6 +54,7 @@ struct PanArgs {
   // grid exchange
   unsigned int* bar;
   double* gpub;            // [2][Q][2*bw]
+  long long* dbg;          // optional phase timers (CTA 0, thread 0)
 };
 
 // 32 per-lane values -> lane l holds the warp sum of column l (31 shuffles,
@@ -101,6 +102,7 @@ __global__ void __launch_bounds__(kPanThreads, 1) panel_kernel(PanArgs a) {
   double* dsum = wpart + NW * bw;      // [bw]
   double* rowj = dsum + bw;            // [bw]
   double* taus = rowj + bw;            // [bw]
+  double* wsh = taus + bw;             // [bw] w of the current step
   __shared__ int s_usable;
   unsigned int epoch = 0;
   const int stride = 2 * bw;
@@ -164,8 +166,20 @@ __global__ void __launch_bounds__(kPanThreads, 1) panel_kernel(PanArgs a) {
   finish_partials(0);
 
   int64_t l2 = 0, l2b = 0;
+  long long tm[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tlast = clock64();
+  const bool timing = a.dbg != nullptr && me == 0 && tid == 0;
+  auto mark = [&](int k) {
+    if (timing) {
+      const long long t = clock64();
+      tm[k] += t - tlast;
+      tlast = t;
+    }
+  };
   for (int j = 0; j < ncols; ++j) {
+    mark(5);
     xsync();
+    mark(0);
     const int par = j & 1;
     const int owner = (int)(j / a.rpb);
     // (A) fixed-order reduction of the Q partial vectors
@@ -194,6 +208,7 @@ __global__ void __launch_bounds__(kPanThreads, 1) panel_kernel(PanArgs a) {
       dsum[c] = d;
     }
     __syncthreads();
+    mark(1);
     // (B) reflector scalars (kernels.py:35-44), computed redundantly by every thread
     const double alpha = rowj[j];
     const double norm = sqrt(__fma_rn(alpha, alpha, dsum[j]));
@@ -205,6 +220,8 @@ __global__ void __launch_bounds__(kPanThreads, 1) panel_kernel(PanArgs a) {
       tau = __ddiv_rn(__dsub_rn(beta, alpha), beta);
     }
     const double rinv = zero ? 0.0 : 1.0 / den;
+    // w_c = P[j,c] + (sum_{r>j} x_r P[r,c]) / (alpha - beta), once per column
+    for (int c = j + 1 + tid; c < bw; c += kPanThreads) wsh[c] = __fma_rn(dsum[c], rinv, rowj[c]);
     if (tid == 0) {
       taus[j] = tau;
       if (s_usable == ncols && fabs(beta) <= a.tol) s_usable = j;  // _panel_rank
@@ -232,8 +249,10 @@ __global__ void __launch_bounds__(kPanThreads, 1) panel_kernel(PanArgs a) {
         rr[j] = diag ? beta : v;
       }
     }
+    mark(2);
     if (!more) break;
-    const double w1 = __fma_rn(dsum[j + 1], rinv, rowj[j + 1]);
+    __syncthreads();  // wsh complete
+    const double w1 = wsh[j + 1];
     // updated x' = P'[r, j+1] of my rows, before any chunk rewrites column j+1
     double x1r[kRowsPerThread];
 #pragma unroll
@@ -262,7 +281,7 @@ __global__ void __launch_bounds__(kPanThreads, 1) panel_kernel(PanArgs a) {
             const int c = cb + i;
             if (c < bw) {
               double nv = rr[c];
-              if (tau != 0.0) nv = __dsub_rn(nv, __dmul_rn(tv, __fma_rn(dsum[c], rinv, rowj[c])));
+              if (tau != 0.0) nv = __dsub_rn(nv, __dmul_rn(tv, wsh[c]));
               rr[c] = nv;
               if (below) d[i] = __fma_rn(x1, nv, d[i]);
             }
@@ -272,7 +291,13 @@ __global__ void __launch_bounds__(kPanThreads, 1) panel_kernel(PanArgs a) {
       const double s = warp_transpose_sum(d);
       if (cb + lane < bw) wpart[warp * bw + cb + lane] = s;
     }
+    mark(3);
     finish_partials(j + 1);
+    mark(4);
+  }
+  if (timing) {
+    for (int k = 0; k < 6; ++k) a.dbg[k] = tm[k];
+    a.dbg[7] = ncols;
   }
   xsync();  // every CTA is done reading the others' partials
 
@@ -326,7 +351,7 @@ void panel_qr(Handle& h, int64_t mm, int64_t bw, const double* P, int64_t ldp,
   const int rpb = (int)((mm + Q - 1) / Q);
   if (rpb > kRowsPerThread * kPanThreads) throw InvalidArg("panel too tall for the kernel");
   const int ldl = (int)(bw | 1);
-  const size_t aux = ((size_t)4 * bw + (size_t)(kPanThreads / 32) * bw + 3 * (size_t)bw + 8) * 8;
+  const size_t aux = ((size_t)4 * bw + (size_t)(kPanThreads / 32) * bw + 4 * (size_t)bw + 8) * 8;
   if (aux > h.smem_optin - 4096) throw InvalidArg("panel too wide for shared memory");
   const size_t rowbytes = (size_t)ldl * 8;
   const int nrs = (int)std::min<size_t>(rpb, (h.smem_optin - 4096 - aux) / rowbytes);
@@ -340,6 +365,7 @@ void panel_qr(Handle& h, int64_t mm, int64_t bw, const double* P, int64_t ldp,
   a.gstore = nrs < rpb ? (double*)h.buf("pan_gstore", (size_t)Q * (rpb - nrs) * rowbytes, s)
                        : nullptr;
   a.rpb = rpb; a.ldl = ldl; a.nrs = nrs;
+  a.dbg = h.dbg;
   {
     ProfScope prof(h, kProfPanel, 2.0 * mm * bw * bw, 16.0 * mm * bw, s);
     count_launch();

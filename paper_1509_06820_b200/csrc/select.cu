@@ -48,37 +48,29 @@ struct SelArgs {
   int cpb, ldl, ncs;
   // grid exchange (global/L2)
   unsigned int* bar;
-  double* gval;     // [2][P]
-  int* gpos;        // [2][P]
-  double* gcol;     // [2][P][ell]
+  unsigned long long* gkey;  // [3] rotating candidate keys
+  double* gcol;     // [2][P][ell+1]
   double* gsq;      // [P]
   long long* dbg;   // optional phase timers (CTA 0, thread 0): [8] cycles
 };
 
-struct Cand {
-  double val;
-  int pos;   // logical position (tie-break: lowest wins)
-  int idx;   // local column (publish) or owner CTA (reduce)
-};
-RQ_DEV bool better(const Cand& a, const Cand& b) {
-  return a.val > b.val || (a.val == b.val && a.pos < b.pos);
-}
-RQ_DEV Cand warp_best(Cand c) {
-#pragma unroll
-  for (int off = 16; off; off >>= 1) {
-    Cand o;
-    o.val = __shfl_xor_sync(0xffffffffu, c.val, off);
-    o.pos = __shfl_xor_sync(0xffffffffu, c.pos, off);
-    o.idx = __shfl_xor_sync(0xffffffffu, c.idx, off);
-    if (better(o, c)) c = o;
-  }
-  return c;
-}
 RQ_DEV double warp_sum(double v) {
 #pragma unroll
   for (int off = 16; off; off >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
   return v;
 }
+
+// Packed argmax key: the top 48 bits of the (non-negative) norm's IEEE
+// pattern, then the complemented 16-bit logical position (ties -> lowest
+// position, np.argmax first-max).  Unsigned order of keys = reference order
+// of candidates up to a 2^-36 relative norm resolution (a near-tie far inside
+// the downdating error).  0 = no candidate.  The owner CTA of a position is
+// read from a position -> owner map every CTA keeps identically.
+RQ_DEV unsigned long long make_key(double nrm, int pos) {
+  const unsigned long long hi = ((unsigned long long)__double_as_longlong(nrm)) >> 16;
+  return (hi << 16) | (unsigned long long)(0xFFFF - pos);
+}
+RQ_DEV int key_pos(unsigned long long k) { return 0xFFFF - (int)(k & 0xFFFF); }
 
 template <bool kCluster>
 __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
@@ -104,23 +96,42 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
   auto colp = [&](int c) -> double* {
     return c < ncs ? sm + (size_t)c * ldl : gsp + (size_t)(c - ncs) * ldl;
   };
+  const int cstride = ell + 1;               // published column + its exact norm
   double* meta = sm + (size_t)ncs * ldl;
-  double* vw = meta;                         // [NW][2][ell] per-warp v and tau*v
-  double* ccol = vw + (size_t)NW * 2 * ell;  // [2][ell] my published candidate column
-  double* nrm = ccol + 2 * ell;              // [cpb]
+  double* vbuf = meta;                       // [ell] v
+  double* tvbuf = vbuf + ell;                // [ell] tau*v
+  double* ccol = tvbuf + ell;                // [2][ell+1] my published candidate (cluster)
+  double* nrm = ccol + 2 * cstride;          // [cpb]
   double* orig = nrm + a.cpb;                // [cpb]
   int* pos = (int*)(orig + a.cpb);           // [cpb]
-  __shared__ Cand s_red[NW];
-  __shared__ int s_lc[2];
-  __shared__ double s_cval[2][kMaxCluster];  // candidates pushed by every peer (cluster)
-  __shared__ int s_cpos[2][kMaxCluster];
+  unsigned char* omap = (unsigned char*)(pos + a.cpb);  // [nt] position -> owner CTA
+  __shared__ unsigned long long s_key[3][kMaxCluster];  // pushed candidate keys [slot][src]
+  __shared__ unsigned long long s_bkey;      // block best key
   __shared__ double s_sq[kMaxCluster];
   __shared__ double s_all[160];
+  __shared__ double s_step[2];
+  __shared__ int s_stepi[2];
   unsigned int epoch = 0;
 
   auto xsync = [&]() {
     if constexpr (kCluster) cg::this_cluster().sync();
     else grid_barrier(a.bar, epoch);
+  };
+  // cluster-wide best key of a slot: max over the per-source entries (cluster)
+  // or the global atomic max (grid); warp 0 only
+  auto slot_max = [&](int slot) -> unsigned long long {
+    unsigned long long k = 0ull;
+    if constexpr (kCluster) {
+      if (lane < P) k = s_key[slot][lane];
+#pragma unroll
+      for (int off = 16; off; off >>= 1) {
+        const unsigned long long o = __shfl_xor_sync(0xffffffffu, k, off);
+        k = o > k ? o : k;
+      }
+    } else {
+      k = __ldcg(a.gkey + slot);
+    }
+    return k;
   };
 
   // ---- load my columns; initial norms (pairwise, bit-identical to numpy)
@@ -132,6 +143,9 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
       colp(c)[i] = a.B[(size_t)(c0 + c) * a.ldb + i];
     }
   }
+  for (int e = tid; e < 3 * kMaxCluster; e += kSelThreads) (&s_key[0][0])[e] = 0ull;
+  for (int q = tid; q < a.nt; q += kSelThreads) omap[q] = (unsigned char)(q / a.cpb);
+  if (!kCluster && me == 0 && tid < 3) a.gkey[tid] = 0ull;
   __syncthreads();
   double mysq = 0.0;
   for (int c = tid; c < ncol; c += kSelThreads) {
@@ -144,11 +158,12 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
   }
   {
     const double v = warp_sum(mysq);
-    if (lane == 0) s_red[warp].val = v;
+    if (lane == 0) s_all[warp] = v;
     __syncthreads();
     if (tid == 0) {
       double t = 0.0;
-      for (int w = 0; w < NW; ++w) t = __dadd_rn(t, s_red[w].val);
+      for (int w = 0; w < NW; ++w) t = __dadd_rn(t, s_all[w]);
+      s_bkey = 0ull;
       if constexpr (kCluster) {
         for (int q = 0; q < P; ++q) cg::this_cluster().map_shared_rank(s_sq, q)[me] = t;
       } else {
@@ -156,40 +171,34 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
       }
     }
   }
+  xsync();  // key slots are zero everywhere before anyone publishes
 
-  // block argmax over my active columns -> publish into slot `par`
-  auto publish = [&](int jstart, int par) {
-    Cand best{-1.0, kNoPos, -1};
-    for (int c = tid; c < ncol; c += kSelThreads)
-      if (pos[c] >= jstart) {
-        Cand cc{nrm[c], pos[c], c};
-        if (better(cc, best)) best = cc;
-      }
-    best = warp_best(best);
-    if (lane == 0) s_red[warp] = best;
+  // publish my block's best candidate (group leaders already atomically
+  // maxed their keys into s_bkey) into key slot `slot`, column parity `par`
+  auto publish = [&](int slot, int par) {
     __syncthreads();
-    if (warp == 0) {
-      Cand b = lane < NW ? s_red[lane] : Cand{-1.0, kNoPos, -1};
-      b = warp_best(b);
-      const int lc = b.idx;
+    const unsigned long long bk = s_bkey;
+    if (bk != 0ull) {
       if constexpr (kCluster) {
-        if (lane < P) {  // push (value, position) into every peer's candidate table
-          cg::this_cluster().map_shared_rank(&s_cval[par][0], lane)[me] = b.val;
-          cg::this_cluster().map_shared_rank(&s_cpos[par][0], lane)[me] = b.pos;
-        }
-      } else if (lane == 0) {
-        a.gval[par * P + me] = b.val;
-        a.gpos[par * P + me] = b.pos;
+        if (tid < P) cg::this_cluster().map_shared_rank(&s_key[slot][0], tid)[me] = bk;
+      } else {
+        if (tid == 0) atomicMax(a.gkey + slot, bk);
       }
-      if (lane == 0) s_lc[par] = lc;
-      if (lc >= 0) {
-        const double* src = colp(lc);
-        double* dst = kCluster ? ccol + par * ell : a.gcol + ((size_t)par * P + me) * ell;
-        for (int i = lane; i < ell; i += 32) dst[i] = src[i];
+      // the winning group copies its column (+ exact norm) to the publish slot
+      const int bpos = key_pos(bk);
+      for (int c = grp; c < ncol; c += NG) {
+        if (pos[c] != bpos) continue;
+        const double* src = colp(c);
+        double* dst = kCluster ? ccol + par * cstride : a.gcol + ((size_t)par * P + me) * cstride;
+        for (int i = gl; i < ell; i += 8) dst[i] = src[i];
+        if (gl == 0) dst[ell] = nrm[c];
       }
     }
   };
 
+  // step-0 candidates
+  for (int c = grp; c < ncol; c += NG)
+    if (gl == 0) atomicMax(&s_bkey, make_key(nrm[c], pos[c]));
   publish(0, 0);
   xsync();
   double tol;
@@ -216,41 +225,40 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
       tlast = t;
     }
   };
-  double* myv = vw;          // v and tau*v (written by warp 0)
-  double* mytv = vw + ell;
-  __shared__ double s_step[2];
-  __shared__ int s_stepi[2];
   for (int j = 0; j < a.want; ++j) {
     const int par = j & 1;
-    // ---- warp 0: winner among the P candidates (order independent) and the
-    //      reflector (kernels.py:26-44); the rest of the CTA waits at one barrier
+    // ---- warp 0: winner (one key read) and the reflector (kernels.py:26-44)
     if (warp == 0) {
-      Cand win{-1.0, kNoPos, -1};
-      for (int q = lane; q < P; q += 32) {
-        double v;
-        int p;
-        if constexpr (kCluster) {
-          v = s_cval[par][q];
-          p = s_cpos[par][q];
-        } else {
-          v = a.gval[par * P + q];
-          p = a.gpos[par * P + q];
-        }
-        Cand cc{v, p, q};
-        if (p != kNoPos && better(cc, win)) win = cc;
-      }
-      win = warp_best(win);
-      const bool halt = win.idx < 0 || !(win.val > tol);  // qrcp.py:69-71
-      if (!halt) {
+      const unsigned long long wk = slot_max(j % 3);
+      const int owner = wk ? (int)omap[key_pos(wk)] : -1;
+      double xv[5];  // ell <= 160
+      double xnorm = -1.0;
+      if (owner >= 0) {
         const double* xc;
-        if constexpr (kCluster) xc = cg::this_cluster().map_shared_rank(ccol, win.idx) + par * ell;
-        else xc = a.gcol + ((size_t)par * P + win.idx) * ell;
-        double xv[5];  // ell <= 160
+        if constexpr (kCluster) {
+          xc = cg::this_cluster().map_shared_rank(ccol, owner) + par * cstride;
+#pragma unroll
+          for (int k = 0; k < 5; ++k) {
+            const int i = lane + 32 * k;
+            xv[k] = i < ell ? xc[i] : 0.0;
+          }
+          xnorm = xc[ell];
+        } else {
+          xc = a.gcol + ((size_t)par * P + owner) * cstride;
+#pragma unroll
+          for (int k = 0; k < 5; ++k) {
+            const int i = lane + 32 * k;
+            xv[k] = i < ell ? __ldcg(xc + i) : 0.0;
+          }
+          xnorm = __ldcg(xc + ell);
+        }
+      }
+      const bool halt = owner < 0 || !(xnorm > tol);  // qrcp.py:69-71
+      if (!halt) {
         double sq = 0.0;
 #pragma unroll
         for (int k = 0; k < 5; ++k) {
           const int i = lane + 32 * k;
-          xv[k] = i < ell ? xc[i] : 0.0;
           if (i >= j && i < ell) sq = __fma_rn(xv[k], xv[k], sq);
         }
         sq = warp_sum(sq);
@@ -273,8 +281,8 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
           const int i = lane + 32 * k;
           if (i >= j && i < ell) {
             const double v = (i == j) ? 1.0 : (zero ? xv[k] : __ddiv_rn(xv[k], den));
-            myv[i] = v;
-            mytv[i] = __dmul_rn(tau, v);
+            vbuf[i] = v;
+            tvbuf[i] = __dmul_rn(tau, v);
           }
         }
         if (lane == 0) {
@@ -283,8 +291,21 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
         }
       }
       if (lane == 0) {
-        s_stepi[0] = halt ? -1 : win.idx;
-        s_stepi[1] = win.pos;
+        s_stepi[0] = halt ? -1 : owner;
+        s_stepi[1] = key_pos(wk);
+        if (!halt) {  // the swap j <-> p moves the owners too
+          const int pp = key_pos(wk);
+          const unsigned char oj = omap[j];
+          omap[j] = omap[pp];
+          omap[pp] = oj;
+        }
+        s_bkey = 0ull;
+        // recycle the slot read two steps ago (every CTA passed a sync since)
+        if constexpr (kCluster) {
+          for (int q = 0; q < P; ++q) s_key[(j + 2) % 3][q] = 0ull;
+        } else if (me == 0) {
+          a.gkey[(j + 2) % 3] = 0ull;
+        }
       }
     }
     __syncthreads();
@@ -295,8 +316,6 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
       break;
     }
     const double beta = s_step[0], tau = s_step[1];
-    mark(1);
-    const int lc_piv = s_lc[par];
     if (me == 0 && tid == 0) {
       a.piv[j] = p;
       if (a.taus) a.taus[j] = tau;
@@ -307,16 +326,17 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
       }
     }
     if (me == 0 && a.Ys && warp == 0)
-      for (int i = lane; i < ell; i += 32) a.Ys[(size_t)j * a.ldys + i] = i < j ? 0.0 : myv[i];
+      for (int i = lane; i < ell; i += 32) a.Ys[(size_t)j * a.ldys + i] = i < j ? 0.0 : vbuf[i];
+    mark(1);
     // ---- my columns, one 8-lane group per column: relabel (swap j <-> p),
-    //      pivot column, apply H_j, downdate
+    //      pivot column, apply H_j, downdate, next-step candidate key
     for (int c = grp; c < ncol; c += NG) {
       double* col = colp(c);
       // read the column state before any lane of the group writes it
       int pc = pos[c];
       const double nv = nrm[c], og = orig[c];
       __syncwarp(gmask);
-      if (owner == me && c == lc_piv) {
+      if (pc == p) {
         // pivot column: rows < j keep R, row j = beta, below = 0 (qrcp.py:80-81)
         for (int i = j + gl; i < ell; i += 8) col[i] = (i == j) ? beta : 0.0;
         if (gl == 0) pos[c] = j;
@@ -331,16 +351,17 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
         double d0 = 0.0, d1 = 0.0;
         int i = j + gl;
         for (; i + 8 < ell; i += 16) {
-          d0 = __fma_rn(myv[i], col[i], d0);
-          d1 = __fma_rn(myv[i + 8], col[i + 8], d1);
+          d0 = __fma_rn(vbuf[i], col[i], d0);
+          d1 = __fma_rn(vbuf[i + 8], col[i + 8], d1);
         }
-        if (i < ell) d0 = __fma_rn(myv[i], col[i], d0);
+        if (i < ell) d0 = __fma_rn(vbuf[i], col[i], d0);
         double w = __dadd_rn(d0, d1);
 #pragma unroll
         for (int off = 4; off; off >>= 1) w = __dadd_rn(w, __shfl_xor_sync(gmask, w, off, 8));
 #pragma unroll 2
-        for (int r = j + gl; r < ell; r += 8) col[r] = __dsub_rn(col[r], __dmul_rn(mytv[r], w));
+        for (int r = j + gl; r < ell; r += 8) col[r] = __dsub_rn(col[r], __dmul_rn(tvbuf[r], w));
       }
+      double nn = nv;
       if (j + 1 < a.nt) {
         // NormTracker.downdate with row j of the updated sample (kernels.py:222-233)
         __syncwarp(gmask);
@@ -348,23 +369,24 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
         double nsq = __dsub_rn(__dmul_rn(nv, nv), __dmul_rn(row, row));
         nsq = nsq > 0.0 ? nsq : 0.0;
         if (!(nsq < __dmul_rn(kGuard, og))) {
-          if (gl == 0) nrm[c] = sqrt(nsq);
+          nn = sqrt(nsq);
+          if (gl == 0) nrm[c] = nn;
         } else {
           double s0 = 0.0;
           for (int r = j + 1 + gl; r < ell; r += 8) s0 = __fma_rn(col[r], col[r], s0);
 #pragma unroll
           for (int off = 4; off; off >>= 1) s0 = __dadd_rn(s0, __shfl_xor_sync(gmask, s0, off, 8));
-          const double fresh = sqrt(s0);
+          nn = sqrt(s0);
           if (gl == 0) {
-            nrm[c] = fresh;
-            orig[c] = __dmul_rn(fresh, fresh);
+            nrm[c] = nn;
+            orig[c] = __dmul_rn(nn, nn);
           }
         }
+        if (gl == 0) atomicMax(&s_bkey, make_key(nn, pc));
       }
     }
-    __syncthreads();  // norms/positions written by the groups are read by publish
     mark(2);
-    publish(j + 1, par ^ 1);
+    publish((j + 1) % 3, par ^ 1);
     mark(3);
     xsync();
     mark(4);
@@ -373,7 +395,6 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
     for (int k = 0; k < 5; ++k) a.dbg[k] = tm[k];
     a.dbg[7] = a.want;
   }
-
   __syncthreads();
   // ---- write the transformed sample in pivoted order (group per column)
   for (int c = grp; c < ncol; c += NG) {
@@ -403,11 +424,12 @@ void select_pivots(Handle& h, int64_t ell, int64_t nt, int64_t want, const doubl
     throw InvalidArg("cannot select " + std::to_string(want) + " pivots from a " +
                      std::to_string(ell) + " x " + std::to_string(nt) + " sample");
   if (ell > 160) throw InvalidArg("sample rows > 160 not supported by the pivot kernel");
+  if (nt > 65535) throw InvalidArg("sample wider than 65535 columns");
   const bool grid = h.force_select == 1 ||
                     (h.force_select == 0 && nt > h.select_cluster_max_cols);
   int P;
   if (grid) {
-    P = (int)std::min<int64_t>(std::min(h.num_sms, 160), (nt + 31) / 32);
+    P = (int)std::min<int64_t>(std::min(h.num_sms, 160), (nt + 31) / 32);  // owner ids fit a byte
     P = std::max(P, 1);
     const int cpb = (int)((nt + P - 1) / P);
     P = (int)((nt + cpb - 1) / cpb);
@@ -418,8 +440,8 @@ void select_pivots(Handle& h, int64_t ell, int64_t nt, int64_t want, const doubl
   const int cpb = (int)((nt + P - 1) / P);
   if (cpb > 8192) throw InvalidArg("sample too wide for the pivot kernel");
   const int ldl = (int)(ell | 1);
-  const size_t meta = ((size_t)(kSelThreads / 32) * 2 * ell + 2 * ell + 2 * (size_t)cpb + 16) * 8 +
-                      (size_t)cpb * 4 + 256;
+  const size_t meta = ((size_t)2 * ell + 2 * (ell + 1) + 2 * (size_t)cpb + 16) * 8 +
+                      (size_t)cpb * 4 + (size_t)nt + 256;
   const size_t colbytes = (size_t)ldl * 8;
   const int ncs = (int)std::min<size_t>(cpb, (h.smem_optin - 4096 - meta) / colbytes);
   const size_t smem = (size_t)ncs * colbytes + meta;
@@ -439,9 +461,8 @@ void select_pivots(Handle& h, int64_t ell, int64_t nt, int64_t want, const doubl
   count_launch();
   if (grid) {
     a.bar = (unsigned int*)h.buf("sel_bar", 64, s);
-    a.gval = (double*)h.buf("sel_gval", (size_t)2 * P * 8, s);
-    a.gpos = (int*)h.buf("sel_gpos", (size_t)2 * P * 4, s);
-    a.gcol = (double*)h.buf("sel_gcol", (size_t)2 * P * ell * 8, s);
+    a.gkey = (unsigned long long*)h.buf("sel_gkey", 64, s);
+    a.gcol = (double*)h.buf("sel_gcol", (size_t)2 * P * (ell + 1) * 8, s);
     a.gsq = (double*)h.buf("sel_gsq", (size_t)P * 8, s);
     RQ_CUDA(cudaMemsetAsync(a.bar, 0, 64, s));
     static size_t attr = 0;
