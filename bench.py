@@ -303,11 +303,13 @@ def main():
             raise SystemExit("multi-GPU bench: only the RQRCP configs are sharded")
         cfgP = P.RandomizedConfig(block=cfg["block"], padding=cfg["padding"], seed=0)
 
-        def run_ours(P_, cfg_, A_, _x):  # noqa: F811 - sharded step
+        def step(P_, cfg_, A_, _x):
             return rqrcp_sharded(A_loc, cfg_["m"], cfg_["n"], cfg_["k"], cfgP, gather_r=False)
         A = None
+    else:
+        step = run_ours
     for _ in range(args.warmup):
-        f = run_ours(P, cfg, A, None)
+        f = step(P, cfg, A, None)
     barrier()
     _abi.check(lib.rq_profile_reset(h))
     _abi.check(lib.rq_profile_enable(h, 1))
@@ -318,7 +320,7 @@ def main():
         barrier()
         e0.record(stream)
         for _ in range(args.steps):
-            f = run_ours(P, cfg, A, None)
+            f = step(P, cfg, A, None)
         e1.record(stream)
         barrier()
     launches = lib.rq_launch_count() - launches0

@@ -129,6 +129,25 @@ def _counters(res):
                       bytes_touched=int(res.bytes_touched), resamples=int(res.resamples))
 
 
+def to_host_many(*ts):
+    """D2H of several device tensors into pinned host buffers (torch's caching
+    host allocator recycles them across calls), one stream sync, numpy views;
+    column-major layouts are kept (no host-side reshuffle)."""
+    outs = []
+    for t in ts:
+        if t is None:
+            outs.append(None)
+            continue
+        if t.dim() == 2 and t.stride(0) == 1 and t.shape[1] > 1:
+            h = torch.empty((t.shape[1], t.shape[0]), dtype=t.dtype, pin_memory=True).t()
+        else:
+            h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t, non_blocking=True)
+        outs.append(h)
+    torch.cuda.current_stream().synchronize()
+    return tuple(None if h is None else h.numpy() for h in outs)
+
+
 def _swap_list(swaps, n):
     pairs = swaps[: 2 * n].view(-1, 2).cpu().numpy()
     return [(int(a), int(b)) for a, b in pairs]
@@ -151,9 +170,7 @@ def package(out, host, trailing_update=True, truncated=False):
         trailing = out["work"][rank:, rank:] if trailing_update else None
     perm = out["perm"]
     if host:
-        # one D2H copy per output, layout kept (column-major), no host-side reshuffle
-        cv = lambda t: None if t is None else t.cpu().numpy()  # noqa: E731
-        Y, tau, R, W, trailing, perm = cv(Y), cv(tau), cv(R), cv(W), cv(trailing), cv(perm)
+        Y, tau, R, W, trailing, perm = to_host_many(Y, tau, R, W, trailing, perm)
     else:
         R = R.clone()
         trailing = trailing.clone() if trailing is not None else None

@@ -136,7 +136,8 @@ def tuxv(A, k, config=None, j_max=1, svd_of_x=False, omega=None):
         X = torch.diag(sx)
     counters = _counters(res.f)
     if host:
-        U, V, X = U.cpu().numpy(), V.cpu().numpy(), X.cpu().numpy()
+        from .randomized import to_host_many
+        U, V, X = to_host_many(U, V, X)
     else:
         U, V, X = U.clone(), V.clone(), X.clone()
     return TuxvFactorization(U=U, V=V, X=X, iterations=j_max, rank=r, counters=counters)
