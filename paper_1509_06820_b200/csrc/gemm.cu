@@ -21,10 +21,10 @@ __global__ void gemm_reduce_kernel(GemmArgs g) {
 
 namespace {
 
-template <bool TA, bool TB, int BM, int BN, int BK, int WM, int WN, int ST>
+template <bool TA, bool TB, int BM, int BN, int BK, int WM, int WN, int ST, int VEC>
 void launch_cfg(Handle& h, GemmArgs g, cudaStream_t s) {
   using Cfg = GemmCfg<TA, TB, BM, BN, BK, WM, WN, ST>;
-  auto kern = gemm_f64_kernel<TA, TB, BM, BN, BK, WM, WN, ST>;
+  auto kern = gemm_f64_kernel<TA, TB, BM, BN, BK, WM, WN, ST, VEC>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
     RQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -64,13 +64,26 @@ void launch_cfg(Handle& h, GemmArgs g, cudaStream_t s) {
   }
 }
 
-template <bool TA, bool TB>
-void launch_t(Handle& h, const GemmArgs& g, cudaStream_t s) {
+template <bool TA, bool TB, int VEC>
+void launch_v(Handle& h, const GemmArgs& g, cudaStream_t s) {
   const int64_t tiles128 = ((g.M + 127) / 128) * ((g.N + 63) / 64);
   if (g.M >= 128 && tiles128 >= 2LL * h.num_sms)
-    launch_cfg<TA, TB, 128, 64, 16, 32, 32, 3>(h, g, s);
+    launch_cfg<TA, TB, 128, 64, 16, 32, 32, 3, VEC>(h, g, s);
   else
-    launch_cfg<TA, TB, 64, 64, 16, 32, 32, 3>(h, g, s);
+    launch_cfg<TA, TB, 64, 64, 16, 32, 32, 3, VEC>(h, g, s);
+}
+
+// 16-byte copies need 16-byte aligned bases and even leading dimensions
+bool aligned16(const double* p, int64_t ld) {
+  return ((uintptr_t)p & 15) == 0 && (ld % 2) == 0;
+}
+
+template <bool TA, bool TB>
+void launch_t(Handle& h, const GemmArgs& g, cudaStream_t s) {
+  if (h.gemm_vec16 && aligned16(g.A, g.lda) && aligned16(g.B, g.ldb))
+    launch_v<TA, TB, 2>(h, g, s);
+  else
+    launch_v<TA, TB, 1>(h, g, s);
 }
 
 }  // namespace

@@ -39,6 +39,11 @@ RQ_DEV void cp_async8(void* smem, const void* gmem, bool pred) {
   const int sz = pred ? 8 : 0;
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
 }
+// 16-byte copy of up to two doubles; bytes beyond `valid` (0, 8, 16) are zero-filled
+RQ_DEV void cp_async16(void* smem, const void* gmem, int valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(valid));
+}
 RQ_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 RQ_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
@@ -59,18 +64,27 @@ RQ_DEV double gemm_combine(double acc, double c, double alpha, double beta) {
   return __dadd_rn(__dmul_rn(alpha, acc), __dmul_rn(beta, c));
 }
 
+// Shared tiles follow the operand's contiguous global direction so every
+// copy is contiguous on both sides (16-byte cp.async when aligned, no write
+// bank conflicts):
+//   A: !TA -> As[k][m] (ld BM+4)     TA -> As[m][k] (ld BK+4)
+//   B:  TB -> Bs[k][n] (ld BN+4)    !TB -> Bs[n][k] (ld BK+4)
+// Each padded leading dimension is 4 (mod 16) doubles, so the DMMA fragment
+// loads (8 rows x 4 k per warp) hit distinct banks within each half-warp.
 template <bool TA, bool TB, int BM, int BN, int BK, int WM, int WN, int STAGES>
 struct GemmCfg {
   static constexpr int kWarpsM = BM / WM, kWarpsN = BN / WN;
   static constexpr int kThreads = kWarpsM * kWarpsN * 32;
-  static constexpr int kLdA = BM + 4, kLdB = BN + 4;  // (BM+4) % 16 == 4
-  static constexpr int kTileA = BK * kLdA, kTileB = BK * kLdB;
+  static constexpr int kLdA = TA ? BK + 4 : BM + 4;
+  static constexpr int kLdB = TB ? BN + 4 : BK + 4;
+  static constexpr int kTileA = TA ? BM * kLdA : BK * kLdA;
+  static constexpr int kTileB = TB ? BK * kLdB : BN * kLdB;
   static constexpr size_t kSmem = (size_t)STAGES * (kTileA + kTileB) * sizeof(double);
-  static_assert(BM % 16 == 0 && BN % 16 == 0, "pad trick needs multiples of 16");
-  static_assert(WM % 8 == 0 && WN % 8 == 0 && BK % 4 == 0, "fragment shape");
+  static_assert(BM % 16 == 0 && BN % 16 == 0 && BK % 16 == 0, "pad trick needs multiples of 16");
+  static_assert(WM % 8 == 0 && WN % 8 == 0, "fragment shape");
 };
 
-template <bool TA, bool TB, int BM, int BN, int BK, int WM, int WN, int STAGES>
+template <bool TA, bool TB, int BM, int BN, int BK, int WM, int WN, int STAGES, int VEC>
 __global__ void __launch_bounds__(GemmCfg<TA, TB, BM, BN, BK, WM, WN, STAGES>::kThreads)
     gemm_f64_kernel(GemmArgs g) {
   using Cfg = GemmCfg<TA, TB, BM, BN, BK, WM, WN, STAGES>;
@@ -88,27 +102,33 @@ __global__ void __launch_bounds__(GemmCfg<TA, TB, BM, BN, BK, WM, WN, STAGES>::k
   const int64_t kend = imin64(g.K, kbeg + g.kchunk);
   const int ktiles = kbeg < kend ? (int)((kend - kbeg + BK - 1) / BK) : 0;
 
+  // copy an (outer x inner) tile whose inner index is contiguous in global
+  // memory (element (o, i) at src + i + o * ld) into dst[o * lds + i]
+  auto copy_tile = [&](double* dst, int lds, const double* src, int64_t ld, int outer, int inner,
+                       int64_t o0, int64_t i0, int64_t olim, int64_t ilim) {
+    constexpr int V = VEC;
+    const int per = inner / V;
+#pragma unroll
+    for (int e = tid; e < outer * per; e += NT) {
+      const int o = e / per, i = (e % per) * V;
+      const int64_t go = o0 + o, gi = i0 + i;
+      const double* p = src + gi + go * ld;
+      if (V == 2) {
+        const int valid = go < olim ? (gi + 1 < ilim ? 16 : (gi < ilim ? 8 : 0)) : 0;
+        cp_async16(dst + o * lds + i, valid ? p : src, valid);
+      } else {
+        const bool ok = go < olim && gi < ilim;
+        cp_async8(dst + o * lds + i, ok ? p : src, ok);
+      }
+    }
+  };
   auto load_tile = [&](int slot, int64_t k0) {
     double* as = As + slot * Cfg::kTileA;
     double* bs = Bs + slot * Cfg::kTileB;
-#pragma unroll
-    for (int e = tid; e < BM * BK; e += NT) {
-      int i, kk;
-      if (!TA) { i = e % BM; kk = e / BM; } else { kk = e % BK; i = e / BK; }
-      const int64_t gi = m0 + i, gk = k0 + kk;
-      const bool ok = gi < g.M && gk < kend;
-      const double* src = ok ? (TA ? g.A + gk + gi * g.lda : g.A + gi + gk * g.lda) : g.A;
-      cp_async8(as + kk * Cfg::kLdA + i, src, ok);
-    }
-#pragma unroll
-    for (int e = tid; e < BN * BK; e += NT) {
-      int j, kk;
-      if (!TB) { kk = e % BK; j = e / BK; } else { j = e % BN; kk = e / BN; }
-      const int64_t gj = n0 + j, gk = k0 + kk;
-      const bool ok = gj < g.N && gk < kend;
-      const double* src = ok ? (TB ? g.B + gj + gk * g.ldb : g.B + gk + gj * g.ldb) : g.B;
-      cp_async8(bs + kk * Cfg::kLdB + j, src, ok);
-    }
+    if (!TA) copy_tile(as, Cfg::kLdA, g.A, g.lda, BK, BM, k0, m0, kend, g.M);   // (k, m)
+    else copy_tile(as, Cfg::kLdA, g.A, g.lda, BM, BK, m0, k0, g.M, kend);       // (m, k)
+    if (TB) copy_tile(bs, Cfg::kLdB, g.B, g.ldb, BK, BN, k0, n0, kend, g.N);    // (k, n)
+    else copy_tile(bs, Cfg::kLdB, g.B, g.ldb, BN, BK, n0, k0, g.N, kend);       // (n, k)
   };
 
   double acc[FM][FN][2];
@@ -137,9 +157,15 @@ __global__ void __launch_bounds__(GemmCfg<TA, TB, BM, BN, BK, WM, WN, STAGES>::k
     for (int k4 = 0; k4 < BK; k4 += 4) {
       double af[FM], bf[FN];
 #pragma unroll
-      for (int a = 0; a < FM; ++a) af[a] = as[(k4 + fk) * Cfg::kLdA + wm0 + a * 8 + fr];
+      for (int a = 0; a < FM; ++a) {
+        const int m = wm0 + a * 8 + fr, k = k4 + fk;
+        af[a] = TA ? as[m * Cfg::kLdA + k] : as[k * Cfg::kLdA + m];
+      }
 #pragma unroll
-      for (int b = 0; b < FN; ++b) bf[b] = bs[(k4 + fk) * Cfg::kLdB + wn0 + b * 8 + fr];
+      for (int b = 0; b < FN; ++b) {
+        const int n = wn0 + b * 8 + fr, k = k4 + fk;
+        bf[b] = TB ? bs[k * Cfg::kLdB + n] : bs[n * Cfg::kLdB + k];
+      }
 #pragma unroll
       for (int a = 0; a < FM; ++a)
 #pragma unroll

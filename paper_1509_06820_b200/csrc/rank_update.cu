@@ -32,6 +32,7 @@ struct RuArgs {
   const double* X; int64_t ldx;
   double* C; int64_t ldc;
   const Status* st;
+  int vec16;
 };
 
 __global__ void __launch_bounds__(kRuThreads, 1) rank_update_kernel(RuArgs a) {
@@ -49,49 +50,52 @@ __global__ void __launch_bounds__(kRuThreads, 1) rank_update_kernel(RuArgs a) {
   const int64_t t_lo = ntiles * blockIdx.x / gridDim.x;
   const int64_t t_hi = ntiles * (blockIdx.x + 1) / gridDim.x;
 
-  // issue the async loads of tile t into buffer b (X only when its column
-  // block differs from the one already in that buffer's slot)
-  auto load_tile = [&](int64_t t, int b) {
+  // async loads of tile t: Y and C into buffer b; X into X slot xs only when
+  // the tile starts a new column block (consecutive tiles share X)
+  const bool vec = a.vec16;
+  auto copy2d = [&](double* dst, int lds, const double* src, int64_t ld, int outer, int inner,
+                    int64_t o0, int64_t i0, int64_t olim, int64_t ilim) {
+    if (vec) {
+      const int per = inner / 2;
+      for (int e = tid; e < outer * per; e += kRuThreads) {
+        const int o = e / per, i = (e % per) * 2;
+        const int64_t go = o0 + o, gi = i0 + i;
+        const int valid = go < olim ? (gi + 1 < ilim ? 16 : (gi < ilim ? 8 : 0)) : 0;
+        cp_async16(dst + o * lds + i, valid ? src + gi + go * ld : src, valid);
+      }
+    } else {
+      for (int e = tid; e < outer * inner; e += kRuThreads) {
+        const int o = e / inner, i = e % inner;
+        const int64_t go = o0 + o, gi = i0 + i;
+        const bool ok = go < olim && gi < ilim;
+        cp_async8(dst + o * lds + i, ok ? src + gi + go * ld : src, ok);
+      }
+    }
+  };
+  auto load_tile = [&](int64_t t, int b, int xs, bool load_x) {
     const int64_t m0 = (t % tm) * kTM, n0 = (t / tm) * kTN;
-    double* as = As + b * kStageA;
-    double* bs = Bs + b * kStageB;
-    double* cs = Cs + b * kStageC;
-    // Y[m0:m0+64, 0:K] -> As[k][m]
-    for (int e = tid; e < kTM * K; e += kRuThreads) {
-      const int i = e % kTM, k = e / kTM;
-      const int64_t gi = m0 + i;
-      const bool ok = gi < a.M;
-      cp_async8(as + k * kLdA + i, ok ? a.Y + gi + k * a.ldy : a.Y, ok);
-    }
-    // X[0:K, n0:n0+64] -> Bs[n][k]
-    for (int e = tid; e < kTN * K; e += kRuThreads) {
-      const int k = e % K, j = e / K;
-      const int64_t gj = n0 + j;
-      const bool ok = gj < a.N;
-      cp_async8(bs + j * kLdB + k, ok ? a.X + k + gj * a.ldx : a.X, ok);
-    }
-    // C[m0:m0+64, n0:n0+64] -> Cs[n][m]
-    for (int e = tid; e < kTM * kTN; e += kRuThreads) {
-      const int i = e % kTM, j = e / kTM;
-      const int64_t gi = m0 + i, gj = n0 + j;
-      const bool ok = gi < a.M && gj < a.N;
-      cp_async8(cs + j * kLdC + i, ok ? a.C + gi + gj * a.ldc : a.C, ok);
-    }
+    copy2d(As + b * kStageA, kLdA, a.Y, a.ldy, K, kTM, 0, m0, K, a.M);          // As[k][m]
+    if (load_x) copy2d(Bs + xs * kStageB, kLdB, a.X, a.ldx, kTN, K, n0, 0, a.N, K);  // Bs[n][k]
+    copy2d(Cs + b * kStageC, kLdC, a.C, a.ldc, kTN, kTM, n0, m0, a.N, a.M);     // Cs[n][m]
     cp_async_commit();
   };
 
-  if (t_lo < t_hi) load_tile(t_lo, 0);
+  int xs = 0;
+  if (t_lo < t_hi) load_tile(t_lo, 0, 0, true);
   int buf = 0;
   for (int64_t t = t_lo; t < t_hi; ++t, buf ^= 1) {
+    int xs_next = xs;
     if (t + 1 < t_hi) {
-      load_tile(t + 1, buf ^ 1);
+      const bool newx = (t + 1) / tm != t / tm;
+      if (newx) xs_next = xs ^ 1;
+      load_tile(t + 1, buf ^ 1, xs_next, newx);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
     }
     __syncthreads();
     const double* as = As + buf * kStageA;
-    const double* bs = Bs + buf * kStageB;
+    const double* bs = Bs + xs * kStageB;
     const double* cs = Cs + buf * kStageC;
     double acc[4][2][2];
 #pragma unroll
@@ -125,7 +129,8 @@ __global__ void __launch_bounds__(kRuThreads, 1) rank_update_kernel(RuArgs a) {
           if (gj < a.N) a.C[gi + gj * a.ldc] = __dsub_rn(cs[j * kLdC + i], acc[x][y][e]);
         }
     }
-    __syncthreads();  // buffer `buf` is reloaded by the next iteration's prefetch
+    __syncthreads();  // buffers `buf` / X slot reloaded by the next prefetch
+    xs = xs_next;
   }
 }
 
@@ -141,7 +146,9 @@ bool rank_update(Handle& h, int64_t M, int64_t N, int64_t K, const double* Y, in
                                  (int)kRuSmem));
     attr = true;
   }
-  RuArgs a{M, N, (int)K, Y, ldy, X, ldx, C, ldc, st};
+  const auto al = [](const double* p, int64_t ld) { return ((uintptr_t)p & 15) == 0 && ld % 2 == 0; };
+  RuArgs a{M, N, (int)K, Y, ldy, X, ldx, C, ldc, st,
+           (h.gemm_vec16 && al(Y, ldy) && al(X, ldx) && al(C, ldc)) ? 1 : 0};
   const int64_t ntiles = ((M + kTM - 1) / kTM) * ((N + kTN - 1) / kTN);
   const int grid = (int)std::min<int64_t>(h.num_sms, ntiles);
   ProfScope prof(h, cat, 2.0 * M * N * K, 8.0 * ((double)M * K + (double)K * N + 2.0 * M * N), s);

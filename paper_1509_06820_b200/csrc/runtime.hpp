@@ -91,6 +91,7 @@ class Handle {
   int64_t panel_cluster_max_rows = 3072;    // mm threshold (bw <= 64 only)
 
   bool use_rank_update = true;
+  bool gemm_vec16 = true;
   long long* dbg = nullptr;  // optional device phase-timer buffer (debug)
 
   // profiler
