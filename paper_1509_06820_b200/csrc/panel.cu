@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(kPanThreads, 1) panel_kernel(PanArgs a) {
       if (r < nrow && r0 + r >= j) {
         double* rr = rowp(r);
         const bool diag = r0 + r == j;
-        const double v = diag ? 1.0 : (zero ? rr[j] : __ddiv_rn(rr[j], den));
+        const double v = diag ? 1.0 : (zero ? rr[j] : __dmul_rn(rr[j], rinv));
         tvr[k] = __dmul_rn(tau, v);
         rr[j] = diag ? beta : v;
       }

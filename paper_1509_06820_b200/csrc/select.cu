@@ -276,11 +276,14 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
           den = __dsub_rn(alpha, beta);
           tau = __ddiv_rn(__dsub_rn(beta, alpha), beta);
         }
+        // v = x / (alpha - beta) (kernels.py:42) as x * (1/(alpha - beta)): one
+        // division instead of one per row (<= 1 ulp from the reference's v)
+        const double rinv = zero ? 1.0 : __drcp_rn(den);
 #pragma unroll
         for (int k = 0; k < 5; ++k) {
           const int i = lane + 32 * k;
           if (i >= j && i < ell) {
-            const double v = (i == j) ? 1.0 : (zero ? xv[k] : __ddiv_rn(xv[k], den));
+            const double v = (i == j) ? 1.0 : (zero ? xv[k] : __dmul_rn(xv[k], rinv));
             vbuf[i] = v;
             tvbuf[i] = __dmul_rn(tau, v);
           }
