@@ -173,7 +173,11 @@ int rq_frob_norm(rq_handle_t h, const double* A, int64_t m, int64_t n, int64_t l
 
 /* tuning knobs: "force_select" / "force_panel" (0 = size heuristic, 1 = grid
  * cooperative variant, 2 = single-cluster variant), "select_cluster_max_cols",
- * "panel_cluster_max_rows" (size thresholds of the heuristic) */
+ * "panel_cluster_max_rows" (size thresholds of the heuristic), "fast_panel"
+ * (1 = CholeskyQR2 + Householder-reconstruction panel first, falling back to
+ * the column-by-column kernel when the panel is ill-conditioned; 0 = always
+ * column-by-column), "fast_panel_max_ctas", "use_rank_update", "gemm_vec16",
+ * "debug_timers" */
 int rq_set_option(rq_handle_t h, const char* name, int64_t value);
 
 /* debug: phase timers written by the kernels when "debug_timers" is set */

@@ -63,6 +63,31 @@ RQ_DEV void grid_barrier(unsigned int* counter, unsigned int& epoch) {
   __syncthreads();
 }
 
+// Same barrier for waits that can be long (the other CTAs idle while one CTA
+// runs a serial section): after a few fast polls the waiting thread backs off
+// with __nanosleep, so ~150 pollers do not saturate the L2 slice that holds
+// the counter (and with it the working CTA's own global traffic).
+RQ_DEV void grid_barrier_patient(unsigned int* counter, unsigned int& epoch) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    epoch += 1;
+    const unsigned int target = epoch * gridDim.x;
+    __threadfence();
+    atomicAdd(counter, 1u);
+    unsigned int seen, ns = 32;
+    int polls = 0;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(counter) : "memory");
+      if (seen >= target) break;
+      if (++polls > 16) {
+        __nanosleep(ns);
+        ns = ns < 512 ? 2 * ns : 512;
+      }
+    }
+  }
+  __syncthreads();
+}
+
 // numpy's pairwise summation (pairwise_sum_DOUBLE: 8 accumulators for
 // n <= 128, recursive halving on multiples of 8 above) of x[i]*x[i] over a
 // strided vector; bit-identical to np.linalg.norm(B, axis=0)**2 on an

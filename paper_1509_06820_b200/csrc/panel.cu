@@ -55,6 +55,7 @@ struct PanArgs {
   unsigned int* bar;
   double* gpub;            // [2][Q][2*bw]
   long long* dbg;          // optional phase timers (CTA 0, thread 0)
+  const int* skip;         // panel_fast verdict: nonzero = already committed
 };
 
 // 32 per-lane values -> lane l holds the warp sum of column l (31 shuffles,
@@ -78,6 +79,7 @@ RQ_DEV double warp_transpose_sum(double (&d)[kChunk]) {
 template <bool kCluster>
 __global__ void __launch_bounds__(kPanThreads, 1) panel_kernel(PanArgs a) {
   if (aborted(a.st)) return;
+  if (a.skip != nullptr && *(volatile const int*)a.skip != 0) return;
   extern __shared__ __align__(16) double sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = kPanThreads / 32;
@@ -353,6 +355,9 @@ void panel_qr(Handle& h, int64_t mm, int64_t bw, const double* P, int64_t ldp,
   const int ldl = (int)(bw | 1);
   const size_t aux = ((size_t)4 * bw + (size_t)(kPanThreads / 32) * bw + 4 * (size_t)bw + 8) * 8;
   if (aux > h.smem_optin - 4096) throw InvalidArg("panel too wide for shared memory");
+  // CholeskyQR2 + reconstruction first (panel_fast.cu); this kernel then
+  // only runs when that path declined the panel
+  const int* skip = panel_fast(h, mm, bw, P, ldp, out, tol, st, s);
   const size_t rowbytes = (size_t)ldl * 8;
   const int nrs = (int)std::min<size_t>(rpb, (h.smem_optin - 4096 - aux) / rowbytes);
   const size_t smem = (size_t)nrs * rowbytes + aux;
@@ -366,6 +371,7 @@ void panel_qr(Handle& h, int64_t mm, int64_t bw, const double* P, int64_t ldp,
                        : nullptr;
   a.rpb = rpb; a.ldl = ldl; a.nrs = nrs;
   a.dbg = h.dbg;
+  a.skip = skip;
   {
     ProfScope prof(h, kProfPanel, 2.0 * mm * bw * bw, 16.0 * mm * bw, s);
     count_launch();

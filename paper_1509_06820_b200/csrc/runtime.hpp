@@ -91,6 +91,8 @@ class Handle {
   int64_t panel_cluster_max_rows = 3072;    // mm threshold (bw <= 64 only)
 
   bool use_rank_update = true;
+  bool fast_panel = true;   // CholeskyQR2 + Householder reconstruction panel (panel_fast.cu)
+  int fast_panel_max_ctas = 0;  // 0 = one CTA per SM
   bool gemm_vec16 = true;
   long long* dbg = nullptr;  // optional device phase-timer buffer (debug)
 
@@ -157,6 +159,12 @@ enum PanelPolicy { kPanelCommitIfFull = 0, kPanelCommitUsable = 1, kPanelCommitA
 void panel_qr(Handle& h, int64_t mm, int64_t bw, const double* P, int64_t ldp,
               const PanelOut& out, double tol, PanelPolicy policy, bool raise_abort, Status* st,
               int64_t i0, cudaStream_t s);
+
+// CholeskyQR2 + Householder reconstruction of the same panel (panel_fast.cu).
+// Returns the device flag the exact kernel checks (1 = committed, 0 = the
+// exact kernel must run), or nullptr when the panel shape is not eligible.
+const int* panel_fast(Handle& h, int64_t mm, int64_t bw, const double* P, int64_t ldp,
+                      const PanelOut& out, double tol, Status* st, cudaStream_t s);
 
 // B_new = [S12 - S11 R11^{-1} R12; S22] (randomized.py:107-135).  Writes
 // Status.degenerate; with abort_on_degenerate also sets Status.abort.

@@ -132,3 +132,60 @@ def test_sample_update_vs_oracle():
     R11[5, 5] = 1e-300
     _, deg = sample_update(_dev(S), b, _dev(R11), _dev(R12), 10.0)
     assert deg
+
+
+def _panel_with(P0, fast, **kw):
+    from paper_1509_06820_b200 import _abi
+    from paper_1509_06820_b200.primitives import panel_qr
+    lib, h = _abi.load_library(), _abi.handle(0)
+    lib.rq_set_option(h, b"fast_panel", int(fast))
+    try:
+        P = _dev(P0)
+        Y, tau, T, usable, l2 = panel_qr(P, **kw)
+        torch.cuda.synchronize()
+        return (P.cpu().numpy(), Y.cpu().numpy(), tau.cpu().numpy(), T.cpu().numpy(), usable, l2)
+    finally:
+        lib.rq_set_option(h, b"fast_panel", 1)
+
+
+@pytest.mark.parametrize("mm,bw", [(8192, 64), (4096, 64), (1000, 32), (130, 64), (20000, 32),
+                                   (300, 16), (97, 8)])
+def test_fast_panel_matches_oracle(mm, bw):
+    """CholeskyQR2 + Householder reconstruction (panel_fast.cu) reproduces the
+    reference's reflectors (beta = -sign(alpha)||x||) to rounding level."""
+    P0 = np.random.default_rng(mm * 3 + bw).standard_normal((mm, bw))
+    P0 *= np.logspace(0, -1.5, bw)[None, :]
+    Pc = np.asfortranarray(P0.copy())
+    Yo, to = port.panel_qr(Pc)
+    R, Y, tau, T, usable, l2 = _panel_with(P0, True)
+    Re, Ye, taue, Te, usable_e, l2e = _panel_with(P0, False)
+    assert not np.array_equal(R, Re), "fast path did not run"
+    assert np.linalg.norm(R - Pc) <= 1e-13 * np.linalg.norm(P0)
+    assert np.linalg.norm(Y - Yo) <= 1e-12 * np.linalg.norm(Yo)
+    np.testing.assert_allclose(tau, to, rtol=1e-13, atol=0)
+    assert np.all((tau >= 1.0) & (tau <= 2.0))
+    np.testing.assert_allclose(T, port.t_factor(Yo, to), rtol=1e-10, atol=1e-13)
+    assert (usable, l2) == (usable_e, l2e) == (bw, l2)
+
+
+@pytest.mark.parametrize("kind", ["dup", "tiny_col", "zero_col", "near_tol"])
+def test_fast_panel_declines_to_exact_kernel(kind):
+    """Rank-deficient / ill-conditioned / near-threshold panels fall back to the
+    column-by-column kernel: results are bitwise those of the exact path."""
+    mm, bw = 2048, 64
+    P0 = np.random.default_rng(5).standard_normal((mm, bw))
+    kw = {}
+    if kind == "dup":
+        P0[:, 40] = P0[:, 3]
+    elif kind == "tiny_col":
+        P0[:, -1] *= 1e-8
+    elif kind == "zero_col":
+        P0[:, 7] = 0.0
+    else:   # a column whose R diagonal sits just above the usable threshold
+        P0[:, -1] *= 1e-12
+        kw["tol"] = 1e-13 * np.linalg.norm(P0[:, -1])
+    a = _panel_with(P0, True, **kw)
+    b = _panel_with(P0, False, **kw)
+    for x, y in zip(a[:4], b[:4]):
+        assert np.array_equal(x, y)
+    assert a[4:] == b[4:]
