@@ -421,7 +421,10 @@ void panel_qr(Handle& h, int64_t mm, int64_t bw, const double* P, int64_t ldp,
   if (out.T != nullptr) {
     // T factor of the committed columns (kernels.py:139-147); after a failed
     // speculative commit the Status predicate turns this into a no-op
-    t_factor(h, out.Y, out.ldy, mm, bw, out.tau, out.T, out.ldt, s, st);
+    // (already written by the fast path when it committed: its flag word
+    // doubles as the Status predicate of these launches)
+    t_factor(h, out.Y, out.ldy, mm, bw, out.tau, out.T, out.ldt, s,
+             skip != nullptr ? (const Status*)skip : st);
   }
 }
 

@@ -50,10 +50,11 @@ struct FastArgs {
   double* Rdst; int64_t ldr; int64_t rrows;
   double* Y; int64_t ldy;
   double* tau;
+  double* T; int64_t ldt;           // optional T factor (nullptr: not wanted)
   double tol, guard;                // < 0: no threshold
   int64_t nchunks;
   Status* st;
-  unsigned int* bar;                // [0] barrier, [1] exit count, [2] fail, [3] fast_ok
+  unsigned int* bar;                // [0] barrier, [1] exit count, [2] fail, [4] skip flag
   double* gpart;                    // [Q][n8*n8]
   double* gmat;                     // [4][n8*n8]: G1, R1, R1^{-1}, G2 then M
   long long* dbg;
@@ -209,7 +210,10 @@ RQ_DEV void upper_inverse(const double* U, const double* dinv, double* X, double
 }
 
 __global__ void __launch_bounds__(kFT, 1) panel_fast_kernel(FastArgs a) {
-  if (aborted(a.st)) return;  // set only by earlier launches: uniform over the grid
+  if (aborted(a.st)) {  // set only by earlier launches: uniform over the grid
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.bar[4] = 1;   // nothing downstream runs either
+    return;
+  }
   extern __shared__ __align__(16) double sm[];
   __shared__ int s_fail;
   __shared__ double s_sign[kFMaxBw], s_c[kFMaxBw], s_dinv[kFMaxBw];
@@ -423,7 +427,7 @@ __global__ void __launch_bounds__(kFT, 1) panel_fast_kernel(FastArgs a) {
     }
     if (tid == 0) {
       a.bar[2] = s_fail;
-      if (s_fail) a.bar[3] = 0;
+      if (s_fail) a.bar[4] = 0;
     }
     sub(3);
   }
@@ -566,7 +570,10 @@ __global__ void __launch_bounds__(kFT, 1) panel_fast_kernel(FastArgs a) {
       }
       for (int j = tid; j < n; j += kFT) a.tau[j] = fabs(s_c[j]) + 1.0;
       for (int j = n + tid; j < n8; j += kFT) s_dinv[j] = 1.0;
-      __syncthreads();   // T5 (L) is read above and is the scratch below
+      __syncthreads();   // Rt / T5 are read above; W0 <- Y1^T (unit upper) for the T factor
+      for (int i = r0; i < n8; i += rstep)
+        W0[i * ld + c0] = i == c0 ? 1.0 : (i < c0 && c0 < n ? T5[c0 * ld + i] : 0.0);
+      __syncthreads();   // T5 (L) is the scratch below
       upper_inverse(Q1, s_dinv, R1, T5, n8, ld);   // U^{-1}
       __syncthreads();
       sub(7);
@@ -579,10 +586,23 @@ __global__ void __launch_bounds__(kFT, 1) panel_fast_kernel(FastArgs a) {
       chunk_mm<true, true>(Ri, R1, T5, n8, n8, ld);  // M = R1^{-1} M'
       __syncthreads();
       for (int i = r0; i < n8; i += rstep) a.gmat[3 * nn + i * n8 + c0] = T5[i * ld + c0];
+      if (a.T != nullptr) {
+        // compact-WY T of the reconstructed reflectors: U = -T Y1^T, so
+        // T = -U Y1^{-T} (kernels.py:139-147 builds the same T by recurrence)
+        for (int j = tid; j < n8; j += kFT) s_dinv[j] = 1.0;
+        __syncthreads();
+        upper_inverse(W0, s_dinv, W2, W3, n8, ld);   // Y1^{-T}
+        chunk_mm<true, true>(Q1, W2, W4, n8, n8, ld);
+        __syncthreads();
+        for (int e = tid; e < n * n; e += kFT) {
+          const int l = e / n, i = e - l * n;
+          a.T[i + (int64_t)l * a.ldt] = i <= l ? -W4[i * ld + l] : 0.0;
+        }
+      }
     }
     if (tid == 0) {
       a.bar[2] = s_fail;
-      a.bar[3] = s_fail ? 0 : 1;
+      a.bar[4] = s_fail ? 0 : 1;
       if (!s_fail) {
         // _panel_rank: every column usable; level-2 counters of the
         // column-by-column reflections this path replaces
@@ -641,6 +661,7 @@ const int* panel_fast(Handle& h, int64_t mm, int64_t bw, const double* P, int64_
   a.P = P; a.ldp = ldp;
   a.Rdst = out.Rdst; a.ldr = out.ldr; a.rrows = out.rrows;
   a.Y = out.Y; a.ldy = out.ldy; a.tau = out.tau;
+  a.T = out.T; a.ldt = out.ldt;
   a.tol = tol;
   a.guard = tol >= 0.0 ? tol * (kEps34 / kEps) : -1.0;
   a.nchunks = nchunks;
@@ -668,7 +689,7 @@ const int* panel_fast(Handle& h, int64_t mm, int64_t bw, const double* P, int64_
     RQ_CHECK_LAUNCH();
     count_launch();
   }
-  return (const int*)&a.bar[3];
+  return (const int*)&a.bar[4];
 }
 
 }  // namespace rq

@@ -277,7 +277,9 @@ def rqrcp_sharded(A_local: torch.Tensor, m: int, n: int, k=None, config=None, gr
                 blk = fmat(rows, 2 * bw + 1, dev) if me != owner else None
                 if me == owner:
                     work[i0:, lp:lp + bw] = P[:, :bw]
-                    Tb = K_t_factor(Yp[:, :bw], tp[:bw])
+                    # the leading bw x bw block of the panel's T is the T of
+                    # its first bw reflectors (same T the native driver uses)
+                    Tb = T[:bw, :bw]
                     blk = fmat(rows, 2 * bw + 1, dev, fill=0.0)
                     blk[: m - i0, :bw] = Yp[:, :bw]
                     blk[:bw, bw:2 * bw] = Tb
@@ -324,10 +326,6 @@ def rqrcp_sharded(A_local: torch.Tensor, m: int, n: int, k=None, config=None, gr
                                 rank=rank_out, R_local=R_local, R=R, layout=layout,
                                 counters=ctr)
 
-
-def K_t_factor(Y, tau):
-    from .factorization import t_factor
-    return t_factor(Y, tau)
 
 
 def _f(t: torch.Tensor) -> torch.Tensor:
