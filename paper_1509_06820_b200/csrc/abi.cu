@@ -259,6 +259,7 @@ int rq_set_option(rq_handle_t h, const char* name, int64_t value) {
     else if (n == "use_rank_update") hh.use_rank_update = value != 0;
     else if (n == "fast_panel") hh.fast_panel = value != 0;
     else if (n == "fast_panel_max_ctas") hh.fast_panel_max_ctas = (int)value;
+    else if (n == "fast_panel_spec") hh.fast_panel_spec = (int)value;
     else if (n == "gemm_vec16") hh.gemm_vec16 = value != 0;
     else if (n == "debug_timers") {
       hh.dbg = value ? (long long*)hh.buf("dbg_timers", 64 * 8, nullptr) : nullptr;

@@ -24,6 +24,7 @@ enum AbortCode : int {
   kAbortShortSample = 1,  // select: got < want   (randomized.py:217)
   kAbortPanelRank = 2,    // panel: usable < got  (randomized.py:229)
   kAbortDegenerate = 3,   // sample update: |R11_jj| < eps^3/4 ||A|| (randomized.py:117)
+  kAbortPanelFast = 4,    // fast panel declined: redo this block's panel column by column
 };
 
 // Device-side run status shared by the kernels of one driver call.

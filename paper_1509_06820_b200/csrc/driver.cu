@@ -52,6 +52,10 @@ class Factor {
   double *om_d_ = nullptr, *om_h_ = nullptr, *P_ = nullptr, *Z_ = nullptr;
   int64_t* piv_ = nullptr;
   double frob_ = 0.0, tol_ = 0.0;
+  // a declined speculative fast panel rewinds the lookahead; after the first
+  // one (declines cluster near the noise floor) the exact kernel is queued
+  // behind every fast panel instead
+  bool fast_aborts_ = true;
   Counters c_;
   int64_t m_ = 0, n_ = 0, k_ = 0, b_ = 0, ell_ = 0;
 
@@ -68,10 +72,11 @@ class Factor {
   void fresh_sample(int64_t i0);
   void select(int64_t i0, int64_t want, bool spec);
   void swaps(int64_t i0, int64_t got);
-  void panel(int64_t i0, int64_t got, PanelPolicy pol, bool spec, Counters& c);
+  void panel(int64_t i0, int64_t got, PanelPolicy pol, bool spec, Counters& c,
+             bool allow_fast = true);
   void stages(int64_t i0, int64_t bw, Counters& c);
   void update(int64_t i0_new, int64_t bw, bool spec, Counters& c);
-  bool slow_block(int64_t& i0, bool resampled, int64_t& rank);
+  bool slow_block(int64_t& i0, bool resampled, int64_t& rank, bool resume_panel = false);
 };
 
 void Factor::draw_omega(int64_t rows, int64_t cols) {
@@ -133,7 +138,8 @@ void Factor::swaps(int64_t i0, int64_t got) {
   apply_swaps(h_, piv_, got, i0, t, st_, s_);
 }
 
-void Factor::panel(int64_t i0, int64_t got, PanelPolicy pol, bool spec, Counters& c) {
+void Factor::panel(int64_t i0, int64_t got, PanelPolicy pol, bool spec, Counters& c,
+                   bool allow_fast) {
   const int64_t mm = m_ - i0;
   PanelOut o{};
   o.Y = p_.Y + i0 + i0 * p_.ldy; o.ldy = p_.ldy;
@@ -156,7 +162,7 @@ void Factor::panel(int64_t i0, int64_t got, PanelPolicy pol, bool spec, Counters
     src = P_; lds = mm;
     o.Rdst = p_.R + i0 + i0 * p_.ldR; o.ldr = p_.ldR; o.rrows = got;
   }
-  panel_qr(h_, mm, got, src, lds, o, tol_, pol, spec, st_, i0, s_);
+  panel_qr(h_, mm, got, src, lds, o, tol_, pol, spec, st_, i0, s_, allow_fast, fast_aborts_);
 }
 
 // _block_stages (randomized.py:158-180) / trqrcp W+R update (truncated.py:453-470)
@@ -220,22 +226,29 @@ void Factor::update(int64_t i0_new, int64_t bw, bool spec, Counters& c) {
 
 // One block of the reference loop with host-visible branch decisions
 // (randomized.py:208-258).  Returns false when the factorization stops.
-bool Factor::slow_block(int64_t& i0, bool resampled, int64_t& rank) {
+// resume_panel: the speculative pass already selected and swapped this block
+// (got == want) and only its fast panel declined; continue at the panel with
+// the column-by-column kernel.
+bool Factor::slow_block(int64_t& i0, bool resampled, int64_t& rank, bool resume_panel) {
   const int64_t want = std::min(b_, k_ - i0);
   int64_t bw = 0;
   while (true) {
-    select(i0, want, false);
-    const int64_t got = read_status().got;
-    if (got < want && !resampled) {
-      fresh_sample(i0);
-      c_.resamples += 1;
-      resampled = true;
-      continue;
+    int64_t got = want;
+    if (!resume_panel) {
+      select(i0, want, false);
+      got = read_status().got;
+      if (got < want && !resampled) {
+        fresh_sample(i0);
+        c_.resamples += 1;
+        resampled = true;
+        continue;
+      }
+      if (got == 0) { bw = 0; break; }
+      swaps(i0, got);
     }
-    if (got == 0) { bw = 0; break; }
-    swaps(i0, got);
     Counters pc;
-    panel(i0, got, resampled ? kPanelCommitUsable : kPanelCommitIfFull, false, pc);
+    panel(i0, got, resampled ? kPanelCommitUsable : kPanelCommitIfFull, false, pc, !resume_panel);
+    resume_panel = false;
     c_.gemm_flops += pc.gemm_flops;
     c_.bytes_touched += pc.bytes_touched;
     const int64_t usable = read_status().usable;
@@ -308,6 +321,7 @@ FactorResult Factor::run() {
     std::memcpy(&frob_, &hst_->level2, 8);
   }
   tol_ = kEps * frob_;
+  fast_aborts_ = h_.fast_panel_spec != 2;
   first_sample();
 
   const bool speculate = p_.speculate && !p_.resketch_each_block;
@@ -347,6 +361,12 @@ FactorResult Factor::run() {
           i0 = X + bwX;
           fresh_sample(i0);
           c_.resamples += 1;
+        } else if (code == kAbortPanelFast) {
+          // not a reference branch: block X's select and swaps stand, only
+          // its panel is redone column by column
+          i0 = X;
+          fast_aborts_ = h_.fast_panel_spec == 0;
+          if (!slow_block(i0, false, rank, true)) { stopped = true; break; }
         } else {
           i0 = X;
           fresh_sample(i0);

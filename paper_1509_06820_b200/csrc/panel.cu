@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(kPanThreads, 1) panel_kernel(PanArgs a) {
 
 void panel_qr(Handle& h, int64_t mm, int64_t bw, const double* P, int64_t ldp,
               const PanelOut& out, double tol, PanelPolicy policy, bool raise_abort, Status* st,
-              int64_t i0, cudaStream_t s) {
+              int64_t i0, cudaStream_t s, bool allow_fast, bool fast_aborts) {
   if (bw < 1 || bw > kMaxBw) throw InvalidArg("panel width must be in [1, 256]");
   if (mm < 1) throw InvalidArg("panel needs at least one row");
   const bool grid = h.force_panel == 1 || (h.force_panel == 0 && mm > h.panel_cluster_max_rows);
@@ -357,7 +357,10 @@ void panel_qr(Handle& h, int64_t mm, int64_t bw, const double* P, int64_t ldp,
   if (aux > h.smem_optin - 4096) throw InvalidArg("panel too wide for shared memory");
   // CholeskyQR2 + reconstruction first (panel_fast.cu); this kernel then
   // only runs when that path declined the panel
-  const int* skip = panel_fast(h, mm, bw, P, ldp, out, tol, st, s);
+  const bool decline_aborts = raise_abort && fast_aborts;
+  const int* skip =
+      allow_fast ? panel_fast(h, mm, bw, P, ldp, out, tol, st, s, decline_aborts, i0) : nullptr;
+  if (skip != nullptr && decline_aborts) return;   // speculative: a decline rewinds the block
   const size_t rowbytes = (size_t)ldl * 8;
   const int nrs = (int)std::min<size_t>(rpb, (h.smem_optin - 4096 - aux) / rowbytes);
   const size_t smem = (size_t)nrs * rowbytes + aux;

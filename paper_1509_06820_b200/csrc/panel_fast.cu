@@ -52,6 +52,8 @@ struct FastArgs {
   double* tau;
   double* T; int64_t ldt;           // optional T factor (nullptr: not wanted)
   double tol, guard;                // < 0: no threshold
+  int abort_on_decline;             // speculative driver: decline -> Status.abort (kAbortPanelFast)
+  int64_t i0;
   int64_t nchunks;
   Status* st;
   unsigned int* bar;                // [0] barrier, [1] exit count, [2] fail, [4] skip flag
@@ -427,7 +429,14 @@ __global__ void __launch_bounds__(kFT, 1) panel_fast_kernel(FastArgs a) {
     }
     if (tid == 0) {
       a.bar[2] = s_fail;
-      if (s_fail) a.bar[4] = 0;
+      if (s_fail) {
+        a.bar[4] = 0;
+        if (a.abort_on_decline) {
+          a.st->abort_i0 = a.i0;
+          __threadfence();
+          a.st->abort = kAbortPanelFast;
+        }
+      }
     }
     sub(3);
   }
@@ -603,6 +612,11 @@ __global__ void __launch_bounds__(kFT, 1) panel_fast_kernel(FastArgs a) {
     if (tid == 0) {
       a.bar[2] = s_fail;
       a.bar[4] = s_fail ? 0 : 1;
+      if (s_fail && a.abort_on_decline) {
+        a.st->abort_i0 = a.i0;
+        __threadfence();
+        a.st->abort = kAbortPanelFast;
+      }
       if (!s_fail) {
         // _panel_rank: every column usable; level-2 counters of the
         // column-by-column reflections this path replaces
@@ -646,7 +660,8 @@ __global__ void __launch_bounds__(kFT, 1) panel_fast_kernel(FastArgs a) {
 }  // namespace
 
 const int* panel_fast(Handle& h, int64_t mm, int64_t bw, const double* P, int64_t ldp,
-                      const PanelOut& out, double tol, Status* st, cudaStream_t s) {
+                      const PanelOut& out, double tol, Status* st, cudaStream_t s,
+                      bool abort_on_decline, int64_t i0) {
   if (!h.fast_panel || bw < 2 || bw > kFMaxBw || mm < 2 * bw) return nullptr;
   const int n8 = (int)((bw + 7) / 8 * 8);
   if (kFT / n8 > 32 || 32 % (kFT / n8) != 0) return nullptr;  // n8 in {8, 16, 32, 64}
@@ -666,6 +681,8 @@ const int* panel_fast(Handle& h, int64_t mm, int64_t bw, const double* P, int64_
   a.guard = tol >= 0.0 ? tol * (kEps34 / kEps) : -1.0;
   a.nchunks = nchunks;
   a.st = st;
+  a.abort_on_decline = abort_on_decline ? 1 : 0;
+  a.i0 = i0;
   a.bar = (unsigned int*)h.buf("pf_bar", 64, s);
   static void* zeroed = nullptr;
   if (zeroed != (void*)a.bar) {

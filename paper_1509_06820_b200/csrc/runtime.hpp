@@ -93,6 +93,9 @@ class Handle {
   bool use_rank_update = true;
   bool fast_panel = true;   // CholeskyQR2 + Householder reconstruction panel (panel_fast.cu)
   int fast_panel_max_ctas = 0;  // 0 = one CTA per SM
+  // speculative driver on a declined fast panel: 0 = always rewind, 1 = rewind
+  // once then queue the exact kernel behind every fast panel, 2 = never rewind
+  int fast_panel_spec = 1;
   bool gemm_vec16 = true;
   long long* dbg = nullptr;  // optional device phase-timer buffer (debug)
 
@@ -156,15 +159,22 @@ struct PanelOut {
 enum PanelPolicy { kPanelCommitIfFull = 0, kPanelCommitUsable = 1, kPanelCommitAll = 2 };
 // Householder QR of an mm x bw panel (qrcp.py:206-219) + _panel_rank
 // (randomized.py:150-155) + build_t_matrix (kernels.py:139-147).
+// allow_fast: try panel_fast first.  With raise_abort && fast_aborts
+// (speculative driver) the fast path runs alone and a decline aborts the
+// block (kAbortPanelFast); otherwise the exact kernel follows it on the
+// stream and runs only if the fast path declined.
 void panel_qr(Handle& h, int64_t mm, int64_t bw, const double* P, int64_t ldp,
               const PanelOut& out, double tol, PanelPolicy policy, bool raise_abort, Status* st,
-              int64_t i0, cudaStream_t s);
+              int64_t i0, cudaStream_t s, bool allow_fast = true, bool fast_aborts = true);
 
 // CholeskyQR2 + Householder reconstruction of the same panel (panel_fast.cu).
 // Returns the device flag the exact kernel checks (1 = committed, 0 = the
 // exact kernel must run), or nullptr when the panel shape is not eligible.
+// abort_on_decline (speculative driver): a declined panel sets Status.abort =
+// kAbortPanelFast at block i0 instead of leaving the work to the exact kernel.
 const int* panel_fast(Handle& h, int64_t mm, int64_t bw, const double* P, int64_t ldp,
-                      const PanelOut& out, double tol, Status* st, cudaStream_t s);
+                      const PanelOut& out, double tol, Status* st, cudaStream_t s,
+                      bool abort_on_decline = false, int64_t i0 = 0);
 
 // B_new = [S12 - S11 R11^{-1} R12; S22] (randomized.py:107-135).  Writes
 // Status.degenerate; with abort_on_degenerate also sets Status.abort.
