@@ -205,6 +205,12 @@ int rq_profile_reset(rq_handle_t h);
  * summed kernel milliseconds, algorithmic flops and algorithmic bytes */
 int rq_profile_read(rq_handle_t h, int64_t* launches, double* ms, double* flops, double* bytes);
 
+/* launch trace of the profiled launches since the last rq_profile_reset (set
+ * option "profile_trace" first): family index, start and end in ms on the
+ * device timeline; writes min(cap, count) records and the total in *count */
+int rq_profile_trace(rq_handle_t h, int64_t cap, int32_t* cat, double* start_ms, double* end_ms,
+                     int64_t* count);
+
 #ifdef __cplusplus
 }
 #endif

@@ -75,6 +75,8 @@ SIGNATURES = {
     "rq_profile_reset": (C.c_int, [vp]),
     "rq_profile_read": (C.c_int, [vp, C.POINTER(i64), C.POINTER(f64), C.POINTER(f64),
                                   C.POINTER(f64)]),
+    "rq_profile_trace": (C.c_int, [vp, i64, C.POINTER(C.c_int32), C.POINTER(f64), C.POINTER(f64),
+                                   C.POINTER(i64)]),
 }
 
 PROF_NAMES = ["sketch", "inner", "update", "small_gemm", "select", "panel", "sample_update",

@@ -260,6 +260,9 @@ int rq_set_option(rq_handle_t h, const char* name, int64_t value) {
     else if (n == "fast_panel") hh.fast_panel = value != 0;
     else if (n == "fast_panel_max_ctas") hh.fast_panel_max_ctas = (int)value;
     else if (n == "fast_panel_spec") hh.fast_panel_spec = (int)value;
+    else if (n == "profile_trace") hh.tracing = value != 0;
+    else if (n == "select_max_ctas") hh.select_max_ctas = (int)value;
+    else if (n == "select_reg") hh.select_reg = value != 0;
     else if (n == "gemm_vec16") hh.gemm_vec16 = value != 0;
     else if (n == "debug_timers") {
       hh.dbg = value ? (long long*)hh.buf("dbg_timers", 64 * 8, nullptr) : nullptr;
@@ -300,3 +303,18 @@ int rq_profile_read(rq_handle_t h, int64_t* launches, double* ms, double* flops,
 }
 
 }  // extern "C"
+
+int rq_profile_trace(rq_handle_t h, int64_t cap, int32_t* cat, double* start_ms, double* end_ms,
+                     int64_t* count) {
+  return guarded([&] {
+    rq::Handle& hh = H(h);
+    hh.prof_collect();
+    const int64_t nrec = (int64_t)hh.trace.size();
+    for (int64_t i = 0; i < nrec && i < cap; ++i) {
+      cat[i] = hh.trace[i].cat;
+      start_ms[i] = hh.trace[i].start_ms;
+      end_ms[i] = hh.trace[i].end_ms;
+    }
+    *count = nrec;
+  });
+}

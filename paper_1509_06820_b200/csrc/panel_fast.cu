@@ -315,7 +315,6 @@ __global__ void __launch_bounds__(kFT, 1) panel_fast_kernel(FastArgs a) {
   // elimination steps: thread (ty, tx) keeps elements (ty + 16c, tx + 16b) in
   // registers; the pivot row goes through shared memory, one barrier per step
   const int ty = tid >> 4, tx = tid & 15;
-  const unsigned hmask = 0xffffu << (16 * (ty & 1));   // my half-warp (one matrix row class)
   if (me == 0) {
     double* R1 = W1;
     for (int i = r0; i < n8; i += rstep) R1[i * ld + c0] = (i == c0 && i >= n) ? 1.0 : 0.0;

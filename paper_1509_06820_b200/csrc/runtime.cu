@@ -46,6 +46,11 @@ void Handle::prof_collect() {
     RQ_CUDA(cudaEventSynchronize(p.b));
     float ms = 0.f;
     RQ_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+    if (tracing && trace_base_ != nullptr) {
+      float t0 = 0.f;
+      RQ_CUDA(cudaEventElapsedTime(&t0, trace_base_, p.a));
+      trace.push_back({p.cat, (double)t0, (double)t0 + ms});
+    }
     ProfStat& st = stats[p.cat];
     st.launches += 1;
     st.ms += ms;
@@ -60,6 +65,11 @@ void Handle::prof_collect() {
 void Handle::prof_reset() {
   prof_collect();
   for (auto& s : stats) s = ProfStat{};
+  trace.clear();
+  if (tracing) {
+    if (trace_base_ == nullptr) RQ_CUDA(cudaEventCreate(&trace_base_));
+    RQ_CUDA(cudaEventRecord(trace_base_, 0));
+  }
 }
 
 // ------------------------------------------------------------------ Handle

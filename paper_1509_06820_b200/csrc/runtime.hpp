@@ -89,6 +89,8 @@ class Handle {
   // (crossovers measured on B200: tools/variant_sweep.py, profiles/r01_variant_sweep.jsonl)
   int64_t select_cluster_max_cols = 1024;   // nt threshold
   int64_t panel_cluster_max_rows = 3072;    // mm threshold (bw <= 64 only)
+  int select_max_ctas = 0;                  // cap of the grid variant (0 = one CTA per SM)
+  bool select_reg = true;                   // register-resident select (v5) where it fits
 
   bool use_rank_update = true;
   bool fast_panel = true;   // CholeskyQR2 + Householder reconstruction panel (panel_fast.cu)
@@ -102,6 +104,13 @@ class Handle {
   // profiler
   bool profiling = false;
   ProfStat stats[kProfNum];
+  // optional launch trace (family, start, end in ms from the last reset)
+  struct TraceRec {
+    int cat;
+    double start_ms, end_ms;
+  };
+  bool tracing = false;
+  std::vector<TraceRec> trace;
   int prof_begin(int cat, double flops, double bytes, cudaStream_t s);
   void prof_end(int idx, cudaStream_t s);
   void prof_collect();  // synchronises the pending events into `stats`
@@ -114,6 +123,7 @@ class Handle {
     cudaEvent_t a, b;
   };
   std::vector<PendEv> pend_;
+  cudaEvent_t trace_base_ = nullptr;
   std::vector<cudaEvent_t> free_ev_;
   cudaEvent_t take_event();
   struct Buf {

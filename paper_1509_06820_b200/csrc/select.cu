@@ -32,7 +32,6 @@ namespace {
 
 constexpr int kSelThreads = 512;
 constexpr int kMaxCluster = 16;
-constexpr int kNoPos = 0x7fffffff;
 
 struct SelArgs {
   int ell, nt, want;
@@ -418,6 +417,509 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
   if constexpr (kCluster) cg::this_cluster().sync();  // peers may still read my smem
 }
 
+// v5: the same step with every column register-resident in its 8-lane group
+// (lane gl holds rows gl, gl+8, ...; up to CPG columns per group) and the
+// reflector formed redundantly by every warp (v, tau v in a per-warp shared
+// slice), so a step has one block barrier plus the exchange and no shared
+// memory round trips on the column path.  Same arithmetic rules as v4:
+// reflector (kernels.py:26-44), H_j application, NormTracker downdate with
+// the sqrt(eps) recompute guard (kernels.py:222-233), packed argmax key.
+// v[idx] for a warp-uniform idx as a uniform branch (an unrolled compare-select
+// chain is turned into a dynamically indexed local-memory array by the compiler)
+template <int N>
+RQ_DEV double pick_uniform(const double (&v)[N], int idx) {
+  double out = v[0];
+#define RQ_PICK(r) \
+  case r:          \
+    if constexpr (r < N) out = v[r]; \
+    break;
+  switch (idx) {
+    RQ_PICK(1) RQ_PICK(2) RQ_PICK(3) RQ_PICK(4) RQ_PICK(5) RQ_PICK(6) RQ_PICK(7) RQ_PICK(8)
+    RQ_PICK(9) RQ_PICK(10) RQ_PICK(11) RQ_PICK(12) RQ_PICK(13) RQ_PICK(14) RQ_PICK(15)
+    RQ_PICK(16) RQ_PICK(17) RQ_PICK(18) RQ_PICK(19)
+    default: break;
+  }
+#undef RQ_PICK
+  return out;
+}
+
+template <bool kCluster, int RPL, int CPG>
+__global__ void __launch_bounds__(kSelThreads, 1) select_reg_kernel(SelArgs a) {
+  if (aborted(a.st)) return;
+  extern __shared__ __align__(16) double sm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = kSelThreads / 32;
+  constexpr int NG = kSelThreads / 8;
+  const int grp = tid >> 3, gl = tid & 7;
+  const unsigned gmask = 0xffu << (lane & 24);  // my group's lanes
+  int P, me;
+  if constexpr (kCluster) {
+    P = (int)cg::this_cluster().num_blocks();
+    me = (int)cg::this_cluster().block_rank();
+  } else {
+    P = gridDim.x;
+    me = blockIdx.x;
+  }
+  const int ell = a.ell, ldl = a.ldl;
+  const int c0 = me * a.cpb;
+  const int ncol = max(0, min(a.nt - c0, a.cpb));
+  const int cstride = ell + 1;
+  double* stage = sm;                                   // [cpb][ldl] initial load
+  double* wv = stage + (size_t)a.cpb * ldl;             // [NW][ell] v
+  double* wtv = wv + NW * ell;                          // [NW][ell] tau v
+  double* ccol = wtv + NW * ell;                        // [2][ell+1] published candidate
+  double* nrm0 = ccol + 2 * cstride;                    // [cpb] initial norms
+  unsigned char* omap = (unsigned char*)(nrm0 + a.cpb); // [nt] position -> owner CTA
+  __shared__ unsigned long long s_key[3][kMaxCluster];
+  __shared__ unsigned long long s_wkey[2][NW];   // per-warp best keys, by step parity
+  __shared__ double s_sq[kMaxCluster];
+  __shared__ double s_all[160];
+  __shared__ double s_step[2];
+  __shared__ int s_stepi[2];
+  unsigned int epoch = 0;
+  auto xsync = [&]() {
+    if constexpr (kCluster) cg::this_cluster().sync();
+    else grid_barrier(a.bar, epoch);
+  };
+  auto slot_max = [&](int slot) -> unsigned long long {
+    unsigned long long k = 0ull;
+    if constexpr (kCluster) {
+      if (lane < P) k = s_key[slot][lane];
+#pragma unroll
+      for (int off = 16; off; off >>= 1) {
+        const unsigned long long o = __shfl_xor_sync(0xffffffffu, k, off);
+        k = o > k ? o : k;
+      }
+    } else {
+      k = __ldcg(a.gkey + slot);
+    }
+    return k;
+  };
+
+  // ---- load, initial norms (pairwise, bit-identical to numpy), registers
+  {
+    const int total = ncol * ell;
+#pragma unroll 4
+    for (int e = tid; e < total; e += kSelThreads) {
+      const int c = e / ell, i = e - c * ell;
+      stage[(size_t)c * ldl + i] = a.B[(size_t)(c0 + c) * a.ldb + i];
+    }
+  }
+  for (int e = tid; e < 3 * kMaxCluster; e += kSelThreads) (&s_key[0][0])[e] = 0ull;
+  for (int q = tid; q < a.nt; q += kSelThreads) omap[q] = (unsigned char)(q / a.cpb);
+  if (!kCluster && me == 0 && tid < 3) a.gkey[tid] = 0ull;
+  __syncthreads();
+  double mysq = 0.0;
+  for (int c = tid; c < ncol; c += kSelThreads) {
+    const double sq = pairwise_sumsq(stage + (size_t)c * ldl, ell, 1);
+    nrm0[c] = sqrt(sq);
+    mysq = __dadd_rn(mysq, sq);
+  }
+  {
+    const double v = warp_sum(mysq);
+    if (lane == 0) s_all[warp] = v;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int w = 0; w < NW; ++w) t = __dadd_rn(t, s_all[w]);
+      if constexpr (kCluster) {
+        for (int q = 0; q < P; ++q) cg::this_cluster().map_shared_rank(s_sq, q)[me] = t;
+      } else {
+        a.gsq[me] = t;
+      }
+    }
+  }
+  double x[CPG][RPL];
+  double nv[CPG], og[CPG];
+  int pc[CPG];   // logical position of my column t (-1: none)
+#pragma unroll
+  for (int t = 0; t < CPG; ++t) {
+    const int c = grp + NG * t;
+    const bool valid = c < ncol;
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+      const int i = gl + 8 * r;
+      x[t][r] = (valid && i < ell) ? stage[(size_t)c * ldl + i] : 0.0;
+    }
+    nv[t] = valid ? nrm0[c] : 0.0;
+    og[t] = __dmul_rn(nv[t], nv[t]);
+    pc[t] = valid ? c0 + c : -1;
+  }
+  xsync();  // key slots are zero everywhere before anyone publishes
+
+  // publish the block's best candidate for step jn (key slot jn % 3, column
+  // parity jn & 1); the caller has passed a block barrier since the keys
+  auto publish = [&](int jn, unsigned long long bk) {
+    if (bk == 0ull) return;
+    if constexpr (kCluster) {
+      if (tid < P) cg::this_cluster().map_shared_rank(&s_key[jn % 3][0], tid)[me] = bk;
+    } else {
+      if (tid == 0) atomicMax(a.gkey + (jn % 3), bk);
+    }
+    const int bpos = key_pos(bk);
+#pragma unroll
+    for (int t = 0; t < CPG; ++t) {
+      if (pc[t] != bpos) continue;
+      double* dst = kCluster ? ccol + (jn & 1) * cstride
+                             : a.gcol + ((size_t)(jn & 1) * P + me) * cstride;
+#pragma unroll
+      for (int r = 0; r < RPL; ++r) {
+        const int i = gl + 8 * r;
+        if (i < ell) dst[i] = x[t][r];
+      }
+      if (gl == 0) dst[ell] = nv[t];
+    }
+  };
+  auto block_key = [&](int b) {   // max of the per-warp keys (every warp, after a barrier)
+    unsigned long long k = lane < NW ? s_wkey[b][lane] : 0ull;
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+      const unsigned long long o = __shfl_xor_sync(0xffffffffu, k, off);
+      k = o > k ? o : k;
+    }
+    return k;
+  };
+  auto group_key = [&](unsigned long long k) {   // warp max of the groups' keys
+#pragma unroll
+    for (int off = 8; off <= 16; off <<= 1) {
+      const unsigned long long o = __shfl_xor_sync(0xffffffffu, k, off);
+      k = o > k ? o : k;
+    }
+    return k;
+  };
+
+  // step-0 candidates
+  {
+    unsigned long long k = 0ull;
+#pragma unroll
+    for (int t = 0; t < CPG; ++t) {
+      if (pc[t] < 0) continue;
+      const unsigned long long kt = make_key(nv[t], pc[t]);
+      k = kt > k ? kt : k;
+    }
+    k = group_key(k);
+    if (lane == 0) s_wkey[0][warp] = k;
+    __syncthreads();
+    publish(0, block_key(0));
+  }
+  xsync();
+  double tol;
+  {
+    for (int q = tid; q < P; q += kSelThreads) {
+      if constexpr (kCluster) s_all[q] = s_sq[q];
+      else s_all[q] = a.gsq[q];
+    }
+    __syncthreads();
+    double t = 0.0;
+    for (int q = 0; q < P; ++q) t = __dadd_rn(t, s_all[q]);
+    tol = kEps * sqrt(t);  // randomized.py:98, same summation order everywhere
+  }
+
+  int got = a.want;
+  int64_t l2 = 0, l2b = 0;
+  long long tm[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tlast = clock64();
+  const bool timing = a.dbg != nullptr && me == 0 && tid == 0;
+  auto mark = [&](int k) {
+    if (timing) {
+      const long long t = clock64();
+      tm[k] += t - tlast;
+      tlast = t;
+    }
+  };
+  for (int j = 0; j < a.want; ++j) {
+    const int par = j & 1;
+    // ---- warp 0: winner and reflector into the shared v / tau v
+    if (warp == 0) {
+      const unsigned long long wk = slot_max(j % 3);
+      const int pw = key_pos(wk);
+      const int owner = wk ? (int)omap[pw] : -1;
+      double xv[5];  // ell <= 160
+      double xnorm = -1.0;
+      if (owner >= 0) {
+        const double* xc;
+        if constexpr (kCluster) {
+          xc = cg::this_cluster().map_shared_rank(ccol, owner) + par * cstride;
+#pragma unroll
+          for (int k = 0; k < 5; ++k) {
+            const int i = lane + 32 * k;
+            xv[k] = i < ell ? xc[i] : 0.0;
+          }
+          xnorm = xc[ell];
+        } else {
+          xc = a.gcol + ((size_t)par * P + owner) * cstride;
+#pragma unroll
+          for (int k = 0; k < 5; ++k) {
+            const int i = lane + 32 * k;
+            xv[k] = i < ell ? __ldcg(xc + i) : 0.0;
+          }
+          xnorm = __ldcg(xc + ell);
+        }
+      }
+      const bool halt = owner < 0 || !(xnorm > tol);  // qrcp.py:69-71
+      double beta = 0.0, tau = 0.0;
+      if (!halt) {
+        double sq = 0.0;
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+          const int i = lane + 32 * k;
+          if (i >= j && i < ell) sq = __fma_rn(xv[k], xv[k], sq);
+        }
+        sq = warp_sum(sq);
+        double alpha = 0.0;
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+          const double t = __shfl_sync(0xffffffffu, xv[k], j & 31);
+          if ((j >> 5) == k) alpha = t;
+        }
+        const double norm = sqrt(sq);
+        double den = 1.0;
+        const bool zero = norm == 0.0;
+        if (!zero) {
+          beta = alpha >= 0.0 ? -norm : norm;
+          den = __dsub_rn(alpha, beta);
+          tau = __ddiv_rn(__dsub_rn(beta, alpha), beta);
+        }
+        const double rinv = zero ? 1.0 : __drcp_rn(den);
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+          const int i = lane + 32 * k;
+          if (i >= j && i < ell) {
+            const double v = (i == j) ? 1.0 : (zero ? xv[k] : __dmul_rn(xv[k], rinv));
+            wv[i] = v;
+            wtv[i] = __dmul_rn(tau, v);
+          }
+        }
+      }
+      if (lane == 0) {
+        s_step[0] = beta;
+        s_step[1] = tau;
+        s_stepi[0] = halt ? -1 : owner;
+        s_stepi[1] = pw;
+      }
+    }
+    __syncthreads();
+    if (s_stepi[0] < 0) {
+      got = j;
+      break;
+    }
+    const int p = s_stepi[1];
+    const double beta = s_step[0], tau = s_step[1];
+    if (me == 0 && warp == 0) {
+      if (lane == 0) {
+        a.piv[j] = p;
+        if (a.taus) a.taus[j] = tau;
+        const int64_t cols = (int64_t)a.nt - j - 1;
+        if (tau != 0.0 && cols > 0) {
+          l2 += 4LL * (ell - j) * cols;
+          l2b += 16LL * (ell - j) * cols;
+        }
+      }
+      if (a.Ys)
+        for (int i = lane; i < ell; i += 32) a.Ys[(size_t)j * a.ldys + i] = i < j ? 0.0 : wv[i];
+    }
+    mark(0);
+    // ---- my columns: relabel (swap j <-> p), pivot column, H_j, downdate, key
+    double vr[RPL], tvr[RPL];
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+      const int i = gl + 8 * r;
+      const bool act = i >= j && i < ell;
+      vr[r] = act ? wv[i] : 0.0;
+      tvr[r] = act ? wtv[i] : 0.0;
+    }
+    unsigned long long key = 0ull;
+#pragma unroll
+    for (int t = 0; t < CPG; ++t) {
+      int q = pc[t];
+      if (q < 0) continue;
+      if (q == p) {
+        // pivot column: rows < j keep R, row j = beta, below = 0 (qrcp.py:80-81)
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) {
+          const int i = gl + 8 * r;
+          if (i == j) x[t][r] = beta;
+          else if (i > j) x[t][r] = 0.0;
+        }
+        pc[t] = j;
+        continue;
+      }
+      if (q == j && p != j) {
+        q = p;
+        pc[t] = p;
+      }
+      if (q <= j) continue;
+      if (tau != 0.0) {
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int r = 0; r < RPL; r += 2) {
+          d0 = __fma_rn(vr[r], x[t][r], d0);
+          if (r + 1 < RPL) d1 = __fma_rn(vr[r + 1], x[t][r + 1], d1);
+        }
+        double w = __dadd_rn(d0, d1);
+#pragma unroll
+        for (int off = 4; off; off >>= 1) w = __dadd_rn(w, __shfl_xor_sync(gmask, w, off, 8));
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) {
+          const int i = gl + 8 * r;
+          if (i >= j) x[t][r] = __dsub_rn(x[t][r], __dmul_rn(tvr[r], w));
+        }
+      }
+      if (j + 1 < a.nt) {
+        // NormTracker.downdate with row j of the updated sample (kernels.py:222-233)
+        const double rsel = pick_uniform<RPL>(x[t], j >> 3);
+        const double row = __shfl_sync(gmask, rsel, j & 7, 8);
+        double nsq = __dsub_rn(__dmul_rn(nv[t], nv[t]), __dmul_rn(row, row));
+        nsq = nsq > 0.0 ? nsq : 0.0;
+        double nn;
+        if (!(nsq < __dmul_rn(kGuard, og[t]))) {
+          nn = sqrt(nsq);
+        } else {
+          double s0 = 0.0;
+#pragma unroll
+          for (int r = 0; r < RPL; ++r) {
+            const int i = gl + 8 * r;
+            if (i > j && i < ell) s0 = __fma_rn(x[t][r], x[t][r], s0);
+          }
+#pragma unroll
+          for (int off = 4; off; off >>= 1) s0 = __dadd_rn(s0, __shfl_xor_sync(gmask, s0, off, 8));
+          nn = sqrt(s0);
+          og[t] = __dmul_rn(nn, nn);
+        }
+        nv[t] = nn;
+        const unsigned long long kt = make_key(nn, q);
+        key = kt > key ? kt : key;
+      }
+    }
+    key = group_key(key);
+    if (lane == 0) s_wkey[par ^ 1][warp] = key;
+    mark(1);
+    __syncthreads();   // block keys complete; every warp is past its omap reads of step j
+    const unsigned long long bk = block_key(par ^ 1);
+    if (tid == 0) {
+      // the swap j <-> p moves the owners too
+      const unsigned char oj = omap[j];
+      omap[j] = omap[p];
+      omap[p] = oj;
+      // recycle the key slot read at step j - 1 (every CTA passed an exchange since)
+      if constexpr (kCluster) {
+        for (int q = 0; q < P; ++q) s_key[(j + 2) % 3][q] = 0ull;
+      } else if (me == 0) {
+        a.gkey[(j + 2) % 3] = 0ull;
+      }
+    }
+    publish(j + 1, bk);
+    mark(2);
+    xsync();
+    mark(3);
+  }
+  if (timing) {
+    for (int k = 0; k < 4; ++k) a.dbg[k] = tm[k];
+    a.dbg[7] = a.want;
+  }
+  // ---- transformed sample in pivoted order
+#pragma unroll
+  for (int t = 0; t < CPG; ++t) {
+    if (pc[t] < 0) continue;
+    double* dst = a.S + (size_t)pc[t] * a.lds;
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+      const int i = gl + 8 * r;
+      if (i < ell) dst[i] = x[t][r];
+    }
+  }
+  if (me == 0 && tid == 0) {
+    a.st->got = got;
+    a.st->level2 += l2;
+    a.st->l2bytes += l2b;
+    if (a.abort_on_short && got < a.want) {
+      a.st->abort_i0 = a.i0;
+      __threadfence();
+      a.st->abort = kAbortShortSample;
+    }
+  }
+  if constexpr (kCluster) cg::this_cluster().sync();  // peers may still read my smem
+}
+
+
+template <bool kCluster, int RPL, int CPG>
+void launch_reg(Handle& h, int P, size_t smem, SelArgs& a, cudaStream_t s) {
+  auto kern = select_reg_kernel<kCluster, RPL, CPG>;
+  static size_t attr = 0;
+  static bool cl = false;
+  if (kCluster && !cl) {
+    RQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cl = true;
+  }
+  if (smem > attr) {
+    RQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)std::max<size_t>(smem, 48 * 1024)));
+    attr = std::max<size_t>(smem, 48 * 1024);
+  }
+  if constexpr (!kCluster) {
+    void* args[] = {&a};
+    RQ_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(P), dim3(kSelThreads), args, smem, s));
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(P);
+    cfg.blockDim = dim3(kSelThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attrs[1];
+    attrs[0].id = cudaLaunchAttributeClusterDimension;
+    attrs[0].val.clusterDim.x = P;
+    attrs[0].val.clusterDim.y = 1;
+    attrs[0].val.clusterDim.z = 1;
+    cfg.attrs = attrs;
+    cfg.numAttrs = 1;
+    RQ_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+  }
+}
+
+// v5 (register-resident columns) when the CTA's columns fit its 64 groups
+// twice and the sample rows fit the per-lane register budget
+bool launch_select_reg(Handle& h, bool grid, int P, int cpb, int64_t ell, int64_t nt,
+                       int64_t want, const double* B, int64_t ldb, const SelectOut& out,
+                       Status* st, bool abort_on_short, int64_t i0, cudaStream_t s) {
+  constexpr int NG = kSelThreads / 8, NW = kSelThreads / 32;
+  const int cpg = cpb <= NG ? 1 : (cpb <= 2 * NG ? 2 : 0);
+  const int rpl = ell <= 40 ? 5 : (ell <= 72 ? 9 : (ell <= 136 ? 17 : (ell <= 160 ? 20 : 0)));
+  if (cpg == 0 || rpl == 0 || (rpl > 9 && cpg > 1)) return false;
+  const int ldl = (int)(ell | 1);
+  const size_t smem = ((size_t)cpb * ldl + 2 * (size_t)NW * ell + 2 * (ell + 1) + cpb) * 8 +
+                      (size_t)nt + 64;
+  if (smem > h.smem_optin) return false;
+  SelArgs a{};
+  a.ell = (int)ell; a.nt = (int)nt; a.want = (int)want;
+  a.abort_on_short = abort_on_short ? 1 : 0;
+  a.i0 = i0;
+  a.B = B; a.ldb = ldb;
+  a.S = out.S; a.lds = out.lds; a.piv = out.piv; a.Ys = out.Ys; a.ldys = out.ldys;
+  a.taus = out.taus;
+  a.st = st;
+  a.cpb = cpb; a.ldl = ldl; a.ncs = cpb;
+  a.dbg = h.dbg;
+  ProfScope prof(h, kProfSelect, 4.0 * ell * nt * want, 16.0 * ell * nt, s);
+  count_launch();
+  if (grid) {
+    a.bar = (unsigned int*)h.buf("sel_bar", 64, s);
+    a.gkey = (unsigned long long*)h.buf("sel_gkey", 64, s);
+    a.gcol = (double*)h.buf("sel_gcol", (size_t)2 * P * (ell + 1) * 8, s);
+    a.gsq = (double*)h.buf("sel_gsq", (size_t)P * 8, s);
+    RQ_CUDA(cudaMemsetAsync(a.bar, 0, 64, s));
+  }
+#define RQ_SEL_REG(R, C)                                                   \
+  if (rpl == R && cpg == C) {                                             \
+    if (grid) launch_reg<false, R, C>(h, P, smem, a, s);                  \
+    else launch_reg<true, R, C>(h, P, smem, a, s);                        \
+    return true;                                                          \
+  }
+  RQ_SEL_REG(5, 1) RQ_SEL_REG(5, 2) RQ_SEL_REG(9, 1) RQ_SEL_REG(9, 2) RQ_SEL_REG(17, 1)
+  RQ_SEL_REG(20, 1)
+#undef RQ_SEL_REG
+  return false;
+}
+
 }  // namespace
 
 void select_pivots(Handle& h, int64_t ell, int64_t nt, int64_t want, const double* B,
@@ -432,7 +934,8 @@ void select_pivots(Handle& h, int64_t ell, int64_t nt, int64_t want, const doubl
                     (h.force_select == 0 && nt > h.select_cluster_max_cols);
   int P;
   if (grid) {
-    P = (int)std::min<int64_t>(std::min(h.num_sms, 160), (nt + 31) / 32);  // owner ids fit a byte
+    const int cap = h.select_max_ctas > 0 ? std::min(h.select_max_ctas, h.num_sms) : h.num_sms;
+    P = (int)std::min<int64_t>(std::min(cap, 160), (nt + 31) / 32);  // owner ids fit a byte
     P = std::max(P, 1);
     const int cpb = (int)((nt + P - 1) / P);
     P = (int)((nt + cpb - 1) / cpb);
@@ -442,6 +945,9 @@ void select_pivots(Handle& h, int64_t ell, int64_t nt, int64_t want, const doubl
   }
   const int cpb = (int)((nt + P - 1) / P);
   if (cpb > 8192) throw InvalidArg("sample too wide for the pivot kernel");
+  if (h.select_reg && launch_select_reg(h, grid, P, cpb, ell, nt, want, B, ldb, out, st,
+                                        abort_on_short, i0, s))
+    return;
   const int ldl = (int)(ell | 1);
   const size_t meta = ((size_t)2 * ell + 2 * (ell + 1) + 2 * (size_t)cpb + 16) * 8 +
                       (size_t)cpb * 4 + (size_t)nt + 256;

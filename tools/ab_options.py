@@ -22,7 +22,7 @@ lib, h = _abi.load_library(), _abi.handle(0)
 
 DEFAULTS = {"fast_panel": 1, "fast_panel_spec": 1, "fast_panel_max_ctas": 0, "use_rank_update": 1,
             "gemm_vec16": 1, "force_select": 0, "force_panel": 0, "select_cluster_max_cols": 1024,
-            "panel_cluster_max_rows": 3072}
+            "panel_cluster_max_rows": 3072, "select_reg": 1, "select_max_ctas": 0}
 
 
 def setopts(v):
@@ -34,7 +34,7 @@ times = {i: [] for i in range(len(variants))}
 for i, v in enumerate(variants):
     setopts(v)
     bench.run_ours(P, cfg, A, None)
-for rep in range(3):
+for rep in range(int(os.environ.get('AB_REPS', 3))):
     for i, v in enumerate(variants):
         setopts(v)
         torch.cuda.synchronize()
