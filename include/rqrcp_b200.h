@@ -169,6 +169,16 @@ int rq_q_columns(rq_handle_t h, int64_t m, int64_t nref, int64_t cols, const dou
 int rq_frob_norm(rq_handle_t h, const double* A, int64_t m, int64_t n, int64_t lda,
                  double* out, void* stream);
 
+/* ---------------------------------------------------------------- host Omega stream */
+
+/* count values of numpy's Philox(key = k0 + 2^64 k1).standard_normal() stream,
+ * starting at raw 64-bit draw `raw` (0 = a fresh RngState), written to out;
+ * *raw_end = raw position of the next value.  Bit-identical to numpy (its own
+ * ziggurat decoder, libnpyrandom.a), decoded by `threads` host threads.
+ * Replaces the draw loop of the reference's RngState (pkg/src/rqrcp/rng.py:16-41). */
+int rq_omega_fill(uint64_t k0, uint64_t k1, uint64_t raw, double* out, int64_t count, int threads,
+                  uint64_t* raw_end);
+
 /* ---------------------------------------------------------------- instrumentation */
 
 /* tuning knobs: "force_select" / "force_panel" (0 = size heuristic, 1 = grid

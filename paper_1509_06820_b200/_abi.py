@@ -77,6 +77,8 @@ SIGNATURES = {
                                   C.POINTER(f64)]),
     "rq_profile_trace": (C.c_int, [vp, i64, C.POINTER(C.c_int32), C.POINTER(f64), C.POINTER(f64),
                                    C.POINTER(i64)]),
+    "rq_omega_fill": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, dp, i64, C.c_int,
+                                C.POINTER(C.c_uint64)]),
 }
 
 PROF_NAMES = ["sketch", "inner", "update", "small_gemm", "select", "panel", "sample_update",

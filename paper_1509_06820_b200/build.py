@@ -35,6 +35,16 @@ def _deps():
                   + glob.glob(os.path.join(INCLUDE, "*.h")))
 
 
+def _npyrandom():
+    """numpy's static distributions library (random_standard_normal, the
+    ziggurat the reference's Omega stream is drawn with; csrc/omega.cu)."""
+    import numpy
+    lib = os.path.join(os.path.dirname(numpy.__file__), "random", "lib", "libnpyrandom.a")
+    if not os.path.exists(lib):
+        raise RuntimeError(f"numpy's libnpyrandom.a not found at {lib}")
+    return lib
+
+
 def _stale(target, inputs):
     if not os.path.exists(target):
         return True
@@ -66,8 +76,8 @@ def build(force=False, verbose=False, extra=()):
                 logs.append((obj, log))
     objs = [os.path.join(OBJ, os.path.basename(s)[:-3] + ".o") for s in srcs]
     if force or todo or _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", *objs, "-o", LIB, "-lcudart_static",
-               "-lrt", "-lpthread", "-ldl"]
+        cmd = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", *objs, _npyrandom(), "-o", LIB,
+               "-lcudart_static", "-lrt", "-lpthread", "-ldl", "-lm"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
