@@ -134,29 +134,36 @@ __global__ void __launch_bounds__(128) sample_update_reg_kernel(
   for (int i = B; i < ell; ++i) out[i] = s12[i];
 }
 
-// ---------------------------------------------------------------- K6
-// Swap replay as a permutation gather: the ordered swaps (i0+j, i0+piv[j])
-// (randomized.py:138-147) only touch positions {j} U {piv[j]}; the plan
-// kernel replays them on a position->source map (and on perm + the swap log),
-// then every touched column is gathered into scratch and scattered back, each
-// row/column in parallel.  Equivalent to the sequential swaps.
-__global__ void swap_plan_kernel(const int64_t* __restrict__ piv, int64_t i0, SwapTargets t,
-                                 Status* st, int* plan_src) {
+// One-launch replay of the select swaps (randomized.py:138-147): the net
+// permutation of the <= 2 got touched positions is planned redundantly by
+// every block (<= 64 pivots), then each block moves ITS rows of every moved
+// column through shared memory -- all sources of a row chunk are read before
+// any destination is written, and blocks own disjoint rows, so no scratch
+// buffer or second pass is needed.  Units: row chunks of the work matrix, of
+// R's columns and of W's rows (TRQRCP followers).  Block 0 also permutes
+// Permutation.forward and appends the swap log.
+constexpr int kSwapRows = 32;
+__global__ void __launch_bounds__(256) swap_fused_kernel(const int64_t* __restrict__ piv, int64_t i0,
+                                                          SwapTargets t, Status* st, int units_w,
+                                                          int units_r) {
   if (aborted(st)) return;
   const int got = (int)st->got;
-  extern __shared__ int ssw[];
-  int* pv = ssw;               // [got]      piv
-  int* slotb = pv + got;       // [got]      slot of position piv[j]
-  int* src = slotb + got;      // [2 got]    source position currently at each slot
-  // slots: position q < got -> slot q; position q >= got -> got + (first k with piv[k] == q)
-  for (int e = threadIdx.x; e < got; e += blockDim.x) pv[e] = (int)piv[e];
+  extern __shared__ double sbuf[];                 // [2 got][kSwapRows]
+  __shared__ int pv[256], slotb[256], src[512], lsrc[512], ldst[512];
+  __shared__ int s_nlive;
+  __shared__ int64_t s_nswaps;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    s_nlive = 0;
+    s_nswaps = st->nswaps;
+  }
+  for (int e = tid; e < got; e += blockDim.x) pv[e] = (int)piv[e];
   __syncthreads();
-  for (int e = threadIdx.x; e < got; e += blockDim.x) {
+  // slots: position q < got -> slot q; q >= got -> got + first k with piv[k] == q
+  for (int e = tid; e < got; e += blockDim.x) {
     const int q = pv[e];
-    int sl;
-    if (q < got) {
-      sl = q;
-    } else {
+    int sl = q;
+    if (q >= got) {
       int k = e;
       for (int kk = 0; kk < e; ++kk)
         if (pv[kk] == q) { k = kk; break; }
@@ -165,13 +172,9 @@ __global__ void swap_plan_kernel(const int64_t* __restrict__ piv, int64_t i0, Sw
     slotb[e] = sl;
     src[e] = e;
     src[got + e] = q;
-    if (st->nswaps + e < t.log_cap) {  // swap log: stores only
-      t.log[2 * (st->nswaps + e)] = i0 + e;
-      t.log[2 * (st->nswaps + e) + 1] = i0 + q;
-    }
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (tid == 0)
     for (int j = 0; j < got; ++j) {
       const int b = slotb[j];
       if (b != j) {
@@ -180,49 +183,55 @@ __global__ void swap_plan_kernel(const int64_t* __restrict__ piv, int64_t i0, Sw
         src[b] = tmp;
       }
     }
-    st->nswaps += got;
-  }
   __syncthreads();
-  for (int e = threadIdx.x; e < 2 * got; e += blockDim.x) {
-    // slot e holds position q(e); duplicate slots (got + k whose position is
-    // < got, or not the first occurrence) are never used -> -1
+  for (int e = tid; e < 2 * got; e += blockDim.x) {
     const int q = e < got ? e : pv[e - got];
     const bool live = e < got || (q >= got && slotb[e - got] == e);
-    plan_src[e] = (live && src[e] != q) ? src[e] : -1;
-  }
-}
-
-__global__ void swap_move_kernel(const int64_t* __restrict__ piv, int64_t i0, SwapTargets t,
-                                 const Status* st, const int* __restrict__ plan_src,
-                                 double* scratch, int64_t ldsc, double* wsc, double* rsc,
-                                 int to_scratch) {
-  if (aborted(st)) return;
-  const int got = (int)st->got;
-  const int e = blockIdx.y;
-  if (e >= 2 * got) return;
-  const int src = plan_src[e];
-  if (src < 0) return;
-  const int q = e < got ? e : (int)piv[e - got];
-  const int64_t col = i0 + (to_scratch ? src : q);
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < t.m; r += stride) {
-    if (to_scratch) scratch[r + e * ldsc] = t.work[r + col * t.ldw];
-    else t.work[r + col * t.ldw] = scratch[r + e * ldsc];
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {  // Permutation.forward follows the columns
-    if (to_scratch) ((int64_t*)(scratch + 2 * got * ldsc))[e] = t.perm[col];
-    else t.perm[col] = ((const int64_t*)(scratch + 2 * got * ldsc))[e];
-  }
-  if (t.Wf)
-    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < t.wf_cols; c += stride) {
-      if (to_scratch) wsc[c + e * t.wf_cols] = t.Wf[col + c * t.ldwf];
-      else t.Wf[col + c * t.ldwf] = wsc[c + e * t.wf_cols];
+    if (live && src[e] != q) {
+      const int i = atomicAdd(&s_nlive, 1);
+      lsrc[i] = src[e];
+      ldst[i] = q;
     }
-  if (t.Rf)
-    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < t.rf_rows; r += stride) {
-      if (to_scratch) rsc[r + e * t.rf_rows] = t.Rf[r + col * t.ldrf];
-      else t.Rf[r + col * t.ldrf] = rsc[r + e * t.rf_rows];
-    }
+  }
+  __syncthreads();
+  const int nl = s_nlive;
+  if (blockIdx.x == 0) {
+    int64_t* pbuf = (int64_t*)sbuf;
+    for (int i = tid; i < nl; i += blockDim.x) pbuf[i] = t.perm[i0 + lsrc[i]];
+    for (int e = tid; e < got; e += blockDim.x)
+      if (s_nswaps + e < t.log_cap) {   // swap log: stores only
+        t.log[2 * (s_nswaps + e)] = i0 + e;
+        t.log[2 * (s_nswaps + e) + 1] = i0 + pv[e];
+      }
+    __syncthreads();
+    for (int i = tid; i < nl; i += blockDim.x) t.perm[i0 + ldst[i]] = pbuf[i];
+    if (tid == 0) st->nswaps = s_nswaps + got;
+    __syncthreads();
+  }
+  if (nl == 0) return;
+  // my unit: a chunk of kSwapRows "rows" of one follower array
+  int u = blockIdx.x;
+  double* base;
+  int64_t rows, rstride, cstride;
+  if (u < units_w) {
+    base = t.work; rows = t.m; rstride = 1; cstride = t.ldw;
+  } else if ((u -= units_w) < units_r) {
+    base = t.Rf; rows = t.rf_rows; rstride = 1; cstride = t.ldrf;
+  } else {
+    u -= units_r;
+    base = t.Wf; rows = t.wf_cols; rstride = t.ldwf; cstride = 1;
+  }
+  const int64_t r0 = (int64_t)u * kSwapRows;
+  const int nr = (int)imin64(kSwapRows, rows - r0);
+  for (int e = tid; e < nl * kSwapRows; e += blockDim.x) {
+    const int i = e / kSwapRows, r = e - i * kSwapRows;
+    if (r < nr) sbuf[e] = base[(r0 + r) * rstride + (i0 + lsrc[i]) * cstride];
+  }
+  __syncthreads();
+  for (int e = tid; e < nl * kSwapRows; e += blockDim.x) {
+    const int i = e / kSwapRows, r = e - i * kSwapRows;
+    if (r < nr) base[(r0 + r) * rstride + (i0 + ldst[i]) * cstride] = sbuf[e];
+  }
 }
 
 // ---------------------------------------------------------------- K10
@@ -388,23 +397,21 @@ void sample_update(Handle& h, int64_t ell, int64_t b, int64_t n2, const double* 
 
 void apply_swaps(Handle& h, const int64_t* piv, int64_t got_max, int64_t i0,
                  const SwapTargets& t, Status* st, cudaStream_t s) {
-  const int64_t ne = 2 * got_max;
-  int* plan = (int*)h.buf("swap_plan", (size_t)ne * 4 + 64, s);
-  double* sc = (double*)h.buf("swap_scratch", (size_t)ne * t.m * 8 + (size_t)ne * 8 + 64, s);
-  double* wsc = t.Wf ? (double*)h.buf("swap_wsc", (size_t)ne * t.wf_cols * 8 + 64, s) : nullptr;
-  double* rsc = t.Rf ? (double*)h.buf("swap_rsc", (size_t)ne * t.rf_rows * 8 + 64, s) : nullptr;
+  if (got_max > 256) throw InvalidArg("at most 256 pivots per block");
   ProfScope prof(h, kProfSwap, 0.0, 32.0 * got_max * t.m, s);
-  swap_plan_kernel<<<1, 256, (size_t)4 * got_max * 4, s>>>(piv, i0, t, st, plan);
+  const int uw = (int)((t.m + kSwapRows - 1) / kSwapRows);
+  const int ur = t.Rf ? (int)((t.rf_rows + kSwapRows - 1) / kSwapRows) : 0;
+  const int uf = t.Wf ? (int)((t.wf_cols + kSwapRows - 1) / kSwapRows) : 0;
+  const size_t smem = (size_t)2 * got_max * kSwapRows * 8;
+  static size_t attr = 0;
+  if (smem > attr) {
+    RQ_CUDA(cudaFuncSetAttribute(swap_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)std::max<size_t>(smem, 48 * 1024)));
+    attr = std::max<size_t>(smem, 48 * 1024);
+  }
+  swap_fused_kernel<<<std::max(uw + ur + uf, 1), 256, smem, s>>>(piv, i0, t, st, uw, ur);
   RQ_CHECK_LAUNCH();
-  const int64_t mx = std::max<int64_t>(std::max<int64_t>(t.m, 1),
-                                       std::max<int64_t>(t.Wf ? t.wf_cols : 0, t.Rf ? t.rf_rows : 0));
-  const unsigned gx = (unsigned)std::min<int64_t>((mx + 255) / 256, 64);
-  dim3 grid(gx, (unsigned)ne);
-  swap_move_kernel<<<grid, 256, 0, s>>>(piv, i0, t, st, plan, sc, t.m, wsc, rsc, 1);
-  RQ_CHECK_LAUNCH();
-  swap_move_kernel<<<grid, 256, 0, s>>>(piv, i0, t, st, plan, sc, t.m, wsc, rsc, 0);
-  RQ_CHECK_LAUNCH();
-  count_launch(3);
+  count_launch();
 }
 
 void frob_norm(Handle& h, const double* A, int64_t m, int64_t n, int64_t lda, double* out,
