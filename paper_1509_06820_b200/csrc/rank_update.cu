@@ -134,6 +134,167 @@ __global__ void __launch_bounds__(kRuThreads, 1) rank_update_kernel(RuArgs a) {
   }
 }
 
+// Specialisation for the block widths in use (K = 32, 64) with 16-byte
+// aligned operands: the k-loop unrolls to immediate shared-memory offsets and
+// every thread's cp.async pattern within a tile is fixed, so a tile's copies
+// are a base pointer plus constant strides (the generic kernel above spends
+// ~45% of its issue slots on per-element address arithmetic -- ncu source
+// counters, profiles/).  Edge tiles take the checked path.
+template <int K>
+__global__ void __launch_bounds__(kRuThreads, 1) rank_update_k_kernel(RuArgs a) {
+  if (aborted(a.st)) return;
+  constexpr int LDB = K + 4;
+  constexpr int SA = K * kLdA, SB = kTN * LDB, SC = kTN * kLdC;
+  extern __shared__ __align__(16) double sm[];
+  double* As = sm;
+  double* Bs = As + 2 * SA;
+  double* Cs = Bs + 2 * SB;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm0 = (warp & 1) * 32, wn0 = (warp >> 1) * 16;
+  const int fr = lane >> 2, fk = lane & 3;
+  const int64_t M = a.M, N = a.N;
+  const int64_t tm = (M + kTM - 1) / kTM, tn = (N + kTN - 1) / kTN;
+  const int64_t ntiles = tm * tn;
+  const int64_t t_lo = ntiles * blockIdx.x / gridDim.x;
+  const int64_t t_hi = ntiles * (blockIdx.x + 1) / gridDim.x;
+  const int64_t ldy = a.ldy, ldx = a.ldx, ldc = a.ldc;
+  // fixed per-thread copy pattern (16 B per cp.async)
+  //   Y tile As[k][m]: k = (tid >> 5) + 8 q, m = 2 (tid & 31)        q < K / 8
+  //   C tile Cs[n][m]: n = (tid >> 5) + 8 q, m = 2 (tid & 31)        q < 8
+  //   X tile Bs[n][k]: per = K / 2 pairs per column
+  constexpr int XPER = K / 2, XROWS = kRuThreads / XPER;   // columns per pass
+  const int ym = 2 * (tid & 31), yk = tid >> 5;
+  const int xk = 2 * (tid % XPER), xn = tid / XPER;
+  auto load_full = [&](int64_t t, int b, int xs, bool load_x) {
+    const int64_t m0 = (t % tm) * kTM, n0 = (t / tm) * kTN;
+    {
+      const double* g = a.Y + m0 + ym + yk * ldy;
+      double* d = As + b * SA + yk * kLdA + ym;
+#pragma unroll
+      for (int q = 0; q < K / 8; ++q) cp_async16(d + q * 8 * kLdA, g + q * 8 * ldy, 16);
+    }
+    if (load_x) {
+      const double* g = a.X + xk + (n0 + xn) * ldx;
+      double* d = Bs + xs * SB + xn * LDB + xk;
+#pragma unroll
+      for (int q = 0; q < kTN / XROWS; ++q) cp_async16(d + q * XROWS * LDB, g + q * XROWS * ldx, 16);
+    }
+    {
+      const double* g = a.C + m0 + ym + (n0 + yk) * ldc;
+      double* d = Cs + b * SC + yk * kLdC + ym;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) cp_async16(d + q * 8 * kLdC, g + q * 8 * ldc, 16);
+    }
+    cp_async_commit();
+  };
+  auto load_edge = [&](int64_t t, int b, int xs, bool load_x) {
+    const int64_t m0 = (t % tm) * kTM, n0 = (t / tm) * kTN;
+    for (int e = tid; e < K * kTM; e += kRuThreads) {
+      const int k = e / kTM, i = e % kTM;
+      const bool ok = m0 + i < M;
+      cp_async8(As + b * SA + k * kLdA + i, ok ? a.Y + m0 + i + k * ldy : a.Y, ok);
+    }
+    if (load_x)
+      for (int e = tid; e < kTN * K; e += kRuThreads) {
+        const int n = e / K, k = e % K;
+        const bool ok = n0 + n < N;
+        cp_async8(Bs + xs * SB + n * LDB + k, ok ? a.X + k + (n0 + n) * ldx : a.X, ok);
+      }
+    for (int e = tid; e < kTN * kTM; e += kRuThreads) {
+      const int n = e / kTM, i = e % kTM;
+      const bool ok = m0 + i < M && n0 + n < N;
+      cp_async8(Cs + b * SC + n * kLdC + i, ok ? a.C + m0 + i + (n0 + n) * ldc : a.C, ok);
+    }
+    cp_async_commit();
+  };
+  auto full_tile = [&](int64_t t) {
+    return ((t % tm) + 1) * kTM <= M && ((t / tm) + 1) * kTN <= N;
+  };
+  auto load_tile = [&](int64_t t, int b, int xs, bool load_x) {
+    if (full_tile(t)) load_full(t, b, xs, load_x);
+    else load_edge(t, b, xs, load_x);
+  };
+
+  int xs = 0;
+  if (t_lo < t_hi) load_tile(t_lo, 0, 0, true);
+  int buf = 0;
+  for (int64_t t = t_lo; t < t_hi; ++t, buf ^= 1) {
+    int xs_next = xs;
+    if (t + 1 < t_hi) {
+      const bool newx = (t + 1) / tm != t / tm;
+      if (newx) xs_next = xs ^ 1;
+      load_tile(t + 1, buf ^ 1, xs_next, newx);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* as = As + buf * SA + wm0 + fr;
+    const double* bs = Bs + xs * SB + (wn0 + fr) * LDB;
+    const double* cs = Cs + buf * SC;
+    double acc[4][2][2];
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 2; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+#pragma unroll
+    for (int k4 = 0; k4 < K; k4 += 4) {
+      double af[4], bf[2];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) af[x] = as[(k4 + fk) * kLdA + x * 8];
+#pragma unroll
+      for (int y = 0; y < 2; ++y) bf[y] = bs[y * 8 * LDB + k4 + fk];
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 2; ++y) dmma884(acc[x][y], af[x], bf[y]);
+    }
+    // epilogue: C - acc (C from shared memory; separate subtraction, numpy's C - Y @ X)
+    const int64_t m0 = (t % tm) * kTM, n0 = (t / tm) * kTN;
+    if (full_tile(t)) {
+      double* ct = a.C + (m0 + wm0 + fr) + (n0 + wn0 + 2 * fk) * ldc;
+      const double* cst = cs + (wn0 + 2 * fk) * kLdC + wm0 + fr;
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 2; ++y)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            ct[x * 8 + (y * 8 + e) * ldc] =
+                __dsub_rn(cst[(y * 8 + e) * kLdC + x * 8], acc[x][y][e]);
+    } else {
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        const int i = wm0 + x * 8 + fr;
+        const int64_t gi = m0 + i;
+        if (gi >= M) continue;
+#pragma unroll
+        for (int y = 0; y < 2; ++y)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int j = wn0 + y * 8 + 2 * fk + e;
+            const int64_t gj = n0 + j;
+            if (gj < N) a.C[gi + gj * ldc] = __dsub_rn(cs[j * kLdC + i], acc[x][y][e]);
+          }
+      }
+    }
+    __syncthreads();  // buffers `buf` / X slot reloaded by the next prefetch
+    xs = xs_next;
+  }
+}
+
+template <int K>
+void launch_rank_update_k(Handle& h, const RuArgs& a, int grid, cudaStream_t s) {
+  constexpr size_t smem = (size_t)2 * (K * kLdA + kTN * (K + 4) + kTN * kLdC) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    RQ_CUDA(cudaFuncSetAttribute(rank_update_k_kernel<K>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  rank_update_k_kernel<K><<<grid, kRuThreads, smem, s>>>(a);
+}
+
 }  // namespace
 
 bool rank_update(Handle& h, int64_t M, int64_t N, int64_t K, const double* Y, int64_t ldy,
@@ -152,7 +313,9 @@ bool rank_update(Handle& h, int64_t M, int64_t N, int64_t K, const double* Y, in
   const int64_t ntiles = ((M + kTM - 1) / kTM) * ((N + kTN - 1) / kTN);
   const int grid = (int)std::min<int64_t>(h.num_sms, ntiles);
   ProfScope prof(h, cat, 2.0 * M * N * K, 8.0 * ((double)M * K + (double)K * N + 2.0 * M * N), s);
-  rank_update_kernel<<<grid, kRuThreads, kRuSmem, s>>>(a);
+  if (a.vec16 && K == 64) launch_rank_update_k<64>(h, a, grid, s);
+  else if (a.vec16 && K == 32) launch_rank_update_k<32>(h, a, grid, s);
+  else rank_update_kernel<<<grid, kRuThreads, kRuSmem, s>>>(a);
   RQ_CHECK_LAUNCH();
   count_launch();
   return true;
