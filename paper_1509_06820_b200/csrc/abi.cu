@@ -263,6 +263,8 @@ int rq_set_option(rq_handle_t h, const char* name, int64_t value) {
     else if (n == "profile_trace") hh.tracing = value != 0;
     else if (n == "select_max_ctas") hh.select_max_ctas = (int)value;
     else if (n == "select_reg") hh.select_reg = value != 0;
+    else if (n == "overlap_select") hh.overlap_select = value != 0;
+    else if (n == "overlap_sel_ctas") hh.overlap_sel_ctas = (int)value;
     else if (n == "gemm_vec16") hh.gemm_vec16 = value != 0;
     else if (n == "debug_timers") {
       hh.dbg = value ? (long long*)hh.buf("dbg_timers", 64 * 8, nullptr) : nullptr;

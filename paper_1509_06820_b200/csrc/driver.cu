@@ -36,7 +36,7 @@ struct Pending {
 
 class Factor {
  public:
-  Factor(Handle& h, const FactorParams& p) : h_(h), p_(p), s_(p.stream) {}
+  Factor(Handle& h, const FactorParams& p) : h_(h), p_(p), s_(p.stream), ev_(h.ring_ev) {}
 
   FactorResult run();
 
@@ -46,8 +46,9 @@ class Factor {
   cudaStream_t s_;
   Status* st_ = nullptr;   // device
   Status* hst_ = nullptr;  // pinned
+  Status* pre_ = nullptr;  // device: abort word before a block's sample update
   int* hring_ = nullptr;   // pinned abort snapshots
-  std::vector<cudaEvent_t> ev_;
+  std::vector<cudaEvent_t>& ev_;   // retire events (owned by the handle)
   double *B_ = nullptr, *S_ = nullptr, *T_ = nullptr, *G_ = nullptr, *X_ = nullptr;
   double *om_d_ = nullptr, *om_h_ = nullptr, *P_ = nullptr, *Z_ = nullptr;
   int64_t* piv_ = nullptr;
@@ -70,11 +71,13 @@ class Factor {
   void draw_omega(int64_t rows, int64_t cols);
   void first_sample();
   void fresh_sample(int64_t i0);
-  void select(int64_t i0, int64_t want, bool spec);
+  void select(int64_t i0, int64_t want, bool spec, cudaStream_t s = nullptr, int max_ctas = 0);
   void swaps(int64_t i0, int64_t got);
   void panel(int64_t i0, int64_t got, PanelPolicy pol, bool spec, Counters& c,
              bool allow_fast = true);
-  void stages(int64_t i0, int64_t bw, Counters& c);
+  void stages(int64_t i0, int64_t bw, Counters& c, bool defer_trailing = false);
+  void trailing(int64_t i0, int64_t bw, int max_ctas, const Status* pred);
+  int overlap_split(int64_t i0, int64_t bw) const;
   void update(int64_t i0_new, int64_t bw, bool spec, Counters& c);
   bool slow_block(int64_t& i0, bool resampled, int64_t& rank, bool resume_panel = false);
 };
@@ -122,9 +125,9 @@ void Factor::fresh_sample(int64_t i0) {
   }
 }
 
-void Factor::select(int64_t i0, int64_t want, bool spec) {
+void Factor::select(int64_t i0, int64_t want, bool spec, cudaStream_t s, int max_ctas) {
   SelectOut o{S_, ell_, piv_, nullptr, 0, nullptr};
-  select_pivots(h_, ell_, n_ - i0, want, B_, ell_, o, st_, spec, i0, s_);
+  select_pivots(h_, ell_, n_ - i0, want, B_, ell_, o, st_, spec, i0, s ? s : s_, max_ctas);
 }
 
 void Factor::swaps(int64_t i0, int64_t got) {
@@ -166,7 +169,7 @@ void Factor::panel(int64_t i0, int64_t got, PanelPolicy pol, bool spec, Counters
 }
 
 // _block_stages (randomized.py:158-180) / trqrcp W+R update (truncated.py:453-470)
-void Factor::stages(int64_t i0, int64_t bw, Counters& c) {
+void Factor::stages(int64_t i0, int64_t bw, Counters& c, bool defer_trailing) {
   const int64_t mm = m_ - i0, nt2 = n_ - i0 - bw;
   if (nt2 <= 0) return;
   const double* Yb = p_.Y + i0 + i0 * p_.ldy;
@@ -177,8 +180,9 @@ void Factor::stages(int64_t i0, int64_t bw, Counters& c) {
     gemm(h_, true, false, bw, nt2, bw, 1.0, T_, b_, G_, bw, 0.0, X_, bw, s_, st_);
     c.gemm_flops += 2 * mm * bw * nt2 + bw * bw * nt2;
     const bool trail = p_.update_trailing && i0 + bw < m_;
-    gemm(h_, false, false, trail ? mm : bw, nt2, bw, -1.0, Yb, p_.ldy, X_, bw, 1.0, C, p_.ldw, s_,
-         st_, kProfUpdate);
+    // defer_trailing: only R12 = C[:b] - Y[:b] X here; trailing() does C[b:]
+    gemm(h_, false, false, (trail && !defer_trailing) ? mm : bw, nt2, bw, -1.0, Yb, p_.ldy, X_, bw,
+         1.0, C, p_.ldw, s_, st_, kProfUpdate);
     c.gemm_flops += 2 * bw * bw * nt2;
     touch(c, mm * nt2 + mm * bw + bw * nt2);
     if (trail) {
@@ -207,6 +211,36 @@ void Factor::stages(int64_t i0, int64_t bw, Counters& c) {
        Rr, p_.ldR, s_, st_);
   c.gemm_flops += 2 * bw * (i0 + bw) * nt2;
   touch(c, bw * n_ + nt2 * (i0 + bw));
+}
+
+// C[b:] -= Y[b:] X of the block at i0 (the rows stages() deferred), on at
+// most max_ctas SMs (the rest run the next block's select meanwhile)
+// `pred` is the Status predicate: a snapshot of the abort word taken before
+// the block's sample update, so a degenerate verdict (which keeps this block
+// committed, randomized.py:253-258) cannot skip the rows it still owes.
+void Factor::trailing(int64_t i0, int64_t bw, int max_ctas, const Status* pred) {
+  const int64_t mm = m_ - i0, nt2 = n_ - i0 - bw;
+  if (nt2 <= 0 || mm <= bw) return;
+  const double* Yb = p_.Y + i0 + bw + i0 * p_.ldy;
+  double* C = p_.work + i0 + bw + (i0 + bw) * p_.ldw;
+  if (!rank_update(h_, mm - bw, nt2, bw, Yb, p_.ldy, X_, bw, C, p_.ldw, s_, pred, kProfUpdate,
+                   max_ctas))
+    gemm(h_, false, false, mm - bw, nt2, bw, -1.0, Yb, p_.ldy, X_, bw, 1.0, C, p_.ldw, s_, pred,
+         kProfUpdate);
+}
+
+// SMs for the next block's select while the trailing update of the block at
+// i0 runs on the rest.  The select is latency bound (64 steps of a few us,
+// nearly flat in its CTA count down to ~1/3 of the GPU), the update is not:
+// a fixed ~38% share (56 of 148 SMs) was measured best on cfg2 (40: 109.6 ms,
+// 48: 106.1, 56: 105.6, 64: 107.4; no overlap 112.4); the cluster variant
+// (narrow samples) uses 16.
+int Factor::overlap_split(int64_t i0, int64_t bw) const {
+  const int64_t nt1 = n_ - i0 - bw;
+  const int sms = h_.num_sms;
+  if (nt1 <= h_.select_cluster_max_cols) return 16;   // cluster variant
+  const int P = h_.overlap_sel_ctas > 0 ? h_.overlap_sel_ctas : (int)(0.38 * sms + 0.5);
+  return std::max(16, std::min(P, sms - 16));
 }
 
 // sample_update after a committed block ending at i0_new (randomized.py:253-255)
@@ -289,6 +323,7 @@ FactorResult Factor::run() {
   if (ell_ > m_) throw InvalidArg("sample rows exceed matrix rows");
   if (b_ < 1 || b_ > 256) throw InvalidArg("block must be in [1, 256]");
   st_ = (Status*)h_.buf("st", sizeof(Status), s_);
+  pre_ = (Status*)h_.buf("st_pre", sizeof(Status), s_);
   hst_ = (Status*)h_.host_pinned("hst", sizeof(Status), s_);
   hring_ = (int*)h_.host_pinned("hring", 64 * sizeof(int), s_);
   B_ = (double*)h_.buf("sampleB", (size_t)ell_ * n_ * 8, s_);
@@ -331,6 +366,8 @@ FactorResult Factor::run() {
   }
   std::deque<Pending> pend;
   int slot = 0;
+  const bool overlap = speculate && h_.overlap_select && !p_.truncated && p_.update_trailing;
+  bool next_selected = false;   // the next block's select was launched with the previous block
   int64_t i0 = 0, rank = k_;
   bool stopped = false;
   while (true) {
@@ -356,6 +393,8 @@ FactorResult Factor::run() {
           }
         }
         pend.clear();
+        if (overlap) RQ_CUDA(cudaStreamSynchronize(h_.side_stream()));
+        next_selected = false;
         RQ_CUDA(cudaMemsetAsync(&st_->abort, 0, sizeof(int), s_));
         if (code == kAbortDegenerate) {
           i0 = X + bwX;
@@ -390,12 +429,30 @@ FactorResult Factor::run() {
     Pending e{};
     e.i0 = i0;
     e.bw = want;
-    select(i0, want, true);
+    if (!next_selected) select(i0, want, true);   // else launched during the previous block
+    next_selected = false;
     swaps(i0, want);
     panel(i0, want, kPanelCommitIfFull, true, e.stage);
-    stages(i0, want, e.stage);
     e.has_update = i0 + want < k_;
+    // RQRCP: the next block's select only needs the sample update (R11, R12),
+    // so it runs on a side stream on a share of the SMs while the trailing
+    // rows of this block's update run on the rest (join before its swaps)
+    const bool ovl = overlap && e.has_update && m_ - i0 > want;
+    stages(i0, want, e.stage, ovl);
+    if (ovl) RQ_CUDA(cudaMemcpyAsync(&pre_->abort, &st_->abort, sizeof(int),
+                                     cudaMemcpyDeviceToDevice, s_));
     if (e.has_update) update(i0 + want, want, true, e.update);
+    if (ovl) {
+      const int P = overlap_split(i0, want);
+      cudaStream_t s2 = h_.side_stream();
+      RQ_CUDA(cudaEventRecord(h_.ev_fork, s_));
+      RQ_CUDA(cudaStreamWaitEvent(s2, h_.ev_fork, 0));
+      select(i0 + want, std::min(b_, k_ - i0 - want), true, s2, P);
+      trailing(i0, want, h_.num_sms - P, pre_);
+      RQ_CUDA(cudaEventRecord(h_.ev_join, s2));
+      RQ_CUDA(cudaStreamWaitEvent(s_, h_.ev_join, 0));
+      next_selected = true;
+    }
     e.slot = slot;
     RQ_CUDA(cudaMemcpyAsync(&hring_[slot], &st_->abort, sizeof(int), cudaMemcpyDeviceToHost, s_));
     RQ_CUDA(cudaEventRecord(ev_[slot], s_));

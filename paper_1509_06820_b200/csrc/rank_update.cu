@@ -299,7 +299,7 @@ void launch_rank_update_k(Handle& h, const RuArgs& a, int grid, cudaStream_t s) 
 
 bool rank_update(Handle& h, int64_t M, int64_t N, int64_t K, const double* Y, int64_t ldy,
                  const double* X, int64_t ldx, double* C, int64_t ldc, cudaStream_t s,
-                 const Status* st, int cat) {
+                 const Status* st, int cat, int max_ctas) {
   if (K < 4 || K > kKMax || (K % 4) != 0 || M <= 0 || N <= 0) return false;
   static bool attr = false;
   if (!attr) {
@@ -311,7 +311,8 @@ bool rank_update(Handle& h, int64_t M, int64_t N, int64_t K, const double* Y, in
   RuArgs a{M, N, (int)K, Y, ldy, X, ldx, C, ldc, st,
            (h.gemm_vec16 && al(Y, ldy) && al(X, ldx) && al(C, ldc)) ? 1 : 0};
   const int64_t ntiles = ((M + kTM - 1) / kTM) * ((N + kTN - 1) / kTN);
-  const int grid = (int)std::min<int64_t>(h.num_sms, ntiles);
+  const int cap = max_ctas > 0 ? std::min(max_ctas, h.num_sms) : h.num_sms;
+  const int grid = (int)std::min<int64_t>(cap, ntiles);
   ProfScope prof(h, cat, 2.0 * M * N * K, 8.0 * ((double)M * K + (double)K * N + 2.0 * M * N), s);
   if (a.vec16 && K == 64) launch_rank_update_k<64>(h, a, grid, s);
   else if (a.vec16 && K == 32) launch_rank_update_k<32>(h, a, grid, s);

@@ -81,7 +81,22 @@ Handle::Handle(int dev) : device(dev) {
   smem_optin = (size_t)optin;
 }
 
+cudaStream_t Handle::side_stream() {
+  if (side_ == nullptr) {
+    RQ_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+    RQ_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    RQ_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+  }
+  return side_;
+}
+
 Handle::~Handle() {
+  if (side_ != nullptr) {
+    cudaStreamDestroy(side_);
+    cudaEventDestroy(ev_fork);
+    cudaEventDestroy(ev_join);
+  }
+  for (auto e : ring_ev) cudaEventDestroy(e);
   for (auto e : free_ev_) cudaEventDestroy(e);
   for (auto& p : pend_) {
     cudaEventDestroy(p.a);

@@ -82,6 +82,11 @@ class Handle {
   // grow-only named device buffer; synchronises `s` before re-allocating
   void* buf(const std::string& name, size_t bytes, cudaStream_t s);
   void* host_pinned(const std::string& name, size_t bytes, cudaStream_t s);
+  // side stream + fork/join events for the select || trailing-update overlap,
+  // and the speculative driver's retire events (created once per handle)
+  cudaStream_t side_stream();
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  std::vector<cudaEvent_t> ring_ev;
 
   // kernel-variant overrides (0 = size heuristic, 1 = grid, 2 = cluster)
   int force_select = 0, force_panel = 0;
@@ -98,6 +103,9 @@ class Handle {
   // speculative driver on a declined fast panel: 0 = always rewind, 1 = rewind
   // once then queue the exact kernel behind every fast panel, 2 = never rewind
   int fast_panel_spec = 1;
+  // speculative RQRCP: next block's select concurrently with the trailing update
+  bool overlap_select = true;
+  int overlap_sel_ctas = 0;   // SMs for the overlapped select (0 = size heuristic)
   bool gemm_vec16 = true;
   long long* dbg = nullptr;  // optional device phase-timer buffer (debug)
 
@@ -124,6 +132,7 @@ class Handle {
   };
   std::vector<PendEv> pend_;
   cudaEvent_t trace_base_ = nullptr;
+  cudaStream_t side_ = nullptr;
   std::vector<cudaEvent_t> free_ev_;
   cudaEvent_t take_event();
   struct Buf {
@@ -143,7 +152,7 @@ void gemm(Handle& h, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double a
 // persistent C -= Y X for K <= 64 (rank_update.cu); false if not applicable
 bool rank_update(Handle& h, int64_t M, int64_t N, int64_t K, const double* Y, int64_t ldy,
                  const double* X, int64_t ldx, double* C, int64_t ldc, cudaStream_t s,
-                 const Status* st, int cat);
+                 const Status* st, int cat, int max_ctas = 0);
 
 // ------------------------------------------------------------------ kernels (small.cu, select.cu, panel.cu)
 struct SelectOut {
@@ -156,7 +165,7 @@ struct SelectOut {
 // abort_on_short: set Status.abort = kAbortShortSample when got < want.
 void select_pivots(Handle& h, int64_t ell, int64_t nt, int64_t want, const double* B,
                    int64_t ldb, const SelectOut& out, Status* st, bool abort_on_short,
-                   int64_t i0, cudaStream_t s);
+                   int64_t i0, cudaStream_t s, int max_ctas = 0);
 
 struct PanelOut {
   double* Rdst; int64_t ldr; int64_t rrows;   // transformed panel rows [0, rrows)

@@ -924,7 +924,7 @@ bool launch_select_reg(Handle& h, bool grid, int P, int cpb, int64_t ell, int64_
 
 void select_pivots(Handle& h, int64_t ell, int64_t nt, int64_t want, const double* B,
                    int64_t ldb, const SelectOut& out, Status* st, bool abort_on_short,
-                   int64_t i0, cudaStream_t s) {
+                   int64_t i0, cudaStream_t s, int max_ctas) {
   if (want < 1 || want > std::min(ell, nt))
     throw InvalidArg("cannot select " + std::to_string(want) + " pivots from a " +
                      std::to_string(ell) + " x " + std::to_string(nt) + " sample");
@@ -934,7 +934,8 @@ void select_pivots(Handle& h, int64_t ell, int64_t nt, int64_t want, const doubl
                     (h.force_select == 0 && nt > h.select_cluster_max_cols);
   int P;
   if (grid) {
-    const int cap = h.select_max_ctas > 0 ? std::min(h.select_max_ctas, h.num_sms) : h.num_sms;
+    int cap = h.select_max_ctas > 0 ? std::min(h.select_max_ctas, h.num_sms) : h.num_sms;
+    if (max_ctas > 0) cap = std::min(cap, max_ctas);
     P = (int)std::min<int64_t>(std::min(cap, 160), (nt + 31) / 32);  // owner ids fit a byte
     P = std::max(P, 1);
     const int cpb = (int)((nt + P - 1) / P);

@@ -54,4 +54,19 @@ print(json.dumps({"busy": {k: round(v, 2) for k, v in busy.items()}}))
 print(json.dumps({"gap_before": {k: round(v, 2) for k, v in gap_before.items()}}))
 print(json.dumps({"gap_after": {k: round(v, 2) for k, v in gap_after.items()}}))
 print(json.dumps({"largest_gaps": sorted(big, reverse=True)[:15]}))
+# concurrency: time where a select interval overlaps an update interval
+sel = [(a, b) for a, b, nm in recs if nm == "select"]
+upd = [(a, b) for a, b, nm in recs if nm == "update"]
+ov = 0.0
+j = 0
+for a, b in sel:
+    for c, d in upd:
+        ov += max(0.0, min(b, d) - max(a, c))
+print(json.dumps({"select_update_overlap_ms": round(ov, 2), "select_ms": round(sum(b - a for a, b in sel), 2),
+                  "update_ms": round(sum(b - a for a, b in upd), 2)}))
+pairs = []
+for a, b in sel[:200]:
+    best = max(((min(b, d) - max(a, c)), c, d) for c, d in upd) if upd else (0, 0, 0)
+    pairs.append((round(a, 3), round(b - a, 3), round(best[0], 3), round(best[2] - best[1], 3)))
+print(json.dumps({"first_selects(start,dur,overlap,upd_dur)": pairs[:12]}))
 _abi.check(lib.rq_set_option(h, b"profile_trace", 0))
