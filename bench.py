@@ -254,7 +254,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg2")
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -363,7 +363,11 @@ def main():
         i = _abi.PROF_NAMES.index(dom)
         ach = FL[i] / (MS[i] * 1e-3) / 1e12
         pk = peak["dmma_f64_tflops"] if peak else 37.2
-        roofline = {"bound": "tensor", "kernel": f"gemm_f64_kernel ({dom})", "achieved": ach,
+        kname = {"update": "rank_update_k_kernel<b> (C -= Y X, K = b, persistent)",
+                 "inner": "gemm_f64_kernel (G = Y^T C, split-K)",
+                 "sketch": "gemm_f64_kernel (B = Omega A)",
+                 "small_gemm": "gemm_f64_kernel (small products)"}.get(dom, dom)
+        roofline = {"bound": "tensor", "kernel": kname, "achieved": ach,
                     "peak": pk, "unit": "TFLOP/s", "frac": ach / pk,
                     "traffic": traffic_from_profiles(dom),
                     "peak_source": ("measured DMMA.8x8x4 microbenchmark in this run "
@@ -384,7 +388,10 @@ def main():
         Ah = torch.empty((cfg["n"], cfg["m"]), dtype=torch.float64).pin_memory().t()
         Ah.copy_(A)
         Ahost = Ah.numpy()
-        f = run_ours(P, cfg, Ahost, None)  # warm-up of the host path
+        # W warm-up calls of the host path, as for the device leg (the first
+        # calls also size torch's caching pinned-host allocator for results)
+        for _ in range(max(args.warmup, 1)):
+            f = run_ours(P, cfg, Ahost, None)
         d2h = result_bytes(f, cfg)
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()

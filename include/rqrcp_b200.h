@@ -77,6 +77,13 @@ typedef struct {
   rq_omega_fn omega_fn;  /* host Omega stream for (re)samples */
   void* omega_user;
   void* stream;
+  /* optional host (pinned) outputs, filled while the factorization runs: the
+   * columns of Y (m x k) and of R (k x n; RQRCP: work rows 0..k-1) are
+   * streamed out as their blocks commit (later blocks never touch them) */
+  double* host_Y;
+  int64_t ldhY;
+  double* host_R;
+  int64_t ldhR;
 } rq_factor_args;
 
 typedef struct {

@@ -29,6 +29,7 @@ class FactorArgs(C.Structure):
         ("W", dp), ("ldW", i64), ("R", dp), ("ldR", i64),
         ("perm", lp), ("swaps", lp), ("swap_cap", i64),
         ("omega0", dp), ("omega_fn", OMEGA_FN), ("omega_user", vp), ("stream", vp),
+        ("host_Y", dp), ("ldhY", i64), ("host_R", dp), ("ldhR", i64),
     ]
 
 

@@ -67,6 +67,8 @@ rq::FactorParams to_params(const rq_factor_args& a) {
   p.omega0 = a.omega0; p.omega_fn = a.omega_fn; p.omega_user = a.omega_user;
   p.speculate = a.speculate;
   p.stream = S(a.stream);
+  p.host_Y = a.host_Y; p.ldhY = a.ldhY;
+  p.host_R = a.host_R; p.ldhR = a.ldhR;
   return p;
 }
 

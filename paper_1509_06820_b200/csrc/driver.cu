@@ -77,6 +77,8 @@ class Factor {
              bool allow_fast = true);
   void stages(int64_t i0, int64_t bw, Counters& c, bool defer_trailing = false);
   void trailing(int64_t i0, int64_t bw, int max_ctas, const Status* pred);
+  void stream_out(int64_t upto, bool final);
+  int64_t host_done_ = 0;   // columns whose host copies are enqueued
   int overlap_split(int64_t i0, int64_t bw) const;
   void update(int64_t i0_new, int64_t bw, bool spec, Counters& c);
   bool slow_block(int64_t& i0, bool resampled, int64_t& rank, bool resume_panel = false);
@@ -243,6 +245,29 @@ int Factor::overlap_split(int64_t i0, int64_t bw) const {
   return std::max(16, std::min(P, sms - 16));
 }
 
+// D2H of the committed columns [host_done_, upto) of Y and R into the caller's
+// pinned buffers on the copy stream (ordered after everything enqueued on the
+// compute stream so far); `final` also takes R's columns past k.
+void Factor::stream_out(int64_t upto, bool final) {
+  if (p_.host_Y == nullptr && p_.host_R == nullptr) return;
+  const int64_t c1 = final ? n_ : std::min(upto, n_);
+  if (c1 <= host_done_) return;
+  cudaStream_t cs = h_.copy_stream();
+  RQ_CUDA(cudaEventRecord(h_.ev_copy, s_));
+  RQ_CUDA(cudaStreamWaitEvent(cs, h_.ev_copy, 0));
+  const int64_t c0 = host_done_, y1 = std::min(c1, k_);
+  if (p_.host_Y != nullptr && y1 > c0)
+    RQ_CUDA(cudaMemcpy2DAsync(p_.host_Y + c0 * p_.ldhY, p_.ldhY * 8, p_.Y + c0 * p_.ldy,
+                              p_.ldy * 8, m_ * 8, y1 - c0, cudaMemcpyDeviceToHost, cs));
+  if (p_.host_R != nullptr) {
+    const double* R = p_.truncated ? p_.R : p_.work;
+    const int64_t ldr = p_.truncated ? p_.ldR : p_.ldw;
+    RQ_CUDA(cudaMemcpy2DAsync(p_.host_R + c0 * p_.ldhR, p_.ldhR * 8, R + c0 * ldr, ldr * 8,
+                              k_ * 8, c1 - c0, cudaMemcpyDeviceToHost, cs));
+  }
+  host_done_ = c1;
+}
+
 // sample_update after a committed block ending at i0_new (randomized.py:253-255)
 void Factor::update(int64_t i0_new, int64_t bw, bool spec, Counters& c) {
   const int64_t i0 = i0_new - bw, n2 = n_ - i0_new;
@@ -371,6 +396,7 @@ FactorResult Factor::run() {
   int64_t i0 = 0, rank = k_;
   bool stopped = false;
   while (true) {
+    stream_out(pend.empty() ? i0 : pend.front().i0, false);   // committed columns
     if (!pend.empty() && (stopped || i0 >= k_ || (int)pend.size() >= kLookahead)) {
       Pending e = pend.front();
       RQ_CUDA(cudaEventSynchronize(ev_[e.slot]));
@@ -461,6 +487,9 @@ FactorResult Factor::run() {
     i0 += want;
   }
   const Status fin = read_status();
+  stream_out(n_, true);
+  if (p_.host_Y != nullptr || p_.host_R != nullptr)
+    RQ_CUDA(cudaStreamSynchronize(h_.copy_stream()));
   FactorResult r;
   r.rank = rank;
   r.nswaps = fin.nswaps;

@@ -32,6 +32,8 @@ struct FactorParams {
   void* omega_user = nullptr;
   int speculate = 1;                         // 0: synchronise every block (debug)
   cudaStream_t stream = nullptr;
+  double* host_Y = nullptr; int64_t ldhY = 0;   // optional pinned outputs streamed as blocks commit
+  double* host_R = nullptr; int64_t ldhR = 0;
 };
 
 struct FactorResult {

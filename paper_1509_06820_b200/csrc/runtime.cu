@@ -90,7 +90,19 @@ cudaStream_t Handle::side_stream() {
   return side_;
 }
 
+cudaStream_t Handle::copy_stream() {
+  if (copy_ == nullptr) {
+    RQ_CUDA(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking));
+    RQ_CUDA(cudaEventCreateWithFlags(&ev_copy, cudaEventDisableTiming));
+  }
+  return copy_;
+}
+
 Handle::~Handle() {
+  if (copy_ != nullptr) {
+    cudaStreamDestroy(copy_);
+    cudaEventDestroy(ev_copy);
+  }
   if (side_ != nullptr) {
     cudaStreamDestroy(side_);
     cudaEventDestroy(ev_fork);

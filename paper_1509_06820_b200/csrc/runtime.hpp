@@ -85,6 +85,8 @@ class Handle {
   // side stream + fork/join events for the select || trailing-update overlap,
   // and the speculative driver's retire events (created once per handle)
   cudaStream_t side_stream();
+  cudaStream_t copy_stream();
+  cudaEvent_t ev_copy = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::vector<cudaEvent_t> ring_ev;
 
@@ -133,6 +135,7 @@ class Handle {
   std::vector<PendEv> pend_;
   cudaEvent_t trace_base_ = nullptr;
   cudaStream_t side_ = nullptr;
+  cudaStream_t copy_ = nullptr;
   std::vector<cudaEvent_t> free_ev_;
   cudaEvent_t take_event();
   struct Buf {

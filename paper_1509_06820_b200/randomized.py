@@ -94,12 +94,16 @@ def _prepare_omega(omega, ell, m, seed, dev):
     return om, RngState(seed, position=ell * m)
 
 
-def run_native(A, k, config, *, variant, ell, width, omega=None, speculate=True, device=None):
+def run_native(A, k, config, *, variant, ell, width, omega=None, speculate=True, device=None,
+               host_out=None):
     """Shared body of every factorization entry point: returns the raw device
-    outputs plus the library's result struct."""
+    outputs plus the library's result struct.  host_out (default: A is a host
+    array) streams Y and R into pinned host buffers while the blocks commit."""
     m, n = _shape_of(A)
     dev = require_cuda(device if device is not None else
                        (A.device if torch.is_tensor(A) and A.is_cuda else None))
+    if host_out is None:
+        host_out = not (torch.is_tensor(A) and A.is_cuda)
     work = to_device_fortran(A, dev)
     Y = fmat(m, k, dev)
     tau = torch.empty(k, dtype=torch.float64, device=dev)
@@ -112,16 +116,23 @@ def run_native(A, k, config, *, variant, ell, width, omega=None, speculate=True,
         R = fmat(k, n, dev)
     om, rng = _prepare_omega(omega, ell, m, config.seed, dev)
     src = _OmegaSource(rng)
+    hY = hR = None
+    if host_out:
+        # column-major pinned buffers (torch's caching host allocator recycles them)
+        hY = torch.empty((k, m), dtype=torch.float64, pin_memory=True).t()
+        hR = torch.empty((n, k), dtype=torch.float64, pin_memory=True).t()
     args = _abi.FactorArgs(
         m=m, n=n, k=k, block=width, ell=ell, variant=variant, speculate=1 if speculate else 0,
         work=ptr(work), ldw=ld(work), Y=ptr(Y), ldy=ld(Y), tau=ptr(tau),
         W=ptr(W), ldW=ld(W) if W is not None else 0, R=ptr(R), ldR=ld(R) if R is not None else 0,
         perm=ptr(perm), swaps=ptr(swaps), swap_cap=cap, omega0=ptr(om), omega_fn=src.fn,
-        omega_user=None, stream=stream_ptr(dev))
+        omega_user=None, stream=stream_ptr(dev),
+        host_Y=hY.data_ptr() if hY is not None else None, ldhY=m,
+        host_R=hR.data_ptr() if hR is not None else None, ldhR=k)
     res = _abi.FactorResult()
     _abi.check(lib().rq_factor(handle(dev), C.byref(args), C.byref(res)))
     return dict(work=work, Y=Y, tau=tau, perm=perm, swaps=swaps, W=W, R=R, res=res,
-                rng=rng, device=dev)
+                rng=rng, device=dev, hY=hY, hR=hR)
 
 
 def _counters(res):
@@ -169,7 +180,12 @@ def package(out, host, trailing_update=True, truncated=False):
         W = None
         trailing = out["work"][rank:, rank:] if trailing_update else None
     perm = out["perm"]
-    if host:
+    if host and out.get("hY") is not None:
+        # Y and R were streamed into pinned host buffers during the factorization
+        Y = out["hY"][:, :rank].numpy()
+        R = out["hR"][:rank, :].numpy()
+        tau, W, trailing, perm = to_host_many(tau, W, trailing, perm)
+    elif host:
         Y, tau, R, W, trailing, perm = to_host_many(Y, tau, R, W, trailing, perm)
     else:
         R = R.clone()
