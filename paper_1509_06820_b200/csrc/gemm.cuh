@@ -153,23 +153,30 @@ __global__ void __launch_bounds__(GemmCfg<TA, TB, BM, BN, BK, WM, WN, STAGES>::k
     }
     const double* as = As + (kt % STAGES) * Cfg::kTileA;
     const double* bs = Bs + (kt % STAGES) * Cfg::kTileB;
-#pragma unroll
-    for (int k4 = 0; k4 < BK; k4 += 4) {
-      double af[FM], bf[FN];
+    // fragments double-buffered in registers: step ks+1's loads are issued
+    // before step ks's DMMAs (reusing one fragment set made every load wait
+    // for the DMMA that last read its register -- ncu source view)
+    double af[2][FM], bf[2][FN];
+    auto ldfrag = [&](int buf, int k4) {
 #pragma unroll
       for (int a = 0; a < FM; ++a) {
         const int m = wm0 + a * 8 + fr, k = k4 + fk;
-        af[a] = TA ? as[m * Cfg::kLdA + k] : as[k * Cfg::kLdA + m];
+        af[buf][a] = TA ? as[m * Cfg::kLdA + k] : as[k * Cfg::kLdA + m];
       }
 #pragma unroll
       for (int b = 0; b < FN; ++b) {
         const int n = wn0 + b * 8 + fr, k = k4 + fk;
-        bf[b] = TB ? bs[k * Cfg::kLdB + n] : bs[n * Cfg::kLdB + k];
+        bf[buf][b] = TB ? bs[k * Cfg::kLdB + n] : bs[n * Cfg::kLdB + k];
       }
+    };
+    ldfrag(0, 0);
+#pragma unroll
+    for (int ks = 0; ks < BK / 4; ++ks) {
+      if (ks + 1 < BK / 4) ldfrag((ks + 1) & 1, (ks + 1) * 4);
 #pragma unroll
       for (int a = 0; a < FM; ++a)
 #pragma unroll
-        for (int b = 0; b < FN; ++b) dmma884(acc[a][b], af[a], bf[b]);
+        for (int b = 0; b < FN; ++b) dmma884(acc[a][b], af[ks & 1][a], bf[ks & 1][b]);
     }
   }
   cp_async_wait<0>();

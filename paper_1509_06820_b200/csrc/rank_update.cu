@@ -237,17 +237,21 @@ __global__ void __launch_bounds__(kRuThreads, 1) rank_update_k_kernel(RuArgs a) 
     for (int x = 0; x < 4; ++x)
 #pragma unroll
       for (int y = 0; y < 2; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+    double af[2][4], bf[2][2];   // double-buffered fragments (see gemm.cuh)
+    auto ldfrag = [&](int buf, int k4) {
 #pragma unroll
-    for (int k4 = 0; k4 < K; k4 += 4) {
-      double af[4], bf[2];
+      for (int x = 0; x < 4; ++x) af[buf][x] = as[(k4 + fk) * kLdA + x * 8];
 #pragma unroll
-      for (int x = 0; x < 4; ++x) af[x] = as[(k4 + fk) * kLdA + x * 8];
+      for (int y = 0; y < 2; ++y) bf[buf][y] = bs[y * 8 * LDB + k4 + fk];
+    };
+    ldfrag(0, 0);
 #pragma unroll
-      for (int y = 0; y < 2; ++y) bf[y] = bs[y * 8 * LDB + k4 + fk];
+    for (int ks = 0; ks < K / 4; ++ks) {
+      if (ks + 1 < K / 4) ldfrag((ks + 1) & 1, (ks + 1) * 4);
 #pragma unroll
       for (int x = 0; x < 4; ++x)
 #pragma unroll
-        for (int y = 0; y < 2; ++y) dmma884(acc[x][y], af[x], bf[y]);
+        for (int y = 0; y < 2; ++y) dmma884(acc[x][y], af[ks & 1][x], bf[ks & 1][y]);
     }
     // epilogue: C - acc (C from shared memory; separate subtraction, numpy's C - Y @ X)
     const int64_t m0 = (t % tm) * kTM, n0 = (t / tm) * kTN;
