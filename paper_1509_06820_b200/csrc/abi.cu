@@ -267,6 +267,7 @@ int rq_set_option(rq_handle_t h, const char* name, int64_t value) {
     else if (n == "select_reg") hh.select_reg = value != 0;
     else if (n == "overlap_select") hh.overlap_select = value != 0;
     else if (n == "overlap_sel_ctas") hh.overlap_sel_ctas = (int)value;
+    else if (n == "su_gemm") hh.su_gemm = value != 0;
     else if (n == "gemm_vec16") hh.gemm_vec16 = value != 0;
     else if (n == "debug_timers") {
       hh.dbg = value ? (long long*)hh.buf("dbg_timers", 64 * 8, nullptr) : nullptr;

@@ -107,6 +107,7 @@ class Handle {
   int fast_panel_spec = 1;
   // speculative RQRCP: next block's select concurrently with the trailing update
   bool overlap_select = true;
+  bool su_gemm = true;        // sample update as M = S11 R11^-1 then a rank-b GEMM
   int overlap_sel_ctas = 0;   // SMs for the overlapped select (0 = size heuristic)
   bool gemm_vec16 = true;
   long long* dbg = nullptr;  // optional device phase-timer buffer (debug)

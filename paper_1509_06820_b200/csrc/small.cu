@@ -2,6 +2,7 @@
 // swap replay (K6), Frobenius norm (K10), copies, permutation scatter and
 // the standalone T factor.
 #include "runtime.hpp"
+#include "tri.cuh"
 
 namespace rq {
 
@@ -132,6 +133,68 @@ __global__ void __launch_bounds__(128) sample_update_reg_kernel(
     out[i] = __dsub_rn(s12[i], acc);
   }
   for (int i = B; i < ell; ++i) out[i] = s12[i];
+}
+
+// Sample update as a GEMM (randomized.py:107-135): top = S12 - S11 R11^{-1}
+// R12 = S12 - M R12 with M = S11 R11^{-1} (b x b).  One CTA checks the
+// degenerate guard (|R11_jj| < eps^3/4 ||A||_F, randomized.py:117) and forms M
+// (recursive DMMA triangular inverse, tri.cuh); the rank-b update kernel then
+// applies M to R12.  The per-column back substitution it replaces was a
+// latency chain (66 us at n2 = 8128).  M is written column-major (ld b).
+template <int B>
+__global__ void __launch_bounds__(256) su_prep_kernel(const double* __restrict__ S, int64_t lds,
+                                                      const double* __restrict__ R11, int64_t ldr,
+                                                      double thresh, double* __restrict__ M,
+                                                      Status* st, int abort_on_degenerate,
+                                                      int64_t i0) {
+  if (aborted(st)) return;
+  constexpr int LD = B + 1;
+  extern __shared__ __align__(16) double su_sm[];
+  double* U = su_sm;
+  double* X = U + B * LD;
+  double* Tm = X + B * LD;
+  double* S11 = Tm + B * LD;
+  double* dinv = S11 + B * LD;
+  __shared__ int s_bad;
+  const int tid = threadIdx.x;
+  if (tid == 0) s_bad = 0;
+  __syncthreads();
+  for (int e = tid; e < B * B; e += blockDim.x) {
+    const int i = e % B, l = e / B;   // column-major reads
+    U[i * LD + l] = i <= l ? R11[i + (size_t)l * ldr] : 0.0;
+    S11[i * LD + l] = S[i + (size_t)l * lds];
+  }
+  for (int j = tid; j < B; j += blockDim.x) {
+    const double d = R11[j + (size_t)j * ldr];
+    if (fabs(d) < thresh) s_bad = 1;
+    dinv[j] = 1.0 / d;
+  }
+  __syncthreads();
+  if (s_bad) {
+    if (tid == 0) {
+      st->degenerate = 1;
+      if (abort_on_degenerate) {
+        st->abort_i0 = i0;
+        __threadfence();
+        st->abort = kAbortDegenerate;
+      }
+    }
+    return;
+  }
+  if (tid == 0) st->degenerate = 0;
+  upper_inverse<256>(U, dinv, X, Tm, B, LD);
+  __syncthreads();
+  // M = S11 X (X upper): one 8x8 tile per warp iteration
+  const int warp = tid >> 5, lane = tid & 31, fr = lane >> 2, fk = lane & 3;
+  constexpr int nt = B / 8;
+  for (int t = warp; t < nt * nt; t += 8) {
+    const int ti = t / nt, tj = t % nt;
+    double acc[2] = {0.0, 0.0};
+    tile_mm(S11 + ti * 8 * LD, X + tj * 8, 8 * (tj + 1), LD, acc);
+    const int r = ti * 8 + fr, c = tj * 8 + 2 * fk;
+    M[r + (size_t)c * B] = acc[0];
+    M[r + (size_t)(c + 1) * B] = acc[1];
+  }
 }
 
 // One-launch replay of the select swaps (randomized.py:138-147): the net
@@ -352,6 +415,34 @@ void sample_update(Handle& h, int64_t ell, int64_t b, int64_t n2, const double* 
                    const double* R11, const double* R12, int64_t ldr, double frob,
                    double* Bnew, int64_t ldb, Status* st, bool abort_on_degenerate, int64_t i0,
                    cudaStream_t s) {
+  if (h.su_gemm && (b == 16 || b == 32 || b == 64)) {
+    ProfScope prof(h, kProfSampleUpd, 3.0 * b * b * n2, 8.0 * (2 * ell * n2 + b * b), s);
+    double* M = (double*)h.buf("su_M", (size_t)b * b * 8, s);
+    const double th = kEps34 * frob;
+    const int ab = abort_on_degenerate ? 1 : 0;
+    const size_t psm = ((size_t)4 * b * (b + 1) + b) * 8;
+    static bool pattr = false;
+    if (!pattr) {
+      RQ_CUDA(cudaFuncSetAttribute(su_prep_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(((size_t)4 * 64 * 65 + 64) * 8)));
+      pattr = true;
+    }
+    if (b == 16) su_prep_kernel<16><<<1, 256, psm, s>>>(S, lds, R11, ldr, th, M, st, ab, i0);
+    else if (b == 32) su_prep_kernel<32><<<1, 256, psm, s>>>(S, lds, R11, ldr, th, M, st, ab, i0);
+    else su_prep_kernel<64><<<1, 256, psm, s>>>(S, lds, R11, ldr, th, M, st, ab, i0);
+    RQ_CHECK_LAUNCH();
+    count_launch();
+    if (n2 > 0) {
+      // B_new = S[:, b:] with its top b rows then reduced by M R12; the
+      // degenerate verdict (non-speculative caller) leaves B_new unused
+      const Status* pred = abort_on_degenerate ? st : nullptr;
+      copy2d(S + (size_t)b * lds, lds, Bnew, ldb, ell, n2, s, pred);
+      if (!rank_update(h, b, n2, b, M, b, R12, ldr, Bnew, ldb, s, pred, kProfSampleUpd))
+        gemm(h, false, false, b, n2, b, -1.0, M, b, R12, ldr, 1.0, Bnew, ldb, s, pred,
+             kProfSampleUpd);
+    }
+    return;
+  }
   if (b == 16 || b == 32 || b == 64) {
     const int blocks = (int)std::max<int64_t>(1, (n2 + 127) / 128);
     ProfScope prof(h, kProfSampleUpd, 3.0 * b * b * n2, 8.0 * (2 * ell * n2 + b * b), s);

@@ -69,4 +69,23 @@ for a, b in sel[:200]:
     best = max(((min(b, d) - max(a, c)), c, d) for c, d in upd) if upd else (0, 0, 0)
     pairs.append((round(a, 3), round(b - a, 3), round(best[0], 3), round(best[2] - best[1], 3)))
 print(json.dumps({"first_selects(start,dur,overlap,upd_dur)": pairs[:12]}))
+# exposed time per family: intervals where it is the only family running
+ev = []
+for a, b, nm in recs:
+    ev.append((a, 1, nm)); ev.append((b, -1, nm))
+ev.sort()
+active = {}
+exposed = defaultdict(float)
+idle = 0.0
+last = ev[0][0]
+for t, d, nm in ev:
+    run = [k for k, v in active.items() if v > 0]
+    if len(run) == 1:
+        exposed[run[0]] += t - last
+    elif not run:
+        idle += t - last
+    last = t
+    active[nm] = active.get(nm, 0) + d
+print(json.dumps({"exposed_ms": {k: round(v, 2) for k, v in sorted(exposed.items(), key=lambda x: -x[1])},
+                  "idle_ms": round(idle, 2)}))
 _abi.check(lib.rq_set_option(h, b"profile_trace", 0))
