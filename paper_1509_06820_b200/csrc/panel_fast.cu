@@ -149,6 +149,36 @@ RQ_DEV void store_gram(double* dst, int n8, const double (&acc)[5][2]) {
   }
 }
 
+// element / row of a 4-wide register array for a warp-uniform index, as a
+// uniform branch (compare-select chains cost ~40% of the LU's issue slots)
+RQ_DEV double pick4(const double (&v)[4], int i) {
+  switch (i) {
+    case 1: return v[1];
+    case 2: return v[2];
+    case 3: return v[3];
+    default: return v[0];
+  }
+}
+RQ_DEV void pick_row4(const double (&m)[4][4], int c, double (&out)[4]) {
+  switch (c) {
+    case 1:
+#pragma unroll
+      for (int b = 0; b < 4; ++b) out[b] = m[1][b];
+      break;
+    case 2:
+#pragma unroll
+      for (int b = 0; b < 4; ++b) out[b] = m[2][b];
+      break;
+    case 3:
+#pragma unroll
+      for (int b = 0; b < 4; ++b) out[b] = m[3][b];
+      break;
+    default:
+#pragma unroll
+      for (int b = 0; b < 4; ++b) out[b] = m[0][b];
+  }
+}
+
 __global__ void __launch_bounds__(kFT, 1) panel_fast_kernel(FastArgs a) {
   if (aborted(a.st)) {  // set only by earlier launches: uniform over the grid
     if (blockIdx.x == 0 && threadIdx.x == 0) a.bar[4] = 1;   // nothing downstream runs either
@@ -275,32 +305,19 @@ __global__ void __launch_bounds__(kFT, 1) panel_fast_kernel(FastArgs a) {
       if ((ty >> 1) == (tj >> 1)) {
         const bool h1 = (ty & 1) != 0;       // lanes 16..31: row j+1
         double gj[4];
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          gj[b] = g[0][b];
-#pragma unroll
-          for (int c = 1; c < 4; ++c) if (c == cj) gj[b] = g[c][b];
-        }
-        double dsel = gj[0];
-#pragma unroll
-        for (int b = 1; b < 4; ++b) if (b == cj) dsel = gj[b];
-        const double d0 = __shfl_sync(0xffffffffu, dsel, tj);          // G[j][j]
+        pick_row4(g, cj, gj);
+        const double d0 = __shfl_sync(0xffffffffu, pick4(gj, cj), tj);  // G[j][j]
         const double rinv0 = rsqrt(d0);
         double r0v[4];
 #pragma unroll
         for (int b = 0; b < 4; ++b) r0v[b] = __shfl_xor_sync(0xffffffffu, gj[b] * rinv0, 16);
         // row j+1 after pivot j: g - R[j][j+1] R[j][l]
-        double rj1 = 0.0;
-#pragma unroll
-        for (int b = 0; b < 4; ++b) if (b == cj) rj1 = h1 ? r0v[b] : gj[b] * rinv0;
+        const double rj1 = h1 ? pick4(r0v, cj) : pick4(gj, cj) * rinv0;
         const double r01 = __shfl_sync(0xffffffffu, rj1, tj + 1);       // R[j][j+1]
         double g1[4];
 #pragma unroll
         for (int b = 0; b < 4; ++b) g1[b] = __fma_rn(-r01, r0v[b], gj[b]);
-        double d1sel = g1[0];
-#pragma unroll
-        for (int b = 1; b < 4; ++b) if (b == cj) d1sel = g1[b];
-        const double d1 = two ? __shfl_sync(0xffffffffu, d1sel, 16 + tj + 1) : 1.0;
+        const double d1 = two ? __shfl_sync(0xffffffffu, pick4(g1, cj), 16 + tj + 1) : 1.0;
         const double rinv1 = rsqrt(d1);
         if (!(d0 > 0.0) || !(d1 > 0.0)) {
           if (lane_of(tid) == 0) s_fail = 1;
@@ -320,15 +337,17 @@ __global__ void __launch_bounds__(kFT, 1) panel_fast_kernel(FastArgs a) {
       }
       __syncthreads();
       if (s_fail) break;
+      // unguarded: rows/columns <= j+1 are dead once published, R1 is zero
+      // below the diagonal and in the padding, so only live entries change
       double ri0[4], rl0[4], ri1[4], rl1[4];
+      const int j1 = two ? j + 1 : j;   // row j+1 of R1 is zero when absent
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
         const int i = ty + 16 * b, l = tx + 16 * b;
-        const bool iok = i > j + 1 && i < n, lok = l > j + 1 && l < n;
-        ri0[b] = iok ? R1[j * ld + i] : 0.0;
-        rl0[b] = lok ? R1[j * ld + l] : 0.0;
-        ri1[b] = iok && two ? R1[(j + 1) * ld + i] : 0.0;
-        rl1[b] = lok && two ? R1[(j + 1) * ld + l] : 0.0;
+        ri0[b] = R1[j * ld + i];
+        rl0[b] = R1[j * ld + l];
+        ri1[b] = two ? R1[j1 * ld + i] : 0.0;
+        rl1[b] = two ? R1[j1 * ld + l] : 0.0;
       }
 #pragma unroll
       for (int c = 0; c < 4; ++c)
@@ -452,13 +471,12 @@ __global__ void __launch_bounds__(kFT, 1) panel_fast_kernel(FastArgs a) {
     for (int j = 0; j < n; ++j) {
       const int cj = j >> 4, tj = j & 15;
       if (ty == tj) {
+        double zj[4];
+        pick_row4(z, cj, zj);
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-          double zj = z[0][b];
-#pragma unroll
-          for (int c = 1; c < 4; ++c) if (c == cj) zj = z[c][b];
           const int l = tx + 16 * b;
-          if (l >= j && l < n) Q1[j * ld + l] = zj;
+          if (l >= j && l < n) Q1[j * ld + l] = zj[b];
         }
       }
       __syncthreads();
@@ -469,22 +487,17 @@ __global__ void __launch_bounds__(kFT, 1) panel_fast_kernel(FastArgs a) {
         s_sign[j] = sj;
         s_c[j] = piv;
       }
+      // unguarded: rows/columns <= j are dead (U rows live in Q1, L in T5),
+      // padding rows/columns are exactly zero
       double li[4], zl[4];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        double zc = z[c][0];
-#pragma unroll
-        for (int b = 1; b < 4; ++b) if (b == cj) zc = z[c][b];
         const int i = ty + 16 * c;
-        const double v = __shfl_sync(0xffffffffu, zc, tj, 16) * linv;
-        li[c] = (i > j && i < n) ? v : 0.0;
-        if (tx == tj && i > j && i < n) T5[i * ld + j] = v;
+        li[c] = __shfl_sync(0xffffffffu, pick4(z[c], cj), tj, 16) * linv;
+        if (tx == tj && i > j && i < n) T5[i * ld + j] = li[c];
       }
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int l = tx + 16 * b;
-        zl[b] = (l > j && l < n) ? Q1[j * ld + l] : 0.0;
-      }
+      for (int b = 0; b < 4; ++b) zl[b] = Q1[j * ld + tx + 16 * b];
 #pragma unroll
       for (int c = 0; c < 4; ++c)
 #pragma unroll
