@@ -75,7 +75,9 @@ class Factor {
   void swaps(int64_t i0, int64_t got);
   void panel(int64_t i0, int64_t got, PanelPolicy pol, bool spec, Counters& c,
              bool allow_fast = true);
-  void stages(int64_t i0, int64_t bw, Counters& c, bool defer_trailing = false);
+  void stages(int64_t i0, int64_t bw, Counters& c, bool defer_trailing = false,
+              bool g_ready = false);
+  bool panel_overlap_inner(int64_t i0, int64_t bw);
   void trailing(int64_t i0, int64_t bw, int max_ctas, const Status* pred);
   void stream_out(int64_t upto, bool final);
   int64_t host_done_ = 0;   // columns whose host copies are enqueued
@@ -171,14 +173,15 @@ void Factor::panel(int64_t i0, int64_t got, PanelPolicy pol, bool spec, Counters
 }
 
 // _block_stages (randomized.py:158-180) / trqrcp W+R update (truncated.py:453-470)
-void Factor::stages(int64_t i0, int64_t bw, Counters& c, bool defer_trailing) {
+void Factor::stages(int64_t i0, int64_t bw, Counters& c, bool defer_trailing, bool g_ready) {
   const int64_t mm = m_ - i0, nt2 = n_ - i0 - bw;
   if (nt2 <= 0) return;
   const double* Yb = p_.Y + i0 + i0 * p_.ldy;
   if (!p_.truncated) {
     double* C = p_.work + i0 + (i0 + bw) * p_.ldw;
-    gemm(h_, true, false, bw, nt2, mm, 1.0, Yb, p_.ldy, C, p_.ldw, 0.0, G_, bw, s_, st_,
-         kProfInner);
+    if (!g_ready)   // else panel_overlap_inner() assembled G = Y^T C
+      gemm(h_, true, false, bw, nt2, mm, 1.0, Yb, p_.ldy, C, p_.ldw, 0.0, G_, bw, s_, st_,
+           kProfInner);
     gemm(h_, true, false, bw, nt2, bw, 1.0, T_, b_, G_, bw, 0.0, X_, bw, s_, st_);
     c.gemm_flops += 2 * mm * bw * nt2 + bw * bw * nt2;
     const bool trail = p_.update_trailing && i0 + bw < m_;
@@ -217,6 +220,44 @@ void Factor::stages(int64_t i0, int64_t bw, Counters& c, bool defer_trailing) {
 
 // C[b:] -= Y[b:] X of the block at i0 (the rows stages() deferred), on at
 // most max_ctas SMs (the rest run the next block's select meanwhile)
+// Speculative RQRCP with the fast panel: its Y_below = P_below M, so the
+// inner product G = Y^T C splits into Y_top^T C_top + M^T (P_below^T C_below).
+// The big term H = P_below^T C_below needs only the panel's INPUT columns, so
+// it runs on the side stream while the fast panel (capped CTAs) factors them;
+// afterwards G is assembled with two b x b x nt2 products and the panel rows
+// below the diagonal (left unzeroed for H) are cleared.  A decline aborts the
+// block as usual (nothing was written).  Returns false (nothing launched)
+// when the shape does not qualify.
+bool Factor::panel_overlap_inner(int64_t i0, int64_t bw) {
+  const int64_t mm = m_ - i0, nt2 = n_ - i0 - bw;
+  if (p_.truncated || nt2 <= 0 || mm <= bw || !panel_fast_eligible(h_, mm, bw)) return false;
+  PanelOut o{};
+  o.Y = p_.Y + i0 + i0 * p_.ldy; o.ldy = p_.ldy;
+  o.tau = p_.tau + i0;
+  o.T = T_; o.ldt = b_;
+  o.Rdst = p_.work + i0 + i0 * p_.ldw; o.ldr = p_.ldw; o.rrows = mm;
+  double* H = (double*)h_.buf("inner_H", (size_t)b_ * n_ * 8, s_);
+  cudaStream_t s2 = h_.side_stream();
+  RQ_CUDA(cudaEventRecord(h_.ev_fork, s_));
+  RQ_CUDA(cudaStreamWaitEvent(s2, h_.ev_fork, 0));
+  const double* Mrm = nullptr;
+  int64_t ldm = 0;
+  panel_fast(h_, mm, bw, o.Rdst, p_.ldw, o, tol_, st_, s_, true, i0, h_.overlap_panel_ctas, true,
+             &Mrm, &ldm);
+  const double* Pb = p_.work + i0 + bw + i0 * p_.ldw;
+  const double* Cb = p_.work + i0 + bw + (i0 + bw) * p_.ldw;
+  gemm(h_, true, false, bw, nt2, mm - bw, 1.0, Pb, p_.ldw, Cb, p_.ldw, 0.0, H, bw, s2, st_,
+       kProfInner);
+  RQ_CUDA(cudaEventRecord(h_.ev_join, s2));
+  RQ_CUDA(cudaStreamWaitEvent(s_, h_.ev_join, 0));
+  // G = Y_top^T C_top + M^T H   (M^T is Mrm read column-major with ld ldm)
+  gemm(h_, true, false, bw, nt2, bw, 1.0, o.Y, p_.ldy, p_.work + i0 + (i0 + bw) * p_.ldw, p_.ldw,
+       0.0, G_, bw, s_, st_, kProfInner);
+  gemm(h_, false, false, bw, nt2, bw, 1.0, Mrm, ldm, H, bw, 1.0, G_, bw, s_, st_, kProfInner);
+  fill2d(p_.work + i0 + bw + i0 * p_.ldw, p_.ldw, mm - bw, bw, 0.0, s_, st_);
+  return true;
+}
+
 // `pred` is the Status predicate: a snapshot of the abort word taken before
 // the block's sample update, so a degenerate verdict (which keeps this block
 // committed, randomized.py:253-258) cannot skip the rows it still owes.
@@ -458,13 +499,15 @@ FactorResult Factor::run() {
     if (!next_selected) select(i0, want, true);   // else launched during the previous block
     next_selected = false;
     swaps(i0, want);
-    panel(i0, want, kPanelCommitIfFull, true, e.stage);
+    const bool g_ready = overlap && h_.overlap_inner && fast_aborts_ &&
+                         panel_overlap_inner(i0, want);
+    if (!g_ready) panel(i0, want, kPanelCommitIfFull, true, e.stage);
     e.has_update = i0 + want < k_;
     // RQRCP: the next block's select only needs the sample update (R11, R12),
     // so it runs on a side stream on a share of the SMs while the trailing
     // rows of this block's update run on the rest (join before its swaps)
     const bool ovl = overlap && e.has_update && m_ - i0 > want;
-    stages(i0, want, e.stage, ovl);
+    stages(i0, want, e.stage, ovl, g_ready);
     if (ovl) RQ_CUDA(cudaMemcpyAsync(&pre_->abort, &st_->abort, sizeof(int),
                                      cudaMemcpyDeviceToDevice, s_));
     if (e.has_update) update(i0 + want, want, true, e.update);

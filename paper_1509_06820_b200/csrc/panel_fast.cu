@@ -54,6 +54,7 @@ struct FastArgs {
   double* T; int64_t ldt;           // optional T factor (nullptr: not wanted)
   double tol, guard;                // < 0: no threshold
   int abort_on_decline;             // speculative driver: decline -> Status.abort (kAbortPanelFast)
+  int defer_zero;                   // leave the panel rows below the diagonal to the caller
   int64_t i0;
   int64_t nchunks;
   Status* st;
@@ -600,7 +601,7 @@ __global__ void __launch_bounds__(kFT, 1) panel_fast_kernel(FastArgs a) {
       const int64_t gr = g0 + r;
       if (gr < n || gr >= a.mm) continue;
       a.Y[gr + (int64_t)c * a.ldy] = W1[r * ld + c];
-      if (gr < a.rrows) a.Rdst[gr + (int64_t)c * a.ldr] = 0.0;
+      if (gr < a.rrows && !a.defer_zero) a.Rdst[gr + (int64_t)c * a.ldr] = 0.0;
     }
   }
   mark(6);
@@ -609,16 +610,23 @@ __global__ void __launch_bounds__(kFT, 1) panel_fast_kernel(FastArgs a) {
 
 }  // namespace
 
+bool panel_fast_eligible(const Handle& h, int64_t mm, int64_t bw) {
+  if (!h.fast_panel || bw < 2 || bw > kFMaxBw || mm < 2 * bw) return false;
+  const int n8 = (int)((bw + 7) / 8 * 8);
+  return !(kFT / n8 > 32 || 32 % (kFT / n8) != 0);   // n8 in {8, 16, 32, 64}
+}
+
 const int* panel_fast(Handle& h, int64_t mm, int64_t bw, const double* P, int64_t ldp,
                       const PanelOut& out, double tol, Status* st, cudaStream_t s,
-                      bool abort_on_decline, int64_t i0) {
-  if (!h.fast_panel || bw < 2 || bw > kFMaxBw || mm < 2 * bw) return nullptr;
+                      bool abort_on_decline, int64_t i0, int max_ctas, bool defer_zero,
+                      const double** m_rowmajor, int64_t* m_ld) {
+  if (!panel_fast_eligible(h, mm, bw)) return nullptr;
   const int n8 = (int)((bw + 7) / 8 * 8);
-  if (kFT / n8 > 32 || 32 % (kFT / n8) != 0) return nullptr;  // n8 in {8, 16, 32, 64}
   const int ld = n8 + 1;
   const int64_t nchunks = (mm + kFRows - 1) / kFRows;
   int Q = (int)std::min<int64_t>(h.num_sms, nchunks);
   if (h.fast_panel_max_ctas > 0) Q = std::min(Q, h.fast_panel_max_ctas);
+  if (max_ctas > 0) Q = std::min(Q, max_ctas);
   const size_t smem = (size_t)6 * kFRows * ld * 8;
   const int nn = n8 * n8;
   FastArgs a{};
@@ -632,6 +640,7 @@ const int* panel_fast(Handle& h, int64_t mm, int64_t bw, const double* P, int64_
   a.nchunks = nchunks;
   a.st = st;
   a.abort_on_decline = abort_on_decline ? 1 : 0;
+  a.defer_zero = defer_zero ? 1 : 0;
   a.i0 = i0;
   a.bar = (unsigned int*)h.buf("pf_bar", 64, s);
   static void* zeroed = nullptr;
@@ -641,6 +650,10 @@ const int* panel_fast(Handle& h, int64_t mm, int64_t bw, const double* P, int64_
   }
   a.gpart = (double*)h.buf("pf_part", (size_t)Q * nn * 8, s);
   a.gmat = (double*)h.buf("pf_mat", (size_t)4 * nn * 8, s);
+  // on commit, M = R1^{-1} (I - F) S U^{-1} (Y_below = P_below M) is left
+  // row-major in gmat[3]: as a column-major matrix with ld n8 it is M^T
+  if (m_rowmajor != nullptr) *m_rowmajor = a.gmat + 3 * nn;
+  if (m_ld != nullptr) *m_ld = n8;
   a.dbg = h.dbg;
   static size_t attr = 0;
   if (smem > attr) {

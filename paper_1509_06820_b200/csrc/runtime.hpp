@@ -108,6 +108,9 @@ class Handle {
   // speculative RQRCP: next block's select concurrently with the trailing update
   bool overlap_select = true;
   bool su_gemm = true;        // sample update as M = S11 R11^-1 then a rank-b GEMM
+  // inner GEMM's P_below^T C_below part concurrently with the fast panel
+  bool overlap_inner = true;
+  int overlap_panel_ctas = 48;  // SMs for the fast panel while it overlaps
   int overlap_sel_ctas = 0;   // SMs for the overlapped select (0 = size heuristic)
   bool gemm_vec16 = true;
   long long* dbg = nullptr;  // optional device phase-timer buffer (debug)
@@ -195,9 +198,15 @@ void panel_qr(Handle& h, int64_t mm, int64_t bw, const double* P, int64_t ldp,
 // exact kernel must run), or nullptr when the panel shape is not eligible.
 // abort_on_decline (speculative driver): a declined panel sets Status.abort =
 // kAbortPanelFast at block i0 instead of leaving the work to the exact kernel.
+bool panel_fast_eligible(const Handle& h, int64_t mm, int64_t bw);
+// max_ctas caps the grid (0: one CTA per SM); defer_zero leaves the panel rows
+// below the diagonal unzeroed (the caller zeroes them later); m_rowmajor / m_ld
+// receive the committed M (Y_below = P_below M) as a row-major ld x ld block.
 const int* panel_fast(Handle& h, int64_t mm, int64_t bw, const double* P, int64_t ldp,
                       const PanelOut& out, double tol, Status* st, cudaStream_t s,
-                      bool abort_on_decline = false, int64_t i0 = 0);
+                      bool abort_on_decline = false, int64_t i0 = 0, int max_ctas = 0,
+                      bool defer_zero = false, const double** m_rowmajor = nullptr,
+                      int64_t* m_ld = nullptr);
 
 // B_new = [S12 - S11 R11^{-1} R12; S22] (randomized.py:107-135).  Writes
 // Status.degenerate; with abort_on_degenerate also sets Status.abort.
@@ -223,7 +232,8 @@ void frob_norm(Handle& h, const double* A, int64_t m, int64_t n, int64_t lda, do
                cudaStream_t s);
 void copy2d(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows,
             int64_t cols, cudaStream_t s, const Status* st = nullptr);
-void fill2d(double* dst, int64_t ldd, int64_t rows, int64_t cols, double v, cudaStream_t s);
+void fill2d(double* dst, int64_t ldd, int64_t rows, int64_t cols, double v, cudaStream_t s,
+            const Status* st = nullptr);
 void transpose(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows,
                int64_t cols, cudaStream_t s);
 void scatter_cols(const double* src, int64_t lds, const int64_t* perm, double* dst,

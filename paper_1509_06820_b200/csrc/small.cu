@@ -335,7 +335,9 @@ __global__ void copy2d_kernel(const double* src, int64_t lds, double* dst, int64
     dst[r + c * ldd] = src[r + c * lds];
   }
 }
-__global__ void fill2d_kernel(double* dst, int64_t ldd, int64_t rows, int64_t cols, double v) {
+__global__ void fill2d_kernel(double* dst, int64_t ldd, int64_t rows, int64_t cols, double v,
+                              const Status* st) {
+  if (aborted(st)) return;
   const int64_t total = rows * cols;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x)
@@ -524,9 +526,10 @@ void copy2d(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t ro
   count_launch();
 }
 
-void fill2d(double* dst, int64_t ldd, int64_t rows, int64_t cols, double v, cudaStream_t s) {
+void fill2d(double* dst, int64_t ldd, int64_t rows, int64_t cols, double v, cudaStream_t s,
+            const Status* st) {
   if (rows <= 0 || cols <= 0) return;
-  fill2d_kernel<<<grid_for(rows * cols, 148), 256, 0, s>>>(dst, ldd, rows, cols, v);
+  fill2d_kernel<<<grid_for(rows * cols, 148), 256, 0, s>>>(dst, ldd, rows, cols, v, st);
   RQ_CHECK_LAUNCH();
   count_launch();
 }
