@@ -78,6 +78,7 @@ class Factor {
   void stages(int64_t i0, int64_t bw, Counters& c, bool defer_trailing = false,
               bool g_ready = false);
   bool panel_overlap_inner(int64_t i0, int64_t bw);
+  bool msu_ready_ = false;   // the fast panel left the sample update's M in "su_Mpre"
   void trailing(int64_t i0, int64_t bw, int max_ctas, const Status* pred);
   void stream_out(int64_t upto, bool final);
   int64_t host_done_ = 0;   // columns whose host copies are enqueued
@@ -242,8 +243,10 @@ bool Factor::panel_overlap_inner(int64_t i0, int64_t bw) {
   RQ_CUDA(cudaStreamWaitEvent(s2, h_.ev_fork, 0));
   const double* Mrm = nullptr;
   int64_t ldm = 0;
+  double* msu = (double*)h_.buf("su_Mpre", (size_t)b_ * b_ * 8, s_);
   panel_fast(h_, mm, bw, o.Rdst, p_.ldw, o, tol_, st_, s_, true, i0, h_.overlap_panel_ctas, true,
-             &Mrm, &ldm);
+             &Mrm, &ldm, S_, ell_, msu);
+  msu_ready_ = true;
   const double* Pb = p_.work + i0 + bw + i0 * p_.ldw;
   const double* Cb = p_.work + i0 + bw + (i0 + bw) * p_.ldw;
   gemm(h_, true, false, bw, nt2, mm - bw, 1.0, Pb, p_.ldw, Cb, p_.ldw, 0.0, H, bw, s2, st_,
@@ -319,7 +322,13 @@ void Factor::update(int64_t i0_new, int64_t bw, bool spec, Counters& c) {
   } else {
     R11 = p_.R + i0 + i0 * p_.ldR; R12 = p_.R + i0 + i0_new * p_.ldR; ldr = p_.ldR;
   }
-  sample_update(h_, ell_, bw, n2, S_, ell_, R11, R12, ldr, frob_, B_, ell_, st_, spec, i0, s_);
+  if (msu_ready_ && spec) {
+    sample_update_pre(h_, ell_, bw, n2, S_, ell_, (const double*)h_.buf("su_Mpre", 8, s_), R12,
+                      ldr, B_, ell_, st_, s_);
+  } else {
+    sample_update(h_, ell_, bw, n2, S_, ell_, R11, R12, ldr, frob_, B_, ell_, st_, spec, i0, s_);
+  }
+  msu_ready_ = false;
   c.gemm_flops += 3 * bw * bw * n2;
   touch(c, 2 * bw * bw + 3 * bw * n2);
 }
@@ -462,6 +471,7 @@ FactorResult Factor::run() {
         pend.clear();
         if (overlap) RQ_CUDA(cudaStreamSynchronize(h_.side_stream()));
         next_selected = false;
+        msu_ready_ = false;
         RQ_CUDA(cudaMemsetAsync(&st_->abort, 0, sizeof(int), s_));
         if (code == kAbortDegenerate) {
           i0 = X + bwX;
@@ -499,6 +509,7 @@ FactorResult Factor::run() {
     if (!next_selected) select(i0, want, true);   // else launched during the previous block
     next_selected = false;
     swaps(i0, want);
+    msu_ready_ = false;
     const bool g_ready = overlap && h_.overlap_inner && fast_aborts_ &&
                          panel_overlap_inner(i0, want);
     if (!g_ready) panel(i0, want, kPanelCommitIfFull, true, e.stage);

@@ -55,6 +55,8 @@ struct FastArgs {
   double tol, guard;                // < 0: no threshold
   int abort_on_decline;             // speculative driver: decline -> Status.abort (kAbortPanelFast)
   int defer_zero;                   // leave the panel rows below the diagonal to the caller
+  const double* S11; int64_t lds11; // optional: sample block for the sample update's M
+  double* msu;                      // out (if S11): M = S11 R11^{-1}, b x b column-major
   int64_t i0;
   int64_t nchunks;
   Status* st;
@@ -546,6 +548,25 @@ __global__ void __launch_bounds__(kFT, 1) panel_fast_kernel(FastArgs a) {
       chunk_mm<true, true>(Ri, R1, T5, n8, n8, ld);  // M = R1^{-1} M'
       __syncthreads();
       for (int i = r0; i < n8; i += rstep) a.gmat[3 * nn + i * n8 + c0] = T5[i * ld + c0];
+      if (a.msu != nullptr) {
+        // sample update's M = S11 R11^{-1} (randomized.py:107-135): R11 = S R~,
+        // R~^{-1} = R1^{-1} (I - F) to O(|F|^2), so M = S11 R1^{-1} (I - F) S.
+        // A committed panel cleared the degenerate guard (same threshold).
+        __syncthreads();
+        for (int i = r0; i < n8; i += rstep)
+          W4[i * ld + c0] = (i < n && c0 < n) ? a.S11[i + (int64_t)c0 * a.lds11] : 0.0;
+        __syncthreads();
+        chunk_mm<false, true>(W4, Ri, W5, n8, n8, ld);   // S11 R1^{-1}
+        __syncthreads();
+        chunk_mm<false, true>(W5, F, W4, n8, n8, ld);    // (S11 R1^{-1}) F
+        __syncthreads();
+        for (int e = tid; e < n * n; e += kFT) {
+          const int l = e / n, i = e - l * n;
+          a.msu[i + (int64_t)l * n] = s_sign[l] * (W5[i * ld + l] - W4[i * ld + l]);
+        }
+        if (tid == 0) a.st->degenerate = 0;
+        __syncthreads();
+      }
       if (a.T != nullptr) {
         // compact-WY T of the reconstructed reflectors: U = -T Y1^T, so
         // T = -U Y1^{-T} (kernels.py:139-147 builds the same T by recurrence)
@@ -619,7 +640,8 @@ bool panel_fast_eligible(const Handle& h, int64_t mm, int64_t bw) {
 const int* panel_fast(Handle& h, int64_t mm, int64_t bw, const double* P, int64_t ldp,
                       const PanelOut& out, double tol, Status* st, cudaStream_t s,
                       bool abort_on_decline, int64_t i0, int max_ctas, bool defer_zero,
-                      const double** m_rowmajor, int64_t* m_ld) {
+                      const double** m_rowmajor, int64_t* m_ld, const double* S11,
+                      int64_t lds11, double* msu) {
   if (!panel_fast_eligible(h, mm, bw)) return nullptr;
   const int n8 = (int)((bw + 7) / 8 * 8);
   const int ld = n8 + 1;
@@ -641,6 +663,7 @@ const int* panel_fast(Handle& h, int64_t mm, int64_t bw, const double* P, int64_
   a.st = st;
   a.abort_on_decline = abort_on_decline ? 1 : 0;
   a.defer_zero = defer_zero ? 1 : 0;
+  a.S11 = S11; a.lds11 = lds11; a.msu = S11 != nullptr ? msu : nullptr;
   a.i0 = i0;
   a.bar = (unsigned int*)h.buf("pf_bar", 64, s);
   static void* zeroed = nullptr;

@@ -206,7 +206,14 @@ const int* panel_fast(Handle& h, int64_t mm, int64_t bw, const double* P, int64_
                       const PanelOut& out, double tol, Status* st, cudaStream_t s,
                       bool abort_on_decline = false, int64_t i0 = 0, int max_ctas = 0,
                       bool defer_zero = false, const double** m_rowmajor = nullptr,
-                      int64_t* m_ld = nullptr);
+                      int64_t* m_ld = nullptr, const double* S11 = nullptr,
+                      int64_t lds11 = 0, double* msu = nullptr);
+
+// B_new = [S12 - M R12; S22] with M = S11 R11^{-1} already formed (by the
+// fast panel of the same block, which also cleared the degenerate guard).
+void sample_update_pre(Handle& h, int64_t ell, int64_t b, int64_t n2, const double* S,
+                       int64_t lds, const double* M, const double* R12, int64_t ldr,
+                       double* Bnew, int64_t ldb, Status* st, cudaStream_t s);
 
 // B_new = [S12 - S11 R11^{-1} R12; S22] (randomized.py:107-135).  Writes
 // Status.degenerate; with abort_on_degenerate also sets Status.abort.

@@ -413,6 +413,16 @@ int grid_for(int64_t total, int num_sms) {
 
 }  // namespace
 
+void sample_update_pre(Handle& h, int64_t ell, int64_t b, int64_t n2, const double* S,
+                       int64_t lds, const double* M, const double* R12, int64_t ldr,
+                       double* Bnew, int64_t ldb, Status* st, cudaStream_t s) {
+  if (n2 <= 0) return;
+  ProfScope prof(h, kProfSampleUpd, 3.0 * b * b * n2, 8.0 * (2 * ell * n2 + b * b), s);
+  copy2d(S + (size_t)b * lds, lds, Bnew, ldb, ell, n2, s, st);
+  if (!rank_update(h, b, n2, b, M, b, R12, ldr, Bnew, ldb, s, st, kProfSampleUpd))
+    gemm(h, false, false, b, n2, b, -1.0, M, b, R12, ldr, 1.0, Bnew, ldb, s, st, kProfSampleUpd);
+}
+
 void sample_update(Handle& h, int64_t ell, int64_t b, int64_t n2, const double* S, int64_t lds,
                    const double* R11, const double* R12, int64_t ldr, double frob,
                    double* Bnew, int64_t ldb, Status* st, bool abort_on_degenerate, int64_t i0,
