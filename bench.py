@@ -263,6 +263,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--force-sharded", action="store_true",
+                    help="run the column-block-cyclic driver even at N = 1 (tests the N > 1 path)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -280,7 +282,7 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if world > 1 or args.force_sharded:
         dist.init_process_group("nccl", device_id=dev)
 
     def barrier():
@@ -294,7 +296,7 @@ def main():
     lib = _abi.load_library()
     h = _abi.handle(local)
 
-    sharded = world > 1
+    sharded = world > 1 or args.force_sharded
     if sharded:
         # column-block-cyclic shards of ONE matrix over the ranks (strong scaling)
         from paper_1509_06820_b200.parallel import BlockCyclic, rqrcp_sharded
@@ -449,7 +451,7 @@ def main():
             "fp64_peak": peak,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 

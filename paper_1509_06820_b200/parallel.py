@@ -52,9 +52,13 @@ class BlockCyclic:
         return (blk // self.world) * self.b + j % self.b
 
     def positions(self, rank: int) -> np.ndarray:
-        """Global positions held by `rank`, in local order."""
-        j = np.arange(self.n)
-        return j[(j // self.b) % self.world == rank]
+        """Global positions held by `rank`, in local order (cached)."""
+        cache = self.__dict__.setdefault("_pos_cache", {})
+        p = cache.get(rank)
+        if p is None:
+            j = np.arange(self.n)
+            p = cache[rank] = j[(j // self.b) % self.world == rank]
+        return p
 
     def n_local(self, rank: int) -> int:
         return int(self.positions(rank).size)
@@ -92,45 +96,55 @@ def exchange_columns(local: torch.Tensor, layout: BlockCyclic, moves, rank: int,
                      group=None) -> None:
     """Apply a column permutation (dst <- src moves over global positions) to
     the distributed matrix in place.  Columns whose source and destination
-    ranks differ are packed per peer and moved with one send/recv pair each."""
+    ranks differ are packed per peer and moved with one send/recv pair each.
+    Columns are gathered / scattered with one index kernel per batch on the
+    transposed (row-contiguous) view of the column-major local block."""
     if not moves:
         return
     world = layout.world
     li = layout.local_index
     owner = layout.owner
+    rows = local.t()                       # (n_local x m), each row = one local column
+    dev = local.device
     # snapshot every source column this rank owns before anything is overwritten
     mine_src = sorted({s for _, s in moves if owner(s) == rank})
-    snap = {s: local[:, li(s)].clone() for s in mine_src}
+    slot = {s: k for k, s in enumerate(mine_src)}
+    snap = rows.index_select(0, torch.as_tensor([li(s) for s in mine_src], device=dev)) \
+        if mine_src else None
+    loc_dst, loc_src = [], []
     out_by_peer: dict[int, list[int]] = {}
-    in_by_peer: dict[int, list[tuple[int, int]]] = {}
+    in_by_peer: dict[int, list[int]] = {}
     for d, s in moves:
         od, os_ = owner(d), owner(s)
         if od == rank and os_ == rank:
-            local[:, li(d)] = snap[s]
+            loc_dst.append(li(d))
+            loc_src.append(slot[s])
         elif os_ == rank:
-            out_by_peer.setdefault(od, []).append(s)
+            out_by_peer.setdefault(od, []).append(slot[s])
         elif od == rank:
-            in_by_peer.setdefault(os_, []).append((d, s))
-    ops = []
-    sendbufs, recvbufs = [], []
+            in_by_peer.setdefault(os_, []).append(li(d))
+    if loc_dst:
+        rows.index_copy_(0, torch.as_tensor(loc_dst, device=dev),
+                         snap.index_select(0, torch.as_tensor(loc_src, device=dev)))
+    ops, recvbufs = [], []
     for peer in range(world):
         if peer == rank:
             continue
         if peer in out_by_peer:
-            buf = torch.stack([snap[s] for s in out_by_peer[peer]], dim=1).contiguous()
-            sendbufs.append(buf)
+            buf = snap.index_select(0, torch.as_tensor(out_by_peer[peer], device=dev))
             ops.append(dist.P2POp(dist.isend, buf, _grank(peer, group), group=group))
+            recvbufs.append((None, buf))   # keep alive until the wait
         if peer in in_by_peer:
-            buf = torch.empty((local.shape[0], len(in_by_peer[peer])), dtype=local.dtype,
-                              device=local.device)
+            buf = torch.empty((len(in_by_peer[peer]), local.shape[0]), dtype=local.dtype,
+                              device=dev)
             recvbufs.append((peer, buf))
             ops.append(dist.P2POp(dist.irecv, buf, _grank(peer, group), group=group))
     if ops:
         for r in dist.batch_isend_irecv(ops):
             r.wait()
     for peer, buf in recvbufs:
-        for col, (d, _s) in enumerate(in_by_peer[peer]):
-            local[:, li(d)] = buf[:, col]
+        if peer is not None:
+            rows.index_copy_(0, torch.as_tensor(in_by_peer[peer], device=dev), buf)
 
 
 def _grank(r, group):
