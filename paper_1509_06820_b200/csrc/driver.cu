@@ -186,9 +186,20 @@ void Factor::stages(int64_t i0, int64_t bw, Counters& c, bool defer_trailing, bo
     gemm(h_, true, false, bw, nt2, bw, 1.0, T_, b_, G_, bw, 0.0, X_, bw, s_, st_);
     c.gemm_flops += 2 * mm * bw * nt2 + bw * bw * nt2;
     const bool trail = p_.update_trailing && i0 + bw < m_;
-    // defer_trailing: only R12 = C[:b] - Y[:b] X here; trailing() does C[b:]
-    gemm(h_, false, false, (trail && !defer_trailing) ? mm : bw, nt2, bw, -1.0, Yb, p_.ldy, X_, bw,
-         1.0, C, p_.ldw, s_, st_, kProfUpdate);
+    // defer_trailing: only R12 = C[:b] - Y[:b] X here (its kernel also
+    // snapshots the abort word for trailing(), see there); trailing() does C[b:]
+    const int64_t rows = (trail && !defer_trailing) ? mm : bw;
+    bool snapped = false;
+    if (defer_trailing)
+      snapped = rank_update(h_, rows, nt2, bw, Yb, p_.ldy, X_, bw, C, p_.ldw, s_, st_,
+                            kProfUpdate, 0, pre_);
+    if (!snapped) {
+      if (defer_trailing)
+        RQ_CUDA(cudaMemcpyAsync(&pre_->abort, &st_->abort, sizeof(int), cudaMemcpyDeviceToDevice,
+                                s_));
+      gemm(h_, false, false, rows, nt2, bw, -1.0, Yb, p_.ldy, X_, bw, 1.0, C, p_.ldw, s_, st_,
+           kProfUpdate);
+    }
     c.gemm_flops += 2 * bw * bw * nt2;
     touch(c, mm * nt2 + mm * bw + bw * nt2);
     if (trail) {
@@ -518,9 +529,7 @@ FactorResult Factor::run() {
     // so it runs on a side stream on a share of the SMs while the trailing
     // rows of this block's update run on the rest (join before its swaps)
     const bool ovl = overlap && e.has_update && m_ - i0 > want;
-    stages(i0, want, e.stage, ovl, g_ready);
-    if (ovl) RQ_CUDA(cudaMemcpyAsync(&pre_->abort, &st_->abort, sizeof(int),
-                                     cudaMemcpyDeviceToDevice, s_));
+    stages(i0, want, e.stage, ovl, g_ready);   // with ovl, also snapshots the abort word
     if (e.has_update) update(i0 + want, want, true, e.update);
     if (ovl) {
       const int P = overlap_split(i0, want);

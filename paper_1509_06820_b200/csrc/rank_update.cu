@@ -33,9 +33,19 @@ struct RuArgs {
   double* C; int64_t ldc;
   const Status* st;
   int vec16;
+  Status* snap;   // optional: copy of st->abort taken at kernel entry (block 0)
+  // optional (K-specialised kernel): C is read from Cs (ld ldcs) and written
+  // to C, and rows [M, M + extra_rows) of Cs are copied through unchanged
+  const double* Cs; int64_t ldcs; int extra_rows;
 };
 
+RQ_DEV void snapshot_abort(const RuArgs& a) {
+  if (a.snap != nullptr && blockIdx.x == 0 && threadIdx.x == 0)
+    a.snap->abort = a.st != nullptr ? *((volatile const int*)&a.st->abort) : 0;
+}
+
 __global__ void __launch_bounds__(kRuThreads, 1) rank_update_kernel(RuArgs a) {
+  snapshot_abort(a);
   if (aborted(a.st)) return;
   extern __shared__ __align__(16) double sm[];
   double* As = sm;
@@ -142,6 +152,7 @@ __global__ void __launch_bounds__(kRuThreads, 1) rank_update_kernel(RuArgs a) {
 // counters, profiles/).  Edge tiles take the checked path.
 template <int K>
 __global__ void __launch_bounds__(kRuThreads, 1) rank_update_k_kernel(RuArgs a) {
+  snapshot_abort(a);
   if (aborted(a.st)) return;
   constexpr int LDB = K + 4;
   constexpr int SA = K * kLdA, SB = kTN * LDB, SC = kTN * kLdC;
@@ -158,6 +169,8 @@ __global__ void __launch_bounds__(kRuThreads, 1) rank_update_k_kernel(RuArgs a) 
   const int64_t t_lo = ntiles * blockIdx.x / gridDim.x;
   const int64_t t_hi = ntiles * (blockIdx.x + 1) / gridDim.x;
   const int64_t ldy = a.ldy, ldx = a.ldx, ldc = a.ldc;
+  const double* Csrc = a.Cs != nullptr ? a.Cs : a.C;
+  const int64_t ldcs = a.Cs != nullptr ? a.ldcs : a.ldc;
   // fixed per-thread copy pattern (16 B per cp.async)
   //   Y tile As[k][m]: k = (tid >> 5) + 8 q, m = 2 (tid & 31)        q < K / 8
   //   C tile Cs[n][m]: n = (tid >> 5) + 8 q, m = 2 (tid & 31)        q < 8
@@ -180,10 +193,10 @@ __global__ void __launch_bounds__(kRuThreads, 1) rank_update_k_kernel(RuArgs a) 
       for (int q = 0; q < kTN / XROWS; ++q) cp_async16(d + q * XROWS * LDB, g + q * XROWS * ldx, 16);
     }
     {
-      const double* g = a.C + m0 + ym + (n0 + yk) * ldc;
+      const double* g = Csrc + m0 + ym + (n0 + yk) * ldcs;
       double* d = Cs + b * SC + yk * kLdC + ym;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) cp_async16(d + q * 8 * kLdC, g + q * 8 * ldc, 16);
+      for (int q = 0; q < 8; ++q) cp_async16(d + q * 8 * kLdC, g + q * 8 * ldcs, 16);
     }
     cp_async_commit();
   };
@@ -203,7 +216,7 @@ __global__ void __launch_bounds__(kRuThreads, 1) rank_update_k_kernel(RuArgs a) 
     for (int e = tid; e < kTN * kTM; e += kRuThreads) {
       const int n = e / kTM, i = e % kTM;
       const bool ok = m0 + i < M && n0 + n < N;
-      cp_async8(Cs + b * SC + n * kLdC + i, ok ? a.C + m0 + i + (n0 + n) * ldc : a.C, ok);
+      cp_async8(Cs + b * SC + n * kLdC + i, ok ? Csrc + m0 + i + (n0 + n) * ldcs : Csrc, ok);
     }
     cp_async_commit();
   };
@@ -282,6 +295,12 @@ __global__ void __launch_bounds__(kRuThreads, 1) rank_update_k_kernel(RuArgs a) 
           }
       }
     }
+    if (a.extra_rows > 0 && (t % tm) == tm - 1) {   // pass-through rows below the update
+      for (int e = tid; e < a.extra_rows * kTN; e += kRuThreads) {
+        const int r = e % a.extra_rows, j = e / a.extra_rows;
+        if (n0 + j < N) a.C[M + r + (n0 + j) * ldc] = Csrc[M + r + (n0 + j) * ldcs];
+      }
+    }
     __syncthreads();  // buffers `buf` / X slot reloaded by the next prefetch
     xs = xs_next;
   }
@@ -303,7 +322,8 @@ void launch_rank_update_k(Handle& h, const RuArgs& a, int grid, cudaStream_t s) 
 
 bool rank_update(Handle& h, int64_t M, int64_t N, int64_t K, const double* Y, int64_t ldy,
                  const double* X, int64_t ldx, double* C, int64_t ldc, cudaStream_t s,
-                 const Status* st, int cat, int max_ctas) {
+                 const Status* st, int cat, int max_ctas, Status* snap, const double* Csrc,
+                 int64_t ldcs, int extra_rows) {
   if (K < 4 || K > kKMax || (K % 4) != 0 || M <= 0 || N <= 0) return false;
   static bool attr = false;
   if (!attr) {
@@ -313,7 +333,10 @@ bool rank_update(Handle& h, int64_t M, int64_t N, int64_t K, const double* Y, in
   }
   const auto al = [](const double* p, int64_t ld) { return ((uintptr_t)p & 15) == 0 && ld % 2 == 0; };
   RuArgs a{M, N, (int)K, Y, ldy, X, ldx, C, ldc, st,
-           (h.gemm_vec16 && al(Y, ldy) && al(X, ldx) && al(C, ldc)) ? 1 : 0};
+           (h.gemm_vec16 && al(Y, ldy) && al(X, ldx) && al(C, ldc) &&
+            (Csrc == nullptr || al(Csrc, ldcs))) ? 1 : 0,
+           snap, Csrc, ldcs, extra_rows};
+  if (Csrc != nullptr && !(a.vec16 && (K == 32 || K == 64))) return false;   // k-kernel only
   const int64_t ntiles = ((M + kTM - 1) / kTM) * ((N + kTN - 1) / kTN);
   const int cap = max_ctas > 0 ? std::min(max_ctas, h.num_sms) : h.num_sms;
   const int grid = (int)std::min<int64_t>(cap, ntiles);

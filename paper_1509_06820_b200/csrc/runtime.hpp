@@ -159,7 +159,8 @@ void gemm(Handle& h, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double a
 // persistent C -= Y X for K <= 64 (rank_update.cu); false if not applicable
 bool rank_update(Handle& h, int64_t M, int64_t N, int64_t K, const double* Y, int64_t ldy,
                  const double* X, int64_t ldx, double* C, int64_t ldc, cudaStream_t s,
-                 const Status* st, int cat, int max_ctas = 0);
+                 const Status* st, int cat, int max_ctas = 0, Status* snap = nullptr,
+                 const double* Csrc = nullptr, int64_t ldcs = 0, int extra_rows = 0);
 
 // ------------------------------------------------------------------ kernels (small.cu, select.cu, panel.cu)
 struct SelectOut {

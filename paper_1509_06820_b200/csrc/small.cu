@@ -418,6 +418,11 @@ void sample_update_pre(Handle& h, int64_t ell, int64_t b, int64_t n2, const doub
                        double* Bnew, int64_t ldb, Status* st, cudaStream_t s) {
   if (n2 <= 0) return;
   ProfScope prof(h, kProfSampleUpd, 3.0 * b * b * n2, 8.0 * (2 * ell * n2 + b * b), s);
+  // one launch: Bnew[:b] = S12 - M R12 and Bnew[b:] = S22 (rank-b kernel with a
+  // separate C source and pass-through rows); else copy + GEMM
+  if (rank_update(h, b, n2, b, M, b, R12, ldr, Bnew, ldb, s, st, kProfSampleUpd, 0, nullptr,
+                  S + (size_t)b * lds, lds, (int)(ell - b)))
+    return;
   copy2d(S + (size_t)b * lds, lds, Bnew, ldb, ell, n2, s, st);
   if (!rank_update(h, b, n2, b, M, b, R12, ldr, Bnew, ldb, s, st, kProfSampleUpd))
     gemm(h, false, false, b, n2, b, -1.0, M, b, R12, ldr, 1.0, Bnew, ldb, s, st, kProfSampleUpd);
