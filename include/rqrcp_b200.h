@@ -193,8 +193,12 @@ int rq_omega_fill(uint64_t k0, uint64_t k1, uint64_t raw, double* out, int64_t c
  * "panel_cluster_max_rows" (size thresholds of the heuristic), "fast_panel"
  * (1 = CholeskyQR2 + Householder-reconstruction panel first, falling back to
  * the column-by-column kernel when the panel is ill-conditioned; 0 = always
- * column-by-column), "fast_panel_max_ctas", "use_rank_update", "gemm_vec16",
- * "debug_timers" */
+ * column-by-column), "fast_panel_max_ctas", "fast_panel_spec", "use_rank_update",
+ * "gemm_vec16", "select_reg", "select_max_ctas", "overlap_select",
+ * "overlap_sel_ctas" (next block's select beside the trailing update),
+ * "su_gemm", "overlap_inner", "overlap_panel_ctas" (inner product beside the
+ * fast panel), "block_finish" (X, R12 and the sample update fused per column
+ * tile), "profile_trace", "debug_timers" */
 int rq_set_option(rq_handle_t h, const char* name, int64_t value);
 
 /* debug: phase timers written by the kernels when "debug_timers" is set */

@@ -79,6 +79,7 @@ class Factor {
               bool g_ready = false);
   bool panel_overlap_inner(int64_t i0, int64_t bw);
   bool msu_ready_ = false;   // the fast panel left the sample update's M in "su_Mpre"
+  bool fin_ready_ = false;   // ... and A1 = Y1 T, A2 = M T in "fin_A12": block_finish() path
   void trailing(int64_t i0, int64_t bw, int max_ctas, const Status* pred);
   void stream_out(int64_t upto, bool final);
   int64_t host_done_ = 0;   // columns whose host copies are enqueued
@@ -180,6 +181,29 @@ void Factor::stages(int64_t i0, int64_t bw, Counters& c, bool defer_trailing, bo
   const double* Yb = p_.Y + i0 + i0 * p_.ldy;
   if (!p_.truncated) {
     double* C = p_.work + i0 + (i0 + bw) * p_.ldw;
+    if (g_ready && fin_ready_) {
+      // X, R12, the sample update, the panel's zero fill and the abort
+      // snapshot in one launch (csrc/finish.cu); trailing() does C[b:]
+      FinishArgs f{};
+      f.nt2 = nt2; f.mm = mm; f.b = (int)bw; f.ell = (int)ell_;
+      f.Ctop = C; f.ldw = p_.ldw;
+      f.H = (const double*)h_.buf("inner_H", 8, s_);
+      f.A12 = (const double*)h_.buf("fin_A12", 8, s_);
+      f.Ytop = Yb; f.ldy = p_.ldy;
+      f.Msu = (const double*)h_.buf("su_Mpre", 8, s_);
+      f.S = S_ + bw * ell_; f.lds = ell_;
+      f.X = X_; f.Bn = B_; f.ldb = ell_;
+      f.Pz = p_.work + i0 + bw + i0 * p_.ldw;
+      f.st = st_; f.pre = pre_;
+      if (!block_finish(h_, f, s_)) throw std::runtime_error("block_finish: unsupported shape");
+      c.gemm_flops += 2 * mm * bw * nt2 + bw * bw * nt2 + 2 * bw * bw * nt2;
+      touch(c, mm * nt2 + mm * bw + bw * nt2);
+      if (p_.update_trailing && i0 + bw < m_) {
+        c.gemm_flops += 2 * (mm - bw) * bw * nt2;
+        touch(c, (mm - bw) * nt2);
+      }
+      return;
+    }
     if (!g_ready)   // else panel_overlap_inner() assembled G = Y^T C
       gemm(h_, true, false, bw, nt2, mm, 1.0, Yb, p_.ldy, C, p_.ldw, 0.0, G_, bw, s_, st_,
            kProfInner);
@@ -255,8 +279,12 @@ bool Factor::panel_overlap_inner(int64_t i0, int64_t bw) {
   const double* Mrm = nullptr;
   int64_t ldm = 0;
   double* msu = (double*)h_.buf("su_Mpre", (size_t)b_ * b_ * 8, s_);
+  // block_finish() needs a deferred trailing update (the select overlap) and b in {32, 64}
+  fin_ready_ = h_.block_finish && (bw == 32 || bw == 64) && ell_ >= bw && p_.update_trailing &&
+               i0 + bw < k_ && h_.overlap_select;
+  double* a12 = fin_ready_ ? (double*)h_.buf("fin_A12", (size_t)2 * b_ * b_ * 8, s_) : nullptr;
   panel_fast(h_, mm, bw, o.Rdst, p_.ldw, o, tol_, st_, s_, true, i0, h_.overlap_panel_ctas, true,
-             &Mrm, &ldm, S_, ell_, msu);
+             &Mrm, &ldm, S_, ell_, msu, a12);
   msu_ready_ = true;
   const double* Pb = p_.work + i0 + bw + i0 * p_.ldw;
   const double* Cb = p_.work + i0 + bw + (i0 + bw) * p_.ldw;
@@ -264,6 +292,7 @@ bool Factor::panel_overlap_inner(int64_t i0, int64_t bw) {
        kProfInner);
   RQ_CUDA(cudaEventRecord(h_.ev_join, s2));
   RQ_CUDA(cudaStreamWaitEvent(s_, h_.ev_join, 0));
+  if (fin_ready_) return true;   // stages() runs block_finish()
   // G = Y_top^T C_top + M^T H   (M^T is Mrm read column-major with ld ldm)
   gemm(h_, true, false, bw, nt2, bw, 1.0, o.Y, p_.ldy, p_.work + i0 + (i0 + bw) * p_.ldw, p_.ldw,
        0.0, G_, bw, s_, st_, kProfInner);
@@ -333,13 +362,16 @@ void Factor::update(int64_t i0_new, int64_t bw, bool spec, Counters& c) {
   } else {
     R11 = p_.R + i0 + i0 * p_.ldR; R12 = p_.R + i0 + i0_new * p_.ldR; ldr = p_.ldR;
   }
-  if (msu_ready_ && spec) {
+  if (fin_ready_ && spec) {
+    // done by block_finish()
+  } else if (msu_ready_ && spec) {
     sample_update_pre(h_, ell_, bw, n2, S_, ell_, (const double*)h_.buf("su_Mpre", 8, s_), R12,
                       ldr, B_, ell_, st_, s_);
   } else {
     sample_update(h_, ell_, bw, n2, S_, ell_, R11, R12, ldr, frob_, B_, ell_, st_, spec, i0, s_);
   }
   msu_ready_ = false;
+  fin_ready_ = false;
   c.gemm_flops += 3 * bw * bw * n2;
   touch(c, 2 * bw * bw + 3 * bw * n2);
 }
@@ -482,7 +514,7 @@ FactorResult Factor::run() {
         pend.clear();
         if (overlap) RQ_CUDA(cudaStreamSynchronize(h_.side_stream()));
         next_selected = false;
-        msu_ready_ = false;
+        msu_ready_ = fin_ready_ = false;
         RQ_CUDA(cudaMemsetAsync(&st_->abort, 0, sizeof(int), s_));
         if (code == kAbortDegenerate) {
           i0 = X + bwX;
@@ -520,7 +552,7 @@ FactorResult Factor::run() {
     if (!next_selected) select(i0, want, true);   // else launched during the previous block
     next_selected = false;
     swaps(i0, want);
-    msu_ready_ = false;
+    msu_ready_ = fin_ready_ = false;
     const bool g_ready = overlap && h_.overlap_inner && fast_aborts_ &&
                          panel_overlap_inner(i0, want);
     if (!g_ready) panel(i0, want, kPanelCommitIfFull, true, e.stage);

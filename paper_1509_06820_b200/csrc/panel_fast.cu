@@ -57,6 +57,7 @@ struct FastArgs {
   int defer_zero;                   // leave the panel rows below the diagonal to the caller
   const double* S11; int64_t lds11; // optional: sample block for the sample update's M
   double* msu;                      // out (if S11): M = S11 R11^{-1}, b x b column-major
+  double* a12;                      // out (if T): A1 = Y1 T, A2 = M T, b x b column-major each
   int64_t i0;
   int64_t nchunks;
   Status* st;
@@ -579,6 +580,24 @@ __global__ void __launch_bounds__(kFT, 1) panel_fast_kernel(FastArgs a) {
           const int l = e / n, i = e - l * n;
           a.T[i + (int64_t)l * a.ldt] = i <= l ? -W4[i * ld + l] : 0.0;
         }
+        if (a.a12 != nullptr) {
+          // X = T^T G with G = Y1^T C_top + M^T H  =>  X = A1^T C_top + A2^T H,
+          // A1 = Y1 T, A2 = M T (block_finish_kernel applies them per column tile)
+          __syncthreads();
+          for (int i = r0; i < n8; i += rstep) {
+            W3[i * ld + c0] = W0[c0 * ld + i];                    // Y1 (unit lower) = (Y1^T)^T
+            W5[i * ld + c0] = a.gmat[3 * nn + i * n8 + c0];       // M (this CTA wrote it)
+          }
+          __syncthreads();
+          chunk_mm<false, true>(W3, W4, W2, n8, n8, ld);   // Y1 (-T)
+          chunk_mm<false, true>(W5, W4, W1, n8, n8, ld);   // M (-T)
+          __syncthreads();
+          for (int e = tid; e < n * n; e += kFT) {   // row-major: block_finish's staging layout
+            const int i = e / n, l = e - i * n;
+            a.a12[e] = -W2[i * ld + l];
+            a.a12[(int64_t)n * n + e] = -W1[i * ld + l];
+          }
+        }
       }
     }
     if (tid == 0) {
@@ -641,7 +660,7 @@ const int* panel_fast(Handle& h, int64_t mm, int64_t bw, const double* P, int64_
                       const PanelOut& out, double tol, Status* st, cudaStream_t s,
                       bool abort_on_decline, int64_t i0, int max_ctas, bool defer_zero,
                       const double** m_rowmajor, int64_t* m_ld, const double* S11,
-                      int64_t lds11, double* msu) {
+                      int64_t lds11, double* msu, double* a12) {
   if (!panel_fast_eligible(h, mm, bw)) return nullptr;
   const int n8 = (int)((bw + 7) / 8 * 8);
   const int ld = n8 + 1;
@@ -664,6 +683,7 @@ const int* panel_fast(Handle& h, int64_t mm, int64_t bw, const double* P, int64_
   a.abort_on_decline = abort_on_decline ? 1 : 0;
   a.defer_zero = defer_zero ? 1 : 0;
   a.S11 = S11; a.lds11 = lds11; a.msu = S11 != nullptr ? msu : nullptr;
+  a.a12 = out.T != nullptr ? a12 : nullptr;
   a.i0 = i0;
   a.bar = (unsigned int*)h.buf("pf_bar", 64, s);
   static void* zeroed = nullptr;

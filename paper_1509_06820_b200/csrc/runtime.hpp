@@ -111,6 +111,8 @@ class Handle {
   // inner GEMM's P_below^T C_below part concurrently with the fast panel
   bool overlap_inner = true;
   int overlap_panel_ctas = 48;  // SMs for the fast panel while it overlaps
+  // ... then X, R12 and the sample update fused per column tile (csrc/finish.cu)
+  bool block_finish = true;
   int overlap_sel_ctas = 0;   // SMs for the overlapped select (0 = size heuristic)
   bool gemm_vec16 = true;
   long long* dbg = nullptr;  // optional device phase-timer buffer (debug)
@@ -208,7 +210,27 @@ const int* panel_fast(Handle& h, int64_t mm, int64_t bw, const double* P, int64_
                       bool abort_on_decline = false, int64_t i0 = 0, int max_ctas = 0,
                       bool defer_zero = false, const double** m_rowmajor = nullptr,
                       int64_t* m_ld = nullptr, const double* S11 = nullptr,
-                      int64_t lds11 = 0, double* msu = nullptr);
+                      int64_t lds11 = 0, double* msu = nullptr, double* a12 = nullptr);
+
+// Rest of a speculative RQRCP block after a committed fast panel, one CTA per
+// 64-column tile of the trailing matrix (csrc/finish.cu):
+//   X = A1^T C_top + A2^T H, R12 = C_top - Y_top X (in place),
+//   B_new = [S12 - Msu R12; S22], panel rows below the diagonal zeroed,
+//   and the abort-word snapshot for the deferred trailing update.
+struct FinishArgs {
+  int64_t nt2, mm; int b, ell;
+  double* Ctop; int64_t ldw;        // work rows [i0, i0+b) x cols [i0+b, n): C_top in, R12 out
+  const double* H;                  // b x nt2, ld b
+  const double* A12;                // [A1; A2], b x b row-major each
+  const double* Ytop; int64_t ldy;  // b x b unit lower
+  const double* Msu;                // b x b
+  const double* S; int64_t lds;     // sample columns [b, b+nt2): S12 rows < b, S22 rows >= b
+  double* X;                        // b x nt2, ld b
+  double* Bn; int64_t ldb;          // ell x nt2
+  double* Pz;                       // panel rows below the diagonal: (mm - b) x b, ld ldw
+  Status* st; Status* pre;
+};
+bool block_finish(Handle& h, const FinishArgs& f, cudaStream_t s);
 
 // B_new = [S12 - M R12; S22] with M = S11 R11^{-1} already formed (by the
 // fast panel of the same block, which also cleared the degenerate guard).

@@ -17,6 +17,9 @@ cfg = bench.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "cfg2"]
 dev = torch.device("cuda", 0)
 A = bench.device_matrix(cfg["kind"], cfg["m"], cfg["n"], dev, seed=0)
 lib, h = _abi.load_library(), _abi.handle(0)
+for kv in sys.argv[2:]:   # option overrides, name=value
+    k, v = kv.split("=")
+    _abi.check(lib.rq_set_option(h, k.encode(), int(v)))
 bench.run_ours(P, cfg, A, None)
 torch.cuda.synchronize()
 _abi.check(lib.rq_set_option(h, b"profile_trace", 1))
@@ -51,6 +54,11 @@ span = recs[-1][1] - recs[0][0]
 print(json.dumps({"launches": n, "span_ms": round(span, 2), "busy_ms": round(sum(busy.values()), 2),
                   "idle_ms": round(span - sum(busy.values()), 2)}))
 print(json.dumps({"busy": {k: round(v, 2) for k, v in busy.items()}}))
+cnt_f = defaultdict(int)
+for _, _, nm in recs:
+    cnt_f[nm] += 1
+print(json.dumps({"mean_us": {k: round(1e3 * busy[k] / cnt_f[k], 1) for k in busy},
+                  "count": dict(cnt_f)}))
 print(json.dumps({"gap_before": {k: round(v, 2) for k, v in gap_before.items()}}))
 print(json.dumps({"gap_after": {k: round(v, 2) for k, v in gap_after.items()}}))
 print(json.dumps({"largest_gaps": sorted(big, reverse=True)[:15]}))
