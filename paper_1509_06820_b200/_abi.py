@@ -11,7 +11,7 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "librqrcp_b200.so")
+LIB_PATH = os.environ.get("RQ_LIB_PATH") or os.path.join(HERE, "librqrcp_b200.so")
 
 RQ_OK, RQ_ERR_INVALID, RQ_ERR_INTERNAL, RQ_ERR_CUDA = 0, -1, -2, -3
 RQ_RQRCP, RQ_RSRQRCP, RQ_SSRQRCP, RQ_TRQRCP = 0, 1, 2, 3

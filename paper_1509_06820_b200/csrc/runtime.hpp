@@ -113,6 +113,8 @@ class Handle {
   int overlap_panel_ctas = 48;  // SMs for the fast panel while it overlaps
   // ... then X, R12 and the sample update fused per column tile (csrc/finish.cu)
   bool block_finish = true;
+  int sel_kstride = 16;   // grid select: key entries 128 B apart
+  int sel_poll_ns = 0;
   int overlap_sel_ctas = 0;   // SMs for the overlapped select (0 = size heuristic)
   bool gemm_vec16 = true;
   long long* dbg = nullptr;  // optional device phase-timer buffer (debug)

@@ -617,14 +617,17 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_reg_kernel(SelArgs a) {
 
   int got = a.want;
   int64_t l2 = 0, l2b = 0;
-  long long tm[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  long long tlast = clock64();
+  __shared__ long long tm[5];   // phase timers (thread 0 of CTA 0), off the register budget
   const bool timing = a.dbg != nullptr && me == 0 && tid == 0;
+  if (timing) {
+    for (int k = 0; k < 4; ++k) tm[k] = 0;
+    tm[4] = clock64();
+  }
   auto mark = [&](int k) {
     if (timing) {
       const long long t = clock64();
-      tm[k] += t - tlast;
-      tlast = t;
+      tm[k] += t - tm[4];
+      tm[4] = t;
     }
   };
   for (int j = 0; j < a.want; ++j) {
@@ -685,9 +688,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_reg_kernel(SelArgs a) {
         for (int k = 0; k < 5; ++k) {
           const int i = lane + 32 * k;
           if (i >= j && i < ell) {
-            const double v = (i == j) ? 1.0 : (zero ? xv[k] : __dmul_rn(xv[k], rinv));
-            wv[i] = v;
-            wtv[i] = __dmul_rn(tau, v);
+            wv[i] = (i == j) ? 1.0 : (zero ? xv[k] : __dmul_rn(xv[k], rinv));
           }
         }
       }
@@ -720,13 +721,11 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_reg_kernel(SelArgs a) {
     }
     mark(0);
     // ---- my columns: relabel (swap j <-> p), pivot column, H_j, downdate, key
-    double vr[RPL], tvr[RPL];
+    double vr[RPL];   // tau v is formed per use (same rounding as wtv, fewer live registers)
 #pragma unroll
     for (int r = 0; r < RPL; ++r) {
       const int i = gl + 8 * r;
-      const bool act = i >= j && i < ell;
-      vr[r] = act ? wv[i] : 0.0;
-      tvr[r] = act ? wtv[i] : 0.0;
+      vr[r] = (i >= j && i < ell) ? wv[i] : 0.0;
     }
     unsigned long long key = 0ull;
 #pragma unroll
@@ -762,7 +761,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_reg_kernel(SelArgs a) {
 #pragma unroll
         for (int r = 0; r < RPL; ++r) {
           const int i = gl + 8 * r;
-          if (i >= j) x[t][r] = __dsub_rn(x[t][r], __dmul_rn(tvr[r], w));
+          if (i >= j) x[t][r] = __dsub_rn(x[t][r], __dmul_rn(__dmul_rn(tau, vr[r]), w));
         }
       }
       if (j + 1 < a.nt) {
@@ -882,7 +881,7 @@ bool launch_select_reg(Handle& h, bool grid, int P, int cpb, int64_t ell, int64_
                        int64_t want, const double* B, int64_t ldb, const SelectOut& out,
                        Status* st, bool abort_on_short, int64_t i0, cudaStream_t s) {
   constexpr int NG = kSelThreads / 8, NW = kSelThreads / 32;
-  const int cpg = cpb <= NG ? 1 : (cpb <= 2 * NG ? 2 : 0);
+  const int cpg = cpb <= NG ? 1 : (cpb <= 2 * NG ? 2 : (cpb <= 3 * NG ? 3 : 0));
   const int rpl = ell <= 40 ? 5 : (ell <= 72 ? 9 : (ell <= 136 ? 17 : (ell <= 160 ? 20 : 0)));
   if (cpg == 0 || rpl == 0 || (rpl > 9 && cpg > 1)) return false;
   const int ldl = (int)(ell | 1);
@@ -914,7 +913,8 @@ bool launch_select_reg(Handle& h, bool grid, int P, int cpb, int64_t ell, int64_
     else launch_reg<true, R, C>(h, P, smem, a, s);                        \
     return true;                                                          \
   }
-  RQ_SEL_REG(5, 1) RQ_SEL_REG(5, 2) RQ_SEL_REG(9, 1) RQ_SEL_REG(9, 2) RQ_SEL_REG(17, 1)
+  RQ_SEL_REG(5, 1) RQ_SEL_REG(5, 2) RQ_SEL_REG(5, 3) RQ_SEL_REG(9, 1) RQ_SEL_REG(9, 2)
+  RQ_SEL_REG(9, 3) RQ_SEL_REG(17, 1)
   RQ_SEL_REG(20, 1)
 #undef RQ_SEL_REG
   return false;

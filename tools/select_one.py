@@ -1,4 +1,4 @@
-"""One select call for ncu: python tools/select_one.py nt force(1 grid / 2 cluster)"""
+"""One select call for ncu: python tools/select_one.py nt force(1 grid / 2 cluster) [max_ctas]"""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -7,6 +7,8 @@ from paper_1509_06820_b200.device import to_device_fortran
 lib = _abi.load_library(); h = _abi.handle(0)
 nt, force = int(sys.argv[1]), int(sys.argv[2])
 lib.rq_set_option(h, b"force_select", force)
+if len(sys.argv) > 3:
+    lib.rq_set_option(h, b"select_max_ctas", int(sys.argv[3]))
 B = to_device_fortran(np.random.default_rng(0).standard_normal((72, nt)), torch.device("cuda", 0))
 for _ in range(2):
     K.select_pivots(B, 64)
