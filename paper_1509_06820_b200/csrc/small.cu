@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(256) su_prep_kernel(const double* __restrict__
 
 // One-launch replay of the select swaps (randomized.py:138-147): the net
 // permutation of the <= 2 got touched positions is planned redundantly by
-// every block (<= 64 pivots), then each block moves ITS rows of every moved
+// every block (<= 256 pivots, one backward trace per position), then each block moves ITS rows of every moved
 // column through shared memory -- all sources of a row chunk are read before
 // any destination is written, and blocks own disjoint rows, so no scratch
 // buffer or second pass is needed.  Units: row chunks of the work matrix, of
@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(256) swap_fused_kernel(const int64_t* __restri
   if (aborted(st)) return;
   const int got = (int)st->got;
   extern __shared__ double sbuf[];                 // [2 got][kSwapRows]
-  __shared__ int pv[256], slotb[256], src[512], lsrc[512], ldst[512];
+  __shared__ int pv[256], lsrc[512], ldst[512];
   __shared__ int s_nlive;
   __shared__ int64_t s_nswaps;
   const int tid = threadIdx.x;
@@ -222,37 +222,30 @@ __global__ void __launch_bounds__(256) swap_fused_kernel(const int64_t* __restri
   }
   for (int e = tid; e < got; e += blockDim.x) pv[e] = (int)piv[e];
   __syncthreads();
-  // slots: position q < got -> slot q; q >= got -> got + first k with piv[k] == q
-  for (int e = tid; e < got; e += blockDim.x) {
-    const int q = pv[e];
-    int sl = q;
-    if (q >= got) {
-      int k = e;
-      for (int kk = 0; kk < e; ++kk)
-        if (pv[kk] == q) { k = kk; break; }
-      sl = got + k;
-    }
-    slotb[e] = sl;
-    src[e] = e;
-    src[got + e] = q;
-  }
-  __syncthreads();
-  if (tid == 0)
-    for (int j = 0; j < got; ++j) {
-      const int b = slotb[j];
-      if (b != j) {
-        const int tmp = src[j];
-        src[j] = src[b];
-        src[b] = tmp;
-      }
-    }
-  __syncthreads();
+  // touched positions: q < got, and each pivot position q >= got once (its
+  // first occurrence).  Position q's final content comes from the position
+  // found by replaying the transpositions (k, piv[k]) backwards -- one
+  // independent trace per thread instead of a serial replay.
   for (int e = tid; e < 2 * got; e += blockDim.x) {
-    const int q = e < got ? e : pv[e - got];
-    const bool live = e < got || (q >= got && slotb[e - got] == e);
-    if (live && src[e] != q) {
+    int q;
+    bool cand = true;
+    if (e < got) {
+      q = e;
+    } else {
+      const int k0 = e - got;
+      q = pv[k0];
+      cand = q >= got;
+      for (int kk = 0; kk < k0 && cand; ++kk) cand = pv[kk] != q;
+    }
+    if (!cand) continue;
+    int sp = q;
+    for (int k = got - 1; k >= 0; --k) {
+      const int pk = pv[k];
+      sp = sp == k ? pk : (sp == pk ? k : sp);
+    }
+    if (sp != q) {
       const int i = atomicAdd(&s_nlive, 1);
-      lsrc[i] = src[e];
+      lsrc[i] = sp;
       ldst[i] = q;
     }
   }
@@ -286,9 +279,22 @@ __global__ void __launch_bounds__(256) swap_fused_kernel(const int64_t* __restri
   }
   const int64_t r0 = (int64_t)u * kSwapRows;
   const int nr = (int)imin64(kSwapRows, rows - r0);
-  for (int e = tid; e < nl * kSwapRows; e += blockDim.x) {
-    const int i = e / kSwapRows, r = e - i * kSwapRows;
-    if (r < nr) sbuf[e] = base[(r0 + r) * rstride + (i0 + lsrc[i]) * cstride];
+  // eight independent loads in flight per thread (one dependent round trip
+  // per element made this phase latency bound)
+  const int tot = nl * kSwapRows;
+  for (int e0 = tid; e0 < tot; e0 += 8 * blockDim.x) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * blockDim.x;
+      const int i = e / kSwapRows, r = e - i * kSwapRows;
+      v[u] = (e < tot && r < nr) ? base[(r0 + r) * rstride + (i0 + lsrc[i]) * cstride] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * blockDim.x;
+      if (e < tot) sbuf[e] = v[u];
+    }
   }
   __syncthreads();
   for (int e = tid; e < nl * kSwapRows; e += blockDim.x) {
