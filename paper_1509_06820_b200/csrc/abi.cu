@@ -271,6 +271,9 @@ int rq_set_option(rq_handle_t h, const char* name, int64_t value) {
     else if (n == "overlap_inner") hh.overlap_inner = value != 0;
     else if (n == "overlap_panel_ctas") hh.overlap_panel_ctas = (int)value;
     else if (n == "block_finish") hh.block_finish = value != 0;
+    else if (n == "ru_two_ctas") hh.ru_two_ctas = value != 0;
+    else if (n == "ru_skew_ns") hh.ru_skew_ns = (int)value;
+    else if (n == "ru_big") hh.ru_big = value != 0;
     else if (n == "sel_kstride") hh.sel_kstride = std::max(1, std::min(16, (int)value));
     else if (n == "sel_poll_ns") hh.sel_poll_ns = (int)value;
     else if (n == "gemm_vec16") hh.gemm_vec16 = value != 0;

@@ -318,14 +318,19 @@ void Factor::trailing(int64_t i0, int64_t bw, int max_ctas, const Status* pred) 
 // SMs for the next block's select while the trailing update of the block at
 // i0 runs on the rest.  The select is latency bound (64 steps of a few us,
 // nearly flat in its CTA count down to ~1/3 of the GPU), the update is not:
-// a fixed ~38% share (56 of 148 SMs) was measured best on cfg2 (40: 109.6 ms,
-// 48: 106.1, 56: 105.6, 64: 107.4; no overlap 112.4); the cluster variant
-// (narrow samples) uses 16.
+// a ~30% share (44 of 148 SMs) measured best on cfg2 (38: 90.4 ms, 44: 88.9,
+// 48: 89.1, 56: 90.4, 64: 91.9), raised where needed so every CTA's columns
+// stay register-resident (<= 3 per 8-lane group of the v5 kernel, ell <= 72);
+// the cluster variant (narrow samples) uses 16.
 int Factor::overlap_split(int64_t i0, int64_t bw) const {
   const int64_t nt1 = n_ - i0 - bw;
   const int sms = h_.num_sms;
   if (nt1 <= h_.select_cluster_max_cols) return 16;   // cluster variant
-  const int P = h_.overlap_sel_ctas > 0 ? h_.overlap_sel_ctas : (int)(0.38 * sms + 0.5);
+  int P = h_.overlap_sel_ctas > 0 ? h_.overlap_sel_ctas : (int)(0.30 * sms + 0.5);
+  if (h_.overlap_sel_ctas <= 0) {
+    const int64_t per = ell_ <= 72 ? 3 * 64 : 64;   // v5 columns per CTA
+    P = std::max<int64_t>(P, (nt1 + per - 1) / per);
+  }
   return std::max(16, std::min(P, sms - 16));
 }
 

@@ -113,6 +113,9 @@ class Handle {
   int overlap_panel_ctas = 48;  // SMs for the fast panel while it overlaps
   // ... then X, R12 and the sample update fused per column tile (csrc/finish.cu)
   bool block_finish = true;
+  bool ru_two_ctas = false;  // rank update: two single-buffered CTAs per SM
+  int ru_skew_ns = 0;
+  bool ru_big = true;        // rank update: 128 x 64 tiles, C through registers
   int sel_kstride = 16;   // grid select: key entries 128 B apart
   int sel_poll_ns = 0;
   int overlap_sel_ctas = 0;   // SMs for the overlapped select (0 = size heuristic)
