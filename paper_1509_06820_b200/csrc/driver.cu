@@ -288,8 +288,10 @@ bool Factor::panel_overlap_inner(int64_t i0, int64_t bw) {
   msu_ready_ = true;
   const double* Pb = p_.work + i0 + bw + i0 * p_.ldw;
   const double* Cb = p_.work + i0 + bw + (i0 + bw) * p_.ldw;
-  gemm(h_, true, false, bw, nt2, mm - bw, 1.0, Pb, p_.ldw, Cb, p_.ldw, 0.0, H, bw, s2, st_,
-       kProfInner);
+  if (!inner_gemm(h_, bw, nt2, mm - bw, Pb, p_.ldw, Cb, p_.ldw, H, bw, s2, st_,
+                  h_.num_sms - h_.overlap_panel_ctas, kProfInner))
+    gemm(h_, true, false, bw, nt2, mm - bw, 1.0, Pb, p_.ldw, Cb, p_.ldw, 0.0, H, bw, s2, st_,
+         kProfInner);
   RQ_CUDA(cudaEventRecord(h_.ev_join, s2));
   RQ_CUDA(cudaStreamWaitEvent(s_, h_.ev_join, 0));
   if (fin_ready_) return true;   // stages() runs block_finish()

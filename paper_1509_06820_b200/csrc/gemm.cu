@@ -96,6 +96,10 @@ void gemm(Handle& h, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double a
   if (!ta && !tb && alpha == -1.0 && beta == 1.0 && M >= 64 && N >= 64 && h.use_rank_update &&
       rank_update(h, M, N, K, A, lda, B, ldb, C, ldc, s, st, cat))
     return;
+  // tall-skinny inner products G = Y^T C (b = 64) go to the stream-K kernel
+  if (ta && !tb && M == 64 && alpha == 1.0 && beta == 0.0 &&
+      inner_gemm(h, M, N, K, A, lda, B, ldb, C, ldc, s, st, 0, cat))
+    return;
   // algorithmic traffic: read A, B (+ C when beta != 0), write C
   const double bytes = 8.0 * ((double)M * K + (double)K * N + (double)M * N * (beta != 0.0 ? 2 : 1));
   ProfScope prof(h, cat, 2.0 * (double)M * N * K, bytes, s);

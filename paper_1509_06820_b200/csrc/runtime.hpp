@@ -116,6 +116,8 @@ class Handle {
   bool ru_two_ctas = false;  // rank update: two single-buffered CTAs per SM
   int ru_skew_ns = 0;
   bool ru_big = true;        // rank update: 128 x 64 tiles, C through registers
+  bool inner_kernel = true;  // H = P^T C: tall-skinny split-K kernel (csrc/inner.cu)
+  int inner_ktiles = 16;     // ... k-tiles (32 deep) per CTA
   int sel_kstride = 16;   // grid select: key entries 128 B apart
   int sel_poll_ns = 0;
   int overlap_sel_ctas = 0;   // SMs for the overlapped select (0 = size heuristic)
@@ -236,6 +238,12 @@ struct FinishArgs {
   Status* st; Status* pre;
 };
 bool block_finish(Handle& h, const FinishArgs& f, cudaStream_t s);
+
+// H (64 x N, ld ldh) = P^T C with P (K x 64) and C (K x N) column-major,
+// on at most max_ctas SMs (csrc/inner.cu); false when the shape does not qualify
+bool inner_gemm(Handle& h, int64_t M, int64_t N, int64_t K, const double* P, int64_t ldp,
+                const double* C, int64_t ldc, double* H, int64_t ldh, cudaStream_t s,
+                const Status* st, int max_ctas, int cat);
 
 // B_new = [S12 - M R12; S22] with M = S11 R11^{-1} already formed (by the
 // fast panel of the same block, which also cleared the degenerate guard).

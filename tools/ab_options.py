@@ -22,7 +22,7 @@ lib, h = _abi.load_library(), _abi.handle(0)
 
 DEFAULTS = {"fast_panel": 1, "fast_panel_spec": 1, "fast_panel_max_ctas": 0, "use_rank_update": 1,
             "gemm_vec16": 1, "force_select": 0, "force_panel": 0, "select_cluster_max_cols": 1024,
-            "panel_cluster_max_rows": 3072, "select_reg": 1, "select_max_ctas": 0, "overlap_select": 1, "overlap_sel_ctas": 0, "su_gemm": 1, "overlap_inner": 1, "overlap_panel_ctas": 48, "block_finish": 1, "ru_two_ctas": 0, "ru_skew_ns": 0, "ru_big": 1}
+            "panel_cluster_max_rows": 3072, "select_reg": 1, "select_max_ctas": 0, "overlap_select": 1, "overlap_sel_ctas": 0, "su_gemm": 1, "overlap_inner": 1, "overlap_panel_ctas": 48, "block_finish": 1, "ru_two_ctas": 0, "ru_skew_ns": 0, "ru_big": 1, "inner_kernel": 1, "inner_ktiles": 16}
 
 
 def setopts(v):
