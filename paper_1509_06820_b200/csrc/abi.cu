@@ -276,8 +276,6 @@ int rq_set_option(rq_handle_t h, const char* name, int64_t value) {
     else if (n == "ru_big") hh.ru_big = value != 0;
     else if (n == "inner_kernel") hh.inner_kernel = value != 0;
     else if (n == "inner_ktiles") hh.inner_ktiles = (int)value;
-    else if (n == "sel_kstride") hh.sel_kstride = std::max(1, std::min(16, (int)value));
-    else if (n == "sel_poll_ns") hh.sel_poll_ns = (int)value;
     else if (n == "gemm_vec16") hh.gemm_vec16 = value != 0;
     else if (n == "debug_timers") {
       hh.dbg = value ? (long long*)hh.buf("dbg_timers", 64 * 8, nullptr) : nullptr;

@@ -96,4 +96,7 @@ for t, d, nm in ev:
     active[nm] = active.get(nm, 0) + d
 print(json.dumps({"exposed_ms": {k: round(v, 2) for k, v in sorted(exposed.items(), key=lambda x: -x[1])},
                   "idle_ms": round(idle, 2)}))
+if os.environ.get("TRACE_DUMP"):
+    with open(os.environ["TRACE_DUMP"], "w") as f:
+        json.dump([(round(a, 4), round(b, 4), nm) for a, b, nm in recs], f)
 _abi.check(lib.rq_set_option(h, b"profile_trace", 0))
