@@ -84,6 +84,7 @@ class Factor {
   void stream_out(int64_t upto, bool final);
   int64_t host_done_ = 0;   // columns whose host copies are enqueued
   int overlap_split(int64_t i0, int64_t bw) const;
+  int panel_split(int64_t mm, int64_t nt2, int64_t bw) const;
   void update(int64_t i0_new, int64_t bw, bool spec, Counters& c);
   bool slow_block(int64_t& i0, bool resampled, int64_t& rank, bool resume_panel = false);
 };
@@ -283,13 +284,14 @@ bool Factor::panel_overlap_inner(int64_t i0, int64_t bw) {
   fin_ready_ = h_.block_finish && (bw == 32 || bw == 64) && ell_ >= bw && p_.update_trailing &&
                i0 + bw < k_ && h_.overlap_select;
   double* a12 = fin_ready_ ? (double*)h_.buf("fin_A12", (size_t)2 * b_ * b_ * 8, s_) : nullptr;
-  panel_fast(h_, mm, bw, o.Rdst, p_.ldw, o, tol_, st_, s_, true, i0, h_.overlap_panel_ctas, true,
-             &Mrm, &ldm, S_, ell_, msu, a12);
+  const int qp = panel_split(mm, nt2, bw);
+  panel_fast(h_, mm, bw, o.Rdst, p_.ldw, o, tol_, st_, s_, true, i0, qp, true, &Mrm, &ldm, S_, ell_,
+             msu, a12);
   msu_ready_ = true;
   const double* Pb = p_.work + i0 + bw + i0 * p_.ldw;
   const double* Cb = p_.work + i0 + bw + (i0 + bw) * p_.ldw;
-  if (!inner_gemm(h_, bw, nt2, mm - bw, Pb, p_.ldw, Cb, p_.ldw, H, bw, s2, st_,
-                  h_.num_sms - h_.overlap_panel_ctas, kProfInner))
+  if (!inner_gemm(h_, bw, nt2, mm - bw, Pb, p_.ldw, Cb, p_.ldw, H, bw, s2, st_, h_.num_sms - qp,
+                  kProfInner))
     gemm(h_, true, false, bw, nt2, mm - bw, 1.0, Pb, p_.ldw, Cb, p_.ldw, 0.0, H, bw, s2, st_,
          kProfInner);
   RQ_CUDA(cudaEventRecord(h_.ev_join, s2));
@@ -324,6 +326,10 @@ void Factor::trailing(int64_t i0, int64_t bw, int max_ctas, const Status* pred) 
 // 48: 89.1, 56: 90.4, 64: 91.9), raised where needed so every CTA's columns
 // stay register-resident (<= 3 per 8-lane group of the v5 kernel, ell <= 72);
 // the cluster variant (narrow samples) uses 16.
+// Once the sample is narrow enough (nt <= 4608 at cfg2's b = 64, the trailing
+// update then takes < 100 us), fewer columns per CTA shorten the select's
+// apply phase, and 80 SMs are worth taking from the small update
+// (tools/split_sweep.py: blocks 56-95 of cfg2 ~245 vs ~285 us per select phase).
 int Factor::overlap_split(int64_t i0, int64_t bw) const {
   const int64_t nt1 = n_ - i0 - bw;
   const int sms = h_.num_sms;
@@ -332,8 +338,26 @@ int Factor::overlap_split(int64_t i0, int64_t bw) const {
   if (h_.overlap_sel_ctas <= 0) {
     const int64_t per = ell_ <= 72 ? 3 * 64 : 64;   // v5 columns per CTA
     P = std::max<int64_t>(P, (nt1 + per - 1) / per);
+    if (nt1 <= 72 * 64) P = std::max(P, (sms * 80) / 148);
   }
   return std::max(16, std::min(P, sms - 16));
+}
+
+// SMs for the fast panel while the inner product's P_below^T C_below term
+// runs on the rest: fewer while that term is the longer of the two, more once
+// the panel's own row chunks outnumber its CTAs (cfg2 sweep,
+// tools/split_sweep.py: 32 CTAs above ~4 GFLOP of inner work, 48 down to
+// ~2.6 GFLOP, then one CTA per 64-row chunk up to 80)
+int Factor::panel_split(int64_t mm, int64_t nt2, int64_t bw) const {
+  if (h_.overlap_panel_ctas > 0) return h_.overlap_panel_ctas;
+  const double w = 2.0 * (double)(mm - bw) * (double)nt2 * (double)bw;
+  const int sms = h_.num_sms;
+  int q;
+  if (w > 4.0e9) q = 32;
+  else if (w > 2.6e9) q = 48;
+  else q = (int)std::min<int64_t>((mm + 63) / 64, 80);
+  q = (int)((int64_t)q * sms / 148);
+  return std::max(16, std::min(q, sms - 16));
 }
 
 // D2H of the committed columns [host_done_, upto) of Y and R into the caller's

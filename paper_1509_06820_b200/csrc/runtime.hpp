@@ -110,7 +110,7 @@ class Handle {
   bool su_gemm = true;        // sample update as M = S11 R11^-1 then a rank-b GEMM
   // inner GEMM's P_below^T C_below part concurrently with the fast panel
   bool overlap_inner = true;
-  int overlap_panel_ctas = 48;  // SMs for the fast panel while it overlaps
+  int overlap_panel_ctas = 0;   // SMs for the fast panel while it overlaps (0 = size rule)
   // ... then X, R12 and the sample update fused per column tile (csrc/finish.cu)
   bool block_finish = true;
   bool ru_two_ctas = false;  // rank update: two single-buffered CTAs per SM
