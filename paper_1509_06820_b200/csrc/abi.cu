@@ -258,6 +258,7 @@ int rq_set_option(rq_handle_t h, const char* name, int64_t value) {
     else if (n == "force_panel") hh.force_panel = (int)value;
     else if (n == "select_cluster_max_cols") hh.select_cluster_max_cols = value;
     else if (n == "panel_cluster_max_rows") hh.panel_cluster_max_rows = value;
+    else if (n == "panel_rows_per_cta") hh.panel_rows_per_cta = std::max<int64_t>(32, value);
     else if (n == "use_rank_update") hh.use_rank_update = value != 0;
     else if (n == "fast_panel") hh.fast_panel = value != 0;
     else if (n == "fast_panel_max_ctas") hh.fast_panel_max_ctas = (int)value;
@@ -265,6 +266,8 @@ int rq_set_option(rq_handle_t h, const char* name, int64_t value) {
     else if (n == "profile_trace") hh.tracing = value != 0;
     else if (n == "select_max_ctas") hh.select_max_ctas = (int)value;
     else if (n == "select_reg") hh.select_reg = value != 0;
+    else if (n == "omega_ahead") hh.omega_ahead = value != 0;
+    else if (n == "floor_lookahead") hh.floor_lookahead = (int)value;
     else if (n == "overlap_select") hh.overlap_select = value != 0;
     else if (n == "overlap_sel_ctas") hh.overlap_sel_ctas = (int)value;
     else if (n == "su_gemm") hh.su_gemm = value != 0;

@@ -17,6 +17,7 @@
 // reference's state at that branch.
 #include <cstring>
 #include <deque>
+#include <thread>
 #include <vector>
 
 #include "driver.hpp"
@@ -37,6 +38,9 @@ struct Pending {
 class Factor {
  public:
   Factor(Handle& h, const FactorParams& p) : h_(h), p_(p), s_(p.stream), ev_(h.ring_ev) {}
+  ~Factor() {
+    if (ahead_.joinable()) ahead_.join();
+  }
 
   FactorResult run();
 
@@ -57,8 +61,23 @@ class Factor {
   // one (declines cluster near the noise floor) the exact kernel is queued
   // behind every fast panel instead
   bool fast_aborts_ = true;
+  // set once a block hit the noise floor (a degenerate or panel-rank trigger,
+  // or a declined fast panel): the synchronous path then goes straight to the
+  // exact panel, whose verdict the fast one would only have declined to give
+  bool near_floor_ = false;
   Counters c_;
   int64_t m_ = 0, n_ = 0, k_ = 0, b_ = 0, ell_ = 0;
+
+  // Resample Omega look-ahead: the stream is sequential, so the next l*m
+  // draws (the most one resample can take) are drawn on a host thread and
+  // uploaded while the factorization runs; a resample then takes its draws
+  // from the device copy instead of waiting for the host generator.
+  std::thread ahead_;
+  double *ah_h_ = nullptr, *ah_d_ = nullptr;
+  int64_t ah_n_ = 0, ah_pos_ = 0;
+  int ah_rc_ = 0;
+  void start_ahead(bool after_event);
+  const double* omega_take(int64_t rows, int64_t cols);
 
   void sync() { RQ_CUDA(cudaStreamSynchronize(s_)); }
   Status read_status() {
@@ -98,6 +117,61 @@ void Factor::draw_omega(int64_t rows, int64_t cols) {
   RQ_CUDA(cudaMemcpyAsync(om_d_, om_h_, (size_t)rows * cols * 8, cudaMemcpyHostToDevice, s_));
 }
 
+// after_event: the device copy is still being read by work enqueued on s_
+// (h_.ev_omega recorded there), so the upload waits for it
+void Factor::start_ahead(bool after_event) {
+  if (p_.omega_fn == nullptr || !h_.omega_ahead) return;
+  const int64_t n = ell_ * m_;
+  ah_h_ = (double*)h_.host_pinned("omega_ahead_h", (size_t)n * 8, s_);
+  ah_d_ = (double*)h_.buf("omega_ahead_d", (size_t)n * 8, s_);
+  ah_n_ = n;
+  ah_pos_ = 0;
+  ah_rc_ = 0;
+  cudaStream_t os = h_.omega_stream();
+  if (after_event) RQ_CUDA(cudaEventRecord(h_.ev_omega, s_));
+  const int dev = h_.device;
+  ahead_ = std::thread([this, n, os, dev, after_event] {
+    cudaSetDevice(dev);
+    ah_rc_ = p_.omega_fn(p_.omega_user, ell_, m_, ah_h_);
+    if (ah_rc_ != 0) return;
+    if (after_event) cudaStreamWaitEvent(os, h_.ev_omega, 0);
+    if (cudaMemcpyAsync(ah_d_, ah_h_, (size_t)n * 8, cudaMemcpyHostToDevice, os) != cudaSuccess ||
+        cudaStreamSynchronize(os) != cudaSuccess)
+      ah_rc_ = 1;
+  });
+}
+
+// The next rows*cols draws of the Omega stream as a device pointer ordered on
+// s_: pre-drawn ones first, the rest drawn now (stream order preserved), then
+// a new look-ahead batch.
+const double* Factor::omega_take(int64_t rows, int64_t cols) {
+  const int64_t need = rows * cols;
+  if (!ahead_.joinable() && ah_n_ == 0) {
+    draw_omega(rows, cols);
+    return om_d_;
+  }
+  if (ahead_.joinable()) ahead_.join();
+  if (ah_rc_ != 0) throw InvalidArg("Omega callback failed");
+  const int64_t have = ah_n_ - ah_pos_;
+  if (need < have) {
+    const double* p = ah_d_ + ah_pos_;
+    ah_pos_ += need;
+    return p;
+  }
+  // the rest of the batch, then fresh draws behind it
+  if (have > 0)
+    RQ_CUDA(cudaMemcpyAsync(om_d_, ah_d_ + ah_pos_, (size_t)have * 8, cudaMemcpyDeviceToDevice, s_));
+  if (need > have) {
+    const int rc = p_.omega_fn(p_.omega_user, 1, need - have, om_h_);
+    if (rc != 0) throw InvalidArg("Omega callback failed");
+    RQ_CUDA(cudaMemcpyAsync(om_d_ + have, om_h_, (size_t)(need - have) * 8, cudaMemcpyHostToDevice,
+                            s_));
+  }
+  ah_n_ = 0;
+  start_ahead(true);
+  return om_d_;
+}
+
 // make_sample(work, ell, rng) (randomized.py:69-82; truncated.py:97)
 void Factor::first_sample() {
   const double* om = p_.omega0;
@@ -115,15 +189,15 @@ void Factor::first_sample() {
 void Factor::fresh_sample(int64_t i0) {
   sync();
   const int64_t mm = m_ - i0, nt = n_ - i0;
-  draw_omega(ell_, mm);
+  const double* om = omega_take(ell_, mm);
   const double* At = p_.work + i0 + i0 * p_.ldw;
-  gemm(h_, false, false, ell_, nt, mm, 1.0, om_d_, ell_, At, p_.ldw, 0.0, B_, ell_, s_, nullptr,
+  gemm(h_, false, false, ell_, nt, mm, 1.0, om, ell_, At, p_.ldw, 0.0, B_, ell_, s_, nullptr,
        kProfSketch);
   c_.gemm_flops += 2 * ell_ * mm * nt;
   touch(c_, ell_ * mm + mm * nt + ell_ * nt);
   if (p_.truncated && i0) {
     // B -= (Omega Y[i0:, :i0]) W[i0:, :i0]^T
-    gemm(h_, false, false, ell_, i0, mm, 1.0, om_d_, ell_, p_.Y + i0, p_.ldy, 0.0, Z_, ell_, s_,
+    gemm(h_, false, false, ell_, i0, mm, 1.0, om, ell_, p_.Y + i0, p_.ldy, 0.0, Z_, ell_, s_,
          nullptr, kProfSketch);
     gemm(h_, false, true, ell_, nt, i0, -1.0, Z_, ell_, p_.W + i0, p_.ldW, 1.0, B_, ell_, s_,
          nullptr, kProfSketch);
@@ -430,11 +504,13 @@ bool Factor::slow_block(int64_t& i0, bool resampled, int64_t& rank, bool resume_
       swaps(i0, got);
     }
     Counters pc;
-    panel(i0, got, resampled ? kPanelCommitUsable : kPanelCommitIfFull, false, pc, !resume_panel);
+    panel(i0, got, resampled ? kPanelCommitUsable : kPanelCommitIfFull, false, pc,
+          !resume_panel && !near_floor_);
     resume_panel = false;
     c_.gemm_flops += pc.gemm_flops;
     c_.bytes_touched += pc.bytes_touched;
     const int64_t usable = read_status().usable;
+    if (usable < got) near_floor_ = true;
     if (usable < got && !resampled) {
       fresh_sample(i0);
       c_.resamples += 1;
@@ -455,6 +531,7 @@ bool Factor::slow_block(int64_t& i0, bool resampled, int64_t& rank, bool resume_
       Counters uc;
       update(i0, bw, false, uc);
       if (read_status().degenerate) {
+        near_floor_ = true;
         fresh_sample(i0);
         c_.resamples += 1;
       } else {
@@ -507,6 +584,7 @@ FactorResult Factor::run() {
   tol_ = kEps * frob_;
   fast_aborts_ = h_.fast_panel_spec != 2;
   first_sample();
+  start_ahead(false);
 
   const bool speculate = p_.speculate && !p_.resketch_each_block;
   if (ev_.empty()) {
@@ -521,7 +599,10 @@ FactorResult Factor::run() {
   bool stopped = false;
   while (true) {
     stream_out(pend.empty() ? i0 : pend.front().i0, false);   // committed columns
-    if (!pend.empty() && (stopped || i0 >= k_ || (int)pend.size() >= kLookahead)) {
+    // near the noise floor triggers fire block after block: queue one block
+    // ahead only, so a rewind discards fewer (early-exiting) launches
+    const int ahead = near_floor_ ? std::max(1, std::min(kLookahead, h_.floor_lookahead)) : kLookahead;
+    if (!pend.empty() && (stopped || i0 >= k_ || (int)pend.size() >= ahead)) {
       Pending e = pend.front();
       RQ_CUDA(cudaEventSynchronize(ev_[e.slot]));
       if (hring_[e.slot] != 0) {
@@ -547,6 +628,8 @@ FactorResult Factor::run() {
         next_selected = false;
         msu_ready_ = fin_ready_ = false;
         RQ_CUDA(cudaMemsetAsync(&st_->abort, 0, sizeof(int), s_));
+        if (code == kAbortDegenerate || code == kAbortPanelFast || code == kAbortPanelRank)
+          near_floor_ = true;
         if (code == kAbortDegenerate) {
           i0 = X + bwX;
           fresh_sample(i0);
@@ -584,9 +667,9 @@ FactorResult Factor::run() {
     next_selected = false;
     swaps(i0, want);
     msu_ready_ = fin_ready_ = false;
-    const bool g_ready = overlap && h_.overlap_inner && fast_aborts_ &&
+    const bool g_ready = overlap && h_.overlap_inner && fast_aborts_ && !near_floor_ &&
                          panel_overlap_inner(i0, want);
-    if (!g_ready) panel(i0, want, kPanelCommitIfFull, true, e.stage);
+    if (!g_ready) panel(i0, want, kPanelCommitIfFull, true, e.stage, !near_floor_);
     e.has_update = i0 + want < k_;
     // RQRCP: the next block's select only needs the sample update (R11, R12),
     // so it runs on a side stream on a share of the SMs while the trailing

@@ -348,7 +348,7 @@ void panel_qr(Handle& h, int64_t mm, int64_t bw, const double* P, int64_t ldp,
     Q = (int)std::min<int64_t>(kMaxGrid, (mm + 127) / 128);
     Q = std::max(Q, 1);
   } else {
-    while (Q < kMaxCluster && (int64_t)Q * 128 < mm) Q <<= 1;
+    while (Q < kMaxCluster && (int64_t)Q * h.panel_rows_per_cta < mm) Q <<= 1;
   }
   const int rpb = (int)((mm + Q - 1) / Q);
   if (rpb > kRowsPerThread * kPanThreads) throw InvalidArg("panel too tall for the kernel");

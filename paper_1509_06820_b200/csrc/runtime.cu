@@ -98,7 +98,19 @@ cudaStream_t Handle::copy_stream() {
   return copy_;
 }
 
+cudaStream_t Handle::omega_stream() {
+  if (omega_ == nullptr) {
+    RQ_CUDA(cudaStreamCreateWithFlags(&omega_, cudaStreamNonBlocking));
+    RQ_CUDA(cudaEventCreateWithFlags(&ev_omega, cudaEventDisableTiming));
+  }
+  return omega_;
+}
+
 Handle::~Handle() {
+  if (omega_ != nullptr) {
+    cudaStreamDestroy(omega_);
+    cudaEventDestroy(ev_omega);
+  }
   if (copy_ != nullptr) {
     cudaStreamDestroy(copy_);
     cudaEventDestroy(ev_copy);

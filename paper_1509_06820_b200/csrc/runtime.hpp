@@ -86,7 +86,9 @@ class Handle {
   // and the speculative driver's retire events (created once per handle)
   cudaStream_t side_stream();
   cudaStream_t copy_stream();
+  cudaStream_t omega_stream();   // uploads of pre-drawn resample Omega
   cudaEvent_t ev_copy = nullptr;
+  cudaEvent_t ev_omega = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::vector<cudaEvent_t> ring_ev;
 
@@ -96,8 +98,11 @@ class Handle {
   // (crossovers measured on B200: tools/variant_sweep.py, profiles/r01_variant_sweep.jsonl)
   int64_t select_cluster_max_cols = 1024;   // nt threshold
   int64_t panel_cluster_max_rows = 3072;    // mm threshold (bw <= 64 only)
+  int64_t panel_rows_per_cta = 128;         // cluster variant: rows per CTA (power-of-2 CTA count)
   int select_max_ctas = 0;                  // cap of the grid variant (0 = one CTA per SM)
   bool select_reg = true;                   // register-resident select (v5) where it fits
+  bool omega_ahead = true;                  // pre-draw resample Omega on a host thread
+  int floor_lookahead = 1;                  // speculative blocks queued once near the noise floor
 
   bool use_rank_update = true;
   bool fast_panel = true;   // CholeskyQR2 + Householder reconstruction panel (panel_fast.cu)
@@ -147,6 +152,7 @@ class Handle {
   cudaEvent_t trace_base_ = nullptr;
   cudaStream_t side_ = nullptr;
   cudaStream_t copy_ = nullptr;
+  cudaStream_t omega_ = nullptr;
   std::vector<cudaEvent_t> free_ev_;
   cudaEvent_t take_event();
   struct Buf {
