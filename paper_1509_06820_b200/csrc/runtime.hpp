@@ -103,6 +103,7 @@ class Handle {
   bool select_reg = true;                   // register-resident select (v5) where it fits
   bool omega_ahead = true;                  // pre-draw resample Omega on a host thread
   int floor_lookahead = 1;                  // speculative blocks queued once near the noise floor
+  bool t_inverse = true;                    // T factor as a DMMA triangular inverse (nb <= 64)
 
   bool use_rank_update = true;
   bool fast_panel = true;   // CholeskyQR2 + Householder reconstruction panel (panel_fast.cu)

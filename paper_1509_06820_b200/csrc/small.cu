@@ -413,6 +413,44 @@ __global__ void t_recurrence_kernel(const double* __restrict__ G, int64_t ldg,
       T[(e % nb) + (size_t)(e / nb) * ldt] = Tw[e];
 }
 
+// The same T as the recurrence above, as the inverse of U = striu(Y^T Y) +
+// diag(1/tau): the recurrence is exactly column-wise back substitution for
+// U^{-1} (T[:j, j] = -T[:j, :j] U[:j, j] / U[j, j], U[j, j] = 1/tau_j), so any
+// triangular inversion gives T; this one is the recursive DMMA block inverse
+// of tri.cuh (dinv = tau, no divisions).  A tau_j = 0 reflector is the
+// identity: its row and column of T are zero (the recurrence's result), so
+// index j is decoupled (unit diagonal, zero off-diagonals) and zeroed after.
+__global__ void __launch_bounds__(256, 1) t_inverse_kernel(const double* __restrict__ G, int64_t ldg,
+                                                           const double* __restrict__ tau, int nb,
+                                                           double* T, int64_t ldt,
+                                                           const Status* st) {
+  if (aborted(st)) return;
+  constexpr int kLd = 65;
+  extern __shared__ __align__(16) double tsm_inv[];
+  double* U = tsm_inv;
+  double* X = U + 64 * kLd;
+  double* Tmp = X + 64 * kLd;
+  __shared__ double dinv[64];
+  // upper_inverse joins pairs of blocks level by level: a power-of-2 size
+  const int n8 = nb <= 8 ? 8 : (nb <= 16 ? 16 : (nb <= 32 ? 32 : 64));
+  for (int e = threadIdx.x; e < n8 * n8; e += 256) {
+    const int i = e / n8, l = e - i * n8;
+    double u = 0.0;
+    if (i < l && l < nb && tau[i] != 0.0 && tau[l] != 0.0) u = G[i + (int64_t)l * ldg];
+    U[i * kLd + l] = u;
+  }
+  for (int j = threadIdx.x; j < n8; j += 256) dinv[j] = (j < nb && tau[j] != 0.0) ? tau[j] : 1.0;
+  __syncthreads();
+  upper_inverse<256>(U, dinv, X, Tmp, n8, kLd);
+  __syncthreads();
+  for (int e = threadIdx.x; e < nb * nb; e += 256) {
+    const int i = e % nb, l = e / nb;
+    double t = i <= l ? X[i * kLd + l] : 0.0;
+    if (i == l && tau[i] == 0.0) t = 0.0;
+    T[i + (int64_t)l * ldt] = t;
+  }
+}
+
 int grid_for(int64_t total, int num_sms) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 16LL * num_sms));
 }
@@ -585,6 +623,20 @@ void t_factor(Handle& h, const double* Y, int64_t ldy, int64_t mm, int64_t nb,
   if (nb <= 0) return;
   double* G = (double*)h.buf("tf_gram", (size_t)nb * nb * 8, s);
   gemm(h, true, false, nb, nb, mm, 1.0, Y, ldy, Y, ldy, 0.0, G, nb, s, st, kProfPanel);
+  if (nb <= 64 && h.t_inverse) {
+    constexpr size_t kInvSmem = 3 * 64 * 65 * 8;
+    static bool inv_attr = false;
+    if (!inv_attr) {
+      RQ_CUDA(cudaFuncSetAttribute(t_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)kInvSmem));
+      inv_attr = true;
+    }
+    ProfScope prof(h, kProfPanel, (double)nb * nb * nb / 3.0, 16.0 * nb * nb, s);
+    t_inverse_kernel<<<1, 256, kInvSmem, s>>>(G, nb, tau, (int)nb, T, ldt, st);
+    RQ_CHECK_LAUNCH();
+    count_launch();
+    return;
+  }
   const size_t smem = nb <= 128 ? ((size_t)nb * nb + nb) * 8 : (size_t)nb * 8;
   static size_t attr = 0;
   if (smem > attr) {

@@ -18,7 +18,8 @@ RQ_DEV void tile_store(double* C, int ld, const double (&acc)[2], double scale) 
   C[fr * ld + 2 * fk + 1] = scale * acc[1];
 }
 
-// X = U^{-1} for an upper triangular n8 x n8 U (row-major, stride ld; the
+// X = U^{-1} for an upper triangular n8 x n8 U, n8 in {8, 16, 32, 64} (the
+// levels join pairs of equal blocks; row-major, stride ld; the
 // padding beyond n is the identity; dinv[j] = 1 / U[j][j] for j < n8).
 // Recursive block inverse: warp w inverts diagonal block w (8 x 8, one
 // column per lane, in registers), then levels s = 8, 16, 32 join pairs of

@@ -189,3 +189,31 @@ def test_fast_panel_declines_to_exact_kernel(kind):
     for x, y in zip(a[:4], b[:4]):
         assert np.array_equal(x, y)
     assert a[4:] == b[4:]
+
+
+@pytest.mark.parametrize("nb", [1, 7, 32, 40, 64])
+def test_t_factor_inverse_matches_recurrence(nb):
+    """T as the DMMA inverse of striu(Y^T Y) + diag(1/tau) against the
+    reference recurrence (kernels.py:139-147), with tau = 0 (identity)
+    reflectors mixed in."""
+    from paper_1509_06820_b200 import _abi
+    from paper_1509_06820_b200.factorization import t_factor
+    g = np.random.default_rng(nb)
+    mm = 300
+    Y = np.tril(g.standard_normal((mm, nb)), -1)
+    Y[np.arange(nb), np.arange(nb)] = 1.0
+    tau = 2.0 / np.sum(Y * Y, axis=0)
+    if nb > 3:
+        tau[[1, nb - 2]] = 0.0
+    lib, h = _abi.load_library(), _abi.handle(0)
+    ref = port.t_factor(Y, tau)
+    got = t_factor(Y, tau)
+    lib.rq_set_option(h, b"t_inverse", 0)
+    try:
+        rec = t_factor(Y, tau)
+    finally:
+        lib.rq_set_option(h, b"t_inverse", 1)
+    scale = np.linalg.norm(ref)
+    assert np.linalg.norm(got - ref) <= 1e-13 * scale
+    assert np.linalg.norm(rec - ref) <= 1e-13 * scale
+    np.testing.assert_array_equal(got[np.tril_indices(nb, -1)], 0.0)
