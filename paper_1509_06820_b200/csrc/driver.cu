@@ -410,9 +410,14 @@ int Factor::overlap_split(int64_t i0, int64_t bw) const {
   if (nt1 <= h_.select_cluster_max_cols) return 16;   // cluster variant
   int P = h_.overlap_sel_ctas > 0 ? h_.overlap_sel_ctas : (int)(0.30 * sms + 0.5);
   if (h_.overlap_sel_ctas <= 0) {
+    // v5 (register-resident) needs <= 3 columns per 8-lane group (<= 1 for
+    // ell > 72); take the SMs for it only while that stays within 80, else
+    // the shared-memory v4 runs on the default share
     const int64_t per = ell_ <= 72 ? 3 * 64 : 64;   // v5 columns per CTA
-    P = std::max<int64_t>(P, (nt1 + per - 1) / per);
-    if (nt1 <= 72 * 64) P = std::max(P, (sms * 80) / 148);
+    const int cap = (sms * 80) / 148;
+    const int64_t need = (nt1 + per - 1) / per;
+    if (need <= cap) P = std::max<int64_t>(P, need);
+    if (nt1 <= 72 * 64) P = std::max(P, cap);
   }
   return std::max(16, std::min(P, sms - 16));
 }

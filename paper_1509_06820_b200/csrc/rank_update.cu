@@ -678,7 +678,7 @@ bool rank_update(Handle& h, int64_t M, int64_t N, int64_t K, const double* Y, in
                  const double* X, int64_t ldx, double* C, int64_t ldc, cudaStream_t s,
                  const Status* st, int cat, int max_ctas, Status* snap, const double* Csrc,
                  int64_t ldcs, int extra_rows) {
-  if (K < 4 || K > kKMax || (K % 4) != 0 || M <= 0 || N <= 0) return false;
+  if (K < 4 || (K > kKMax && K != 128) || (K % 4) != 0 || M <= 0 || N <= 0) return false;
   static bool attr = false;
   if (!attr) {
     RQ_CUDA(cudaFuncSetAttribute(rank_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -691,16 +691,32 @@ bool rank_update(Handle& h, int64_t M, int64_t N, int64_t K, const double* Y, in
             (Csrc == nullptr || al(Csrc, ldcs))) ? 1 : 0,
            snap, Csrc, ldcs, extra_rows, (unsigned)h.ru_skew_ns};
   if (Csrc != nullptr && !(a.vec16 && (K == 32 || K == 64))) return false;   // k-kernel only
+  if (K == 128 && !(h.ru_big && a.vec16 && Csrc == nullptr && extra_rows == 0 && M >= kBM))
+    return false;   // the caller's generic GEMM
   const int64_t ntiles = ((M + kTM - 1) / kTM) * ((N + kTN - 1) / kTN);
   const int cap = max_ctas > 0 ? std::min(max_ctas, h.num_sms) : h.num_sms;
   const int grid = (int)std::min<int64_t>(cap, ntiles);
   ProfScope prof(h, cat, 2.0 * M * N * K, 8.0 * ((double)M * K + (double)K * N + 2.0 * M * N), s);
-  if (h.ru_big && a.vec16 && (K == 64 || K == 32) && Csrc == nullptr && extra_rows == 0 &&
-      M >= kBM) {
+  if (h.ru_big && a.vec16 && (K == 64 || K == 32 || K == 128) && Csrc == nullptr &&
+      extra_rows == 0 && M >= kBM) {
     const int64_t tiles = ((M + kBM - 1) / kBM) * ((N + kBN - 1) / kBN);
     const int gridb = (int)std::min<int64_t>(cap, tiles);
     if (K == 64) launch_rank_update_big<64>(h, a, gridb, s);
-    else launch_rank_update_big<32>(h, a, gridb, s);
+    else if (K == 32) launch_rank_update_big<32>(h, a, gridb, s);
+    else {
+      // K = 128 (b = 128, cfg5): two K = 64 passes, C -= Y[:, :64] X[:64] then
+      // C -= Y[:, 64:] X[64:] (twice the C traffic, but the 64-deep tiles
+      // run at ~24 TF/s against ~15 for a generic 128-deep GEMM)
+      RuArgs a2 = a;
+      a2.K = 64;
+      launch_rank_update_big<64>(h, a2, gridb, s);
+      RQ_CHECK_LAUNCH();
+      count_launch();
+      a2.Y = Y + 64 * ldy;
+      a2.X = X + 64;
+      a2.snap = nullptr;
+      launch_rank_update_big<64>(h, a2, gridb, s);
+    }
   } else if (h.ru_two_ctas && a.vec16 && (K == 64 || K == 32)) {
     const int grid2 = (int)std::min<int64_t>(2 * cap, ntiles);
     if (K == 64) launch_rank_update_k2<64>(h, a, grid2, s);

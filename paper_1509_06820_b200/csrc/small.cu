@@ -451,6 +451,62 @@ __global__ void __launch_bounds__(256, 1) t_inverse_kernel(const double* __restr
   }
 }
 
+// b = 128 (cfg5) sample update prep: the degenerate verdict exactly as
+// su_prep_kernel, then the inverses of the two diagonal 64-blocks of R11 =
+// [[A, B], [0, C]] (recursive DMMA inverse, tri.cuh) into Ainv / Cinv
+// (column-major, ld 64); the caller assembles R11^{-1} and M = S11 R11^{-1}
+// with GEMMs.
+__global__ void __launch_bounds__(256, 1) su_prep_wide_kernel(const double* __restrict__ R11,
+                                                              int64_t ldr, int b, double thresh,
+                                                              double* Ainv, double* Cinv,
+                                                              int64_t ldi, Status* st,
+                                                              int abort_on_degenerate,
+                                                              int64_t i0) {
+  if (aborted(st)) return;
+  constexpr int LD = 65;
+  extern __shared__ __align__(16) double wsm[];
+  double* U = wsm;
+  double* X = U + 64 * LD;
+  double* Tm = X + 64 * LD;
+  __shared__ double dinv[64];
+  __shared__ int s_bad;
+  const int tid = threadIdx.x;
+  if (tid == 0) s_bad = 0;
+  __syncthreads();
+  for (int j = tid; j < b; j += blockDim.x)
+    if (fabs(R11[j + (size_t)j * ldr]) < thresh) s_bad = 1;
+  __syncthreads();
+  if (s_bad) {
+    if (tid == 0) {
+      st->degenerate = 1;
+      if (abort_on_degenerate) {
+        st->abort_i0 = i0;
+        __threadfence();
+        st->abort = kAbortDegenerate;
+      }
+    }
+    return;
+  }
+  if (tid == 0) st->degenerate = 0;
+  for (int half = 0; half < 2; ++half) {
+    const int o = 64 * half;
+    for (int e = tid; e < 64 * 64; e += blockDim.x) {
+      const int i = e % 64, l = e / 64;
+      U[i * LD + l] = i <= l ? R11[(o + i) + (size_t)(o + l) * ldr] : 0.0;
+    }
+    for (int j = tid; j < 64; j += blockDim.x) dinv[j] = 1.0 / R11[(o + j) + (size_t)(o + j) * ldr];
+    __syncthreads();
+    upper_inverse<256>(U, dinv, X, Tm, 64, LD);
+    __syncthreads();
+    double* dst = half ? Cinv : Ainv;
+    for (int e = tid; e < 64 * 64; e += blockDim.x) {
+      const int i = e % 64, l = e / 64;
+      dst[i + (size_t)l * ldi] = i <= l ? X[i * LD + l] : 0.0;
+    }
+    __syncthreads();
+  }
+}
+
 int grid_for(int64_t total, int num_sms) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 16LL * num_sms));
 }
@@ -497,6 +553,46 @@ void sample_update(Handle& h, int64_t ell, int64_t b, int64_t n2, const double* 
       // B_new = S[:, b:] with its top b rows then reduced by M R12; the
       // degenerate verdict (non-speculative caller) leaves B_new unused
       const Status* pred = abort_on_degenerate ? st : nullptr;
+      copy2d(S + (size_t)b * lds, lds, Bnew, ldb, ell, n2, s, pred);
+      if (!rank_update(h, b, n2, b, M, b, R12, ldr, Bnew, ldb, s, pred, kProfSampleUpd))
+        gemm(h, false, false, b, n2, b, -1.0, M, b, R12, ldr, 1.0, Bnew, ldb, s, pred,
+             kProfSampleUpd);
+    }
+    return;
+  }
+  if (h.su_gemm && b == 128) {
+    // R11^{-1} = [[A^-1, -A^-1 B C^-1], [0, C^-1]], M = S11 R11^{-1}, then
+    // B_new[:b] = S12 - M R12 as in the b <= 64 path
+    ProfScope prof(h, kProfSampleUpd, 3.0 * b * b * n2, 8.0 * (2 * ell * n2 + b * b), s);
+    double* Ri = (double*)h.buf("su_R11inv", (size_t)128 * 128 * 8, s);
+    double* W = (double*)h.buf("su_wide_tmp", (size_t)64 * 64 * 8, s);
+    double* M = (double*)h.buf("su_M", (size_t)128 * 128 * 8, s);
+    const int ab = abort_on_degenerate ? 1 : 0;
+    constexpr size_t wsm = (size_t)3 * 64 * 65 * 8;
+    static bool wattr = false;
+    if (!wattr) {
+      RQ_CUDA(cudaFuncSetAttribute(su_prep_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)wsm));
+      wattr = true;
+    }
+    double* Ri22 = Ri + 64 + (size_t)64 * 128;
+    fill2d(Ri + 64, 128, 64, 64, 0.0, s, st);   // the zero block below A^-1
+    su_prep_wide_kernel<<<1, 256, wsm, s>>>(R11, ldr, 128, kEps34 * frob, Ri, Ri22, 128, st, ab,
+                                            i0);
+    RQ_CHECK_LAUNCH();
+    count_launch();
+    // the Status predicate skips the rest after a degenerate verdict (the
+    // non-speculative caller reads Status.degenerate and discards B_new)
+    const Status* pred = st;
+    // X12 = -A^-1 (B C^-1):  W = B C^-1, Ri12 = -A^-1 W
+    double* Ri12 = Ri + (size_t)64 * 128;
+    gemm(h, false, false, 64, 64, 64, 1.0, R11 + (size_t)64 * ldr, ldr, Ri22, 128, 0.0, W, 64, s,
+         pred, kProfSampleUpd);
+    gemm(h, false, false, 64, 64, 64, -1.0, Ri, 128, W, 64, 0.0, Ri12, 128, s, pred,
+         kProfSampleUpd);
+    gemm(h, false, false, 128, 128, 128, 1.0, S, lds, Ri, 128, 0.0, M, 128, s, pred,
+         kProfSampleUpd);
+    if (n2 > 0) {
       copy2d(S + (size_t)b * lds, lds, Bnew, ldb, ell, n2, s, pred);
       if (!rank_update(h, b, n2, b, M, b, R12, ldr, Bnew, ldb, s, pred, kProfSampleUpd))
         gemm(h, false, false, b, n2, b, -1.0, M, b, R12, ldr, 1.0, Bnew, ldb, s, pred,

@@ -115,10 +115,11 @@ def test_panel_large_vs_oracle(mm, bw):
     np.testing.assert_allclose(T.cpu().numpy(), port.t_factor(Yo, to), rtol=1e-10, atol=1e-13)
 
 
-def test_sample_update_vs_oracle():
+@pytest.mark.parametrize("b", [64, 128])
+def test_sample_update_vs_oracle(b):
     from paper_1509_06820_b200.primitives import sample_update
     g = np.random.default_rng(3)
-    ell, b, nt = 72, 64, 700
+    ell, nt = b + 8, 700
     B = g.standard_normal((ell, nt))
     smp = port.Sample(B=np.asfortranarray(B.copy()), ell=ell, frob_a=10.0)
     port.pick_pivots(smp, b, port.Counters())
