@@ -97,6 +97,7 @@ class Factor {
   void stages(int64_t i0, int64_t bw, Counters& c, bool defer_trailing = false,
               bool g_ready = false);
   bool panel_overlap_inner(int64_t i0, int64_t bw);
+  bool panel_halves(int64_t i0, int64_t got);
   bool msu_ready_ = false;   // the fast panel left the sample update's M in "su_Mpre"
   bool fin_ready_ = false;   // ... and A1 = Y1 T, A2 = M T in "fin_A12": block_finish() path
   void trailing(int64_t i0, int64_t bw, int max_ctas, const Status* pred);
@@ -222,9 +223,64 @@ void Factor::swaps(int64_t i0, int64_t got) {
   apply_swaps(h_, piv_, got, i0, t, st_, s_);
 }
 
+// A 65..128-column speculative panel as two fast 64-column halves (the
+// recursive panel QR): Householder QR is column-sequential, so the first 64
+// reflectors come from the first 64 columns alone; they are applied to the
+// other columns (G = Y1^T P2, P2 -= Y1 T1^T G), whose rows below 64 are then
+// factored, and T = [[T1, -T1 (Y1^T Y2) T2], [0, T2]].  Each half commits
+// only under the fast panel's margins (else Status.abort rewinds the block
+// to the exact kernel), so a commit means every |R_jj| cleared _panel_rank.
+bool Factor::panel_halves(int64_t i0, int64_t got) {
+  const int64_t mm = m_ - i0, h2 = got - 64;
+  if (p_.truncated || got <= 64 || got > 128 || mm < got + 64 || !h_.panel_halves ||
+      !panel_fast_eligible(h_, mm, 64) || !panel_fast_eligible(h_, mm - 64, h2))
+    return false;
+  double* P1 = p_.work + i0 + i0 * p_.ldw;
+  double* P2 = P1 + 64 * p_.ldw;
+  double* Y1 = p_.Y + i0 + i0 * p_.ldy;
+  double* Y2 = Y1 + 64 + 64 * p_.ldy;
+  double* G = (double*)h_.buf("ph_G", (size_t)64 * 128 * 8, s_);
+  double* X = G + 64 * 64;
+  PanelOut o1{};
+  o1.Y = Y1; o1.ldy = p_.ldy; o1.tau = p_.tau + i0;
+  o1.T = T_; o1.ldt = b_;
+  o1.Rdst = P1; o1.ldr = p_.ldw; o1.rrows = mm;
+  panel_fast(h_, mm, 64, P1, p_.ldw, o1, tol_, st_, s_, true, i0);
+  // P2 <- H_64 ... H_1 P2 = P2 - Y1 (T1^T (Y1^T P2))
+  if (!inner_gemm(h_, 64, h2, mm, Y1, p_.ldy, P2, p_.ldw, G, 64, s_, st_, 0, kProfPanel))
+    gemm(h_, true, false, 64, h2, mm, 1.0, Y1, p_.ldy, P2, p_.ldw, 0.0, G, 64, s_, st_,
+         kProfPanel);
+  gemm(h_, true, false, 64, h2, 64, 1.0, T_, b_, G, 64, 0.0, X, 64, s_, st_, kProfPanel);
+  if (!rank_update(h_, mm, h2, 64, Y1, p_.ldy, X, 64, P2, p_.ldw, s_, st_, kProfPanel))
+    gemm(h_, false, false, mm, h2, 64, -1.0, Y1, p_.ldy, X, 64, 1.0, P2, p_.ldw, s_, st_,
+         kProfPanel);
+  // rows 64.. of the updated columns; the level-2 count of the reference's
+  // column-by-column panel includes reflectors 1..64 applied to them
+  int64_t l2x = 0;
+  for (int64_t j = 0; j < 64; ++j) l2x += (mm - j) * h2;
+  PanelOut o2{};
+  o2.Y = Y2; o2.ldy = p_.ldy; o2.tau = p_.tau + i0 + 64;
+  o2.T = T_ + 64 + 64 * b_; o2.ldt = b_;
+  o2.Rdst = P2 + 64; o2.ldr = p_.ldw; o2.rrows = mm - 64;
+  panel_fast(h_, mm - 64, h2, P2 + 64, p_.ldw, o2, tol_, st_, s_, true, i0, 0, false, nullptr,
+             nullptr, nullptr, 0, nullptr, nullptr, l2x, (int)got);
+  // T12 = -T1 (Y1[64:]^T Y2[64:]) T2, T21 = 0
+  if (!inner_gemm(h_, 64, h2, mm - 64, Y1 + 64, p_.ldy, Y2, p_.ldy, G, 64, s_, st_, 0,
+                  kProfPanel))
+    gemm(h_, true, false, 64, h2, mm - 64, 1.0, Y1 + 64, p_.ldy, Y2, p_.ldy, 0.0, G, 64, s_, st_,
+         kProfPanel);
+  gemm(h_, false, false, 64, h2, h2, 1.0, G, 64, T_ + 64 + 64 * b_, b_, 0.0, X, 64, s_, st_,
+       kProfPanel);
+  gemm(h_, false, false, 64, h2, 64, -1.0, T_, b_, X, 64, 0.0, T_ + 64 * b_, b_, s_, st_,
+       kProfPanel);
+  fill2d(T_ + 64, b_, h2, 64, 0.0, s_, st_);
+  return true;
+}
+
 void Factor::panel(int64_t i0, int64_t got, PanelPolicy pol, bool spec, Counters& c,
                    bool allow_fast) {
   const int64_t mm = m_ - i0;
+  if (spec && allow_fast && fast_aborts_ && panel_halves(i0, got)) return;
   PanelOut o{};
   o.Y = p_.Y + i0 + i0 * p_.ldy; o.ldy = p_.ldy;
   o.tau = p_.tau + i0;

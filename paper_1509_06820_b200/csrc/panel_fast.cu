@@ -58,6 +58,8 @@ struct FastArgs {
   const double* S11; int64_t lds11; // optional: sample block for the sample update's M
   double* msu;                      // out (if S11): M = S11 R11^{-1}, b x b column-major
   double* a12;                      // out (if T): A1 = Y1 T, A2 = M T, b x b column-major each
+  int64_t l2_extra;                 // extra level-2 count on commit (second half of a wider panel)
+  int usable_total;                 // Status.usable on commit (0: the panel width)
   int64_t i0;
   int64_t nchunks;
   Status* st;
@@ -611,9 +613,9 @@ __global__ void __launch_bounds__(kFT, 1) panel_fast_kernel(FastArgs a) {
       if (!s_fail) {
         // _panel_rank: every column usable; level-2 counters of the
         // column-by-column reflections this path replaces
-        int64_t l2 = 0;
+        int64_t l2 = a.l2_extra;
         for (int j = 0; j + 1 < n; ++j) l2 += (a.mm - j) * (int64_t)(n - j - 1);
-        a.st->usable = n;
+        a.st->usable = a.usable_total > 0 ? a.usable_total : n;
         a.st->level2 += 4 * l2;
         a.st->l2bytes += 16 * l2;
       }
@@ -660,7 +662,8 @@ const int* panel_fast(Handle& h, int64_t mm, int64_t bw, const double* P, int64_
                       const PanelOut& out, double tol, Status* st, cudaStream_t s,
                       bool abort_on_decline, int64_t i0, int max_ctas, bool defer_zero,
                       const double** m_rowmajor, int64_t* m_ld, const double* S11,
-                      int64_t lds11, double* msu, double* a12) {
+                      int64_t lds11, double* msu, double* a12, int64_t l2_extra,
+                      int usable_total) {
   if (!panel_fast_eligible(h, mm, bw)) return nullptr;
   const int n8 = (int)((bw + 7) / 8 * 8);
   const int ld = n8 + 1;
@@ -684,6 +687,8 @@ const int* panel_fast(Handle& h, int64_t mm, int64_t bw, const double* P, int64_
   a.defer_zero = defer_zero ? 1 : 0;
   a.S11 = S11; a.lds11 = lds11; a.msu = S11 != nullptr ? msu : nullptr;
   a.a12 = out.T != nullptr ? a12 : nullptr;
+  a.l2_extra = l2_extra;
+  a.usable_total = usable_total;
   a.i0 = i0;
   a.bar = (unsigned int*)h.buf("pf_bar", 64, s);
   static void* zeroed = nullptr;

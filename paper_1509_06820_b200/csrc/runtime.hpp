@@ -104,6 +104,7 @@ class Handle {
   bool omega_ahead = true;                  // pre-draw resample Omega on a host thread
   int floor_lookahead = 1;                  // speculative blocks queued once near the noise floor
   bool t_inverse = true;                    // T factor as a DMMA triangular inverse (nb <= 64)
+  bool panel_halves = true;                 // 65..128-wide speculative panels as two fast halves
 
   bool use_rank_update = true;
   bool fast_panel = true;   // CholeskyQR2 + Householder reconstruction panel (panel_fast.cu)
@@ -222,7 +223,8 @@ const int* panel_fast(Handle& h, int64_t mm, int64_t bw, const double* P, int64_
                       bool abort_on_decline = false, int64_t i0 = 0, int max_ctas = 0,
                       bool defer_zero = false, const double** m_rowmajor = nullptr,
                       int64_t* m_ld = nullptr, const double* S11 = nullptr,
-                      int64_t lds11 = 0, double* msu = nullptr, double* a12 = nullptr);
+                      int64_t lds11 = 0, double* msu = nullptr, double* a12 = nullptr,
+                      int64_t l2_extra = 0, int usable_total = 0);
 
 // Rest of a speculative RQRCP block after a committed fast panel, one CTA per
 // 64-column tile of the trailing matrix (csrc/finish.cu):
