@@ -15,7 +15,7 @@ int64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 ProfScope::ProfScope(Handle& h, int cat, double flops, double bytes, cudaStream_t s)
     : h_(&h), s_(s) {
-  if (h.profiling) idx_ = h.prof_begin(cat, flops, bytes, s);
+  if (h.profiling && cat >= 0) idx_ = h.prof_begin(cat, flops, bytes, s);   // cat < 0: untimed
 }
 ProfScope::~ProfScope() {
   if (idx_ >= 0) h_->prof_end(idx_, s_);

@@ -15,7 +15,7 @@ import bench
 import paper_1509_06820_b200 as P
 from paper_1509_06820_b200 import _abi
 
-cfg = bench.CONFIGS["cfg2"]
+cfg = bench.CONFIGS[os.environ.get("CFG", "cfg2")]
 dev = torch.device("cuda", 0)
 A = bench.device_matrix(cfg["kind"], cfg["m"], cfg["n"], dev, seed=0)
 lib, h = _abi.load_library(), _abi.handle(0)
