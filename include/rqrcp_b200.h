@@ -84,6 +84,14 @@ typedef struct {
   int64_t ldhY;
   double* host_R;
   int64_t ldhR;
+  /* optional native Omega stream: when omega_native = 1 the (re)sample draws
+   * come from rq_omega_fill on the caller's Philox key (omega_k0, omega_k1)
+   * from raw counter omega_raw, on omega_threads host threads, instead of
+   * omega_fn -- no callback into the caller, so they can be drawn ahead on a
+   * host thread while the factorization runs */
+  int32_t omega_native;
+  int32_t omega_threads;
+  uint64_t omega_k0, omega_k1, omega_raw;
 } rq_factor_args;
 
 typedef struct {

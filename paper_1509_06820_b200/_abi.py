@@ -30,6 +30,8 @@ class FactorArgs(C.Structure):
         ("perm", lp), ("swaps", lp), ("swap_cap", i64),
         ("omega0", dp), ("omega_fn", OMEGA_FN), ("omega_user", vp), ("stream", vp),
         ("host_Y", dp), ("ldhY", i64), ("host_R", dp), ("ldhR", i64),
+        ("omega_native", C.c_int32), ("omega_threads", C.c_int32),
+        ("omega_k0", C.c_uint64), ("omega_k1", C.c_uint64), ("omega_raw", C.c_uint64),
     ]
 
 

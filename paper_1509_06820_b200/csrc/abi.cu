@@ -69,6 +69,9 @@ rq::FactorParams to_params(const rq_factor_args& a) {
   p.stream = S(a.stream);
   p.host_Y = a.host_Y; p.ldhY = a.ldhY;
   p.host_R = a.host_R; p.ldhR = a.ldhR;
+  p.omega_native = a.omega_native != 0;
+  p.omega_threads = a.omega_threads;
+  p.omega_k0 = a.omega_k0; p.omega_k1 = a.omega_k1; p.omega_raw = a.omega_raw;
   return p;
 }
 

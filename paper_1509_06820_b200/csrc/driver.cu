@@ -22,6 +22,9 @@
 
 #include "driver.hpp"
 
+extern "C" int rq_omega_fill(uint64_t k0, uint64_t k1, uint64_t raw, double* out, int64_t count,
+                             int threads, uint64_t* raw_end);
+
 namespace rq {
 
 namespace {
@@ -77,6 +80,19 @@ class Factor {
   int64_t ah_n_ = 0, ah_pos_ = 0;
   int ah_rc_ = 0;
   void start_ahead(bool after_event);
+  uint64_t om_raw_ = 0;   // native stream: raw Philox counter after the draws so far
+  bool has_omega() const { return p_.omega_native || p_.omega_fn != nullptr; }
+  // the next `count` draws of the Omega stream into host memory
+  int draw_host(int64_t count, double* dst) {
+    if (p_.omega_native) {
+      uint64_t end = 0;
+      const int rc = rq_omega_fill(p_.omega_k0, p_.omega_k1, om_raw_, dst, count,
+                                   std::max(1, p_.omega_threads), &end);
+      if (rc == 0) om_raw_ = end;
+      return rc;
+    }
+    return p_.omega_fn(p_.omega_user, 1, count, dst);
+  }
   const double* omega_take(int64_t rows, int64_t cols);
 
   void sync() { RQ_CUDA(cudaStreamSynchronize(s_)); }
@@ -110,10 +126,10 @@ class Factor {
 };
 
 void Factor::draw_omega(int64_t rows, int64_t cols) {
-  if (p_.omega_fn == nullptr) throw InvalidArg("no Omega source for a (re)sample");
+  if (!has_omega()) throw InvalidArg("no Omega source for a (re)sample");
   // the pinned staging buffer is reused: every caller has synchronised the
   // stream, so no earlier H2D copy is still reading it
-  const int rc = p_.omega_fn(p_.omega_user, rows, cols, om_h_);
+  const int rc = draw_host(rows * cols, om_h_);
   if (rc != 0) throw InvalidArg("Omega callback failed");
   RQ_CUDA(cudaMemcpyAsync(om_d_, om_h_, (size_t)rows * cols * 8, cudaMemcpyHostToDevice, s_));
 }
@@ -121,7 +137,9 @@ void Factor::draw_omega(int64_t rows, int64_t cols) {
 // after_event: the device copy is still being read by work enqueued on s_
 // (h_.ev_omega recorded there), so the upload waits for it
 void Factor::start_ahead(bool after_event) {
-  if (p_.omega_fn == nullptr || !h_.omega_ahead) return;
+  // the look-ahead thread draws natively only: a callback into the caller
+  // (Python) from a second thread could wait on the caller's lock
+  if (!p_.omega_native || !h_.omega_ahead) return;
   const int64_t n = ell_ * m_;
   ah_h_ = (double*)h_.host_pinned("omega_ahead_h", (size_t)n * 8, s_);
   ah_d_ = (double*)h_.buf("omega_ahead_d", (size_t)n * 8, s_);
@@ -133,7 +151,7 @@ void Factor::start_ahead(bool after_event) {
   const int dev = h_.device;
   ahead_ = std::thread([this, n, os, dev, after_event] {
     cudaSetDevice(dev);
-    ah_rc_ = p_.omega_fn(p_.omega_user, ell_, m_, ah_h_);
+    ah_rc_ = draw_host(n, ah_h_);
     if (ah_rc_ != 0) return;
     if (after_event) cudaStreamWaitEvent(os, h_.ev_omega, 0);
     if (cudaMemcpyAsync(ah_d_, ah_h_, (size_t)n * 8, cudaMemcpyHostToDevice, os) != cudaSuccess ||
@@ -163,7 +181,7 @@ const double* Factor::omega_take(int64_t rows, int64_t cols) {
   if (have > 0)
     RQ_CUDA(cudaMemcpyAsync(om_d_, ah_d_ + ah_pos_, (size_t)have * 8, cudaMemcpyDeviceToDevice, s_));
   if (need > have) {
-    const int rc = p_.omega_fn(p_.omega_user, 1, need - have, om_h_);
+    const int rc = draw_host(need - have, om_h_);
     if (rc != 0) throw InvalidArg("Omega callback failed");
     RQ_CUDA(cudaMemcpyAsync(om_d_ + have, om_h_, (size_t)(need - have) * 8, cudaMemcpyHostToDevice,
                             s_));
@@ -606,6 +624,7 @@ bool Factor::slow_block(int64_t& i0, bool resampled, int64_t& rank, bool resume_
 
 FactorResult Factor::run() {
   m_ = p_.m; n_ = p_.n; k_ = p_.k; b_ = p_.block; ell_ = p_.ell;
+  om_raw_ = p_.omega_raw;
   if (k_ < 1 || k_ > std::min(m_, n_)) throw InvalidArg("rank outside [1, min(m, n)]");
   if (ell_ > m_) throw InvalidArg("sample rows exceed matrix rows");
   if (b_ < 1 || b_ > 256) throw InvalidArg("block must be in [1, 256]");

@@ -34,6 +34,9 @@ struct FactorParams {
   cudaStream_t stream = nullptr;
   double* host_Y = nullptr; int64_t ldhY = 0;   // optional pinned outputs streamed as blocks commit
   double* host_R = nullptr; int64_t ldhR = 0;
+  bool omega_native = false;                  // draw with rq_omega_fill (key, raw) instead of omega_fn
+  int omega_threads = 1;
+  uint64_t omega_k0 = 0, omega_k1 = 0, omega_raw = 0;
 };
 
 struct FactorResult {

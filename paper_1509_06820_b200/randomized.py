@@ -73,6 +73,16 @@ class _OmegaSource:
 
         self.fn = _abi.OMEGA_FN(fill)
 
+    def native(self):
+        """FactorArgs fields that let the library draw this stream itself
+        (rq_omega_fill on the same Philox key and raw counter: the same
+        values as ``fill``), so resample draws can be made ahead on a host
+        thread without calling back into Python.  The RngState is not
+        advanced (each factorization owns a fresh one)."""
+        from .rng import THREADS
+        return dict(omega_native=1, omega_threads=THREADS, omega_k0=self.rng._k0,
+                    omega_k1=self.rng._k1, omega_raw=self.rng._raw)
+
 
 def _shape_of(A):
     if torch.is_tensor(A):
@@ -126,7 +136,7 @@ def run_native(A, k, config, *, variant, ell, width, omega=None, speculate=True,
         work=ptr(work), ldw=ld(work), Y=ptr(Y), ldy=ld(Y), tau=ptr(tau),
         W=ptr(W), ldW=ld(W) if W is not None else 0, R=ptr(R), ldR=ld(R) if R is not None else 0,
         perm=ptr(perm), swaps=ptr(swaps), swap_cap=cap, omega0=ptr(om), omega_fn=src.fn,
-        omega_user=None, stream=stream_ptr(dev),
+        **src.native(), omega_user=None, stream=stream_ptr(dev),
         host_Y=hY.data_ptr() if hY is not None else None, ldhY=m,
         host_R=hR.data_ptr() if hR is not None else None, ldhR=k)
     res = _abi.FactorResult()

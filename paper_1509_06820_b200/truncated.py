@@ -120,7 +120,7 @@ def tuxv(A, k, config=None, j_max=1, svd_of_x=False, omega=None):
         m=m, n=n, k=k, block=config.block, ell=config.ell, variant=_abi.RQ_TRQRCP, speculate=1,
         work=ptr(work), ldw=ld(work), Y=ptr(Y), ldy=ld(Y), tau=ptr(tau), W=ptr(W), ldW=ld(W),
         R=ptr(R), ldR=ld(R), perm=ptr(perm), swaps=ptr(swaps), swap_cap=cap, omega0=ptr(om),
-        omega_fn=src.fn, omega_user=None, stream=stream_ptr(dev))
+        omega_fn=src.fn, **src.native(), omega_user=None, stream=stream_ptr(dev))
     ta = _abi.TuxvArgs(f=fa, A=ptr(Ad), lda=ld(Ad), j_max=j_max, U=ptr(U), ldu=ld(U), V=ptr(V),
                        ldv=ld(V), X=ptr(X), ldx=ld(X))
     res = _abi.TuxvResult()
