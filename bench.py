@@ -371,7 +371,7 @@ def main():
         i = _abi.PROF_NAMES.index(dom)
         ach = FL[i] / (MS[i] * 1e-3) / 1e12
         pk = peak["dmma_f64_tflops"] if peak else 37.2
-        kname = {"update": "rank_update_k_kernel<b> (C -= Y X, K = b, persistent)",
+        kname = {"update": "rank_update_big_kernel<b> (C -= Y X, K = b, persistent 128x64 tiles)",
                  "inner": "gemm_f64_kernel (G = Y^T C, split-K)",
                  "sketch": "gemm_f64_kernel (B = Omega A)",
                  "small_gemm": "gemm_f64_kernel (small products)"}.get(dom, dom)

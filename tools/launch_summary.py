@@ -13,12 +13,14 @@ note = sys.argv[3] if len(sys.argv) > 3 else src
 rows = [r for r in csv.reader(open(src)) if len(r) > 10]
 hdr = rows[0]
 iname, im, iv, iu = (hdr.index(k) for k in ("Kernel Name", "Metric Name", "Metric Value", "Metric Unit"))
-scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}
+scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3,
+         "second": 1e6, "s": 1e6}
 agg = collections.defaultdict(lambda: [0, 0.0])
 for r in rows[1:]:
     if r[im] != "gpu__time_duration.sum":
         continue
     name = re.sub(r"\(.*$", "", r[iname]).replace("rq::(anonymous namespace)::", "")
+    name = name.replace("unnamed>::", "")
     name = re.sub(r"^void ", "", name)
     us = float(r[iv].replace(",", "")) * scale.get(r[iu], 1.0)
     agg[name][0] += 1

@@ -7,7 +7,8 @@ rows = [r for r in csv.reader(open(src)) if len(r) > 10]
 hdr = rows[0]
 iid, iname, im, iv, iu = (hdr.index(k) for k in ("ID", "Kernel Name", "Metric Name", "Metric Value", "Metric Unit"))
 per = collections.defaultdict(dict)
-scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3}
+scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
+         "msecond": 1e-3, "ns": 1e-9, "us": 1e-6, "ms": 1e-3}
 for r in rows[1:]:
     per[r[iid]][r[im]] = float(r[iv].replace(",", "")) * scale.get(r[iu], 1)
     per[r[iid]]["name"] = r[iname]
