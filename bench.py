@@ -140,7 +140,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "20"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -295,6 +295,10 @@ def main():
     torch.cuda.synchronize(dev)
     lib = _abi.load_library()
     h = _abi.handle(local)
+    # diagnostics: RQ_OPTIONS="name=value,..." sets library options (rq_set_option)
+    for kv in filter(None, os.environ.get("RQ_OPTIONS", "").split(",")):
+        k, v = kv.split("=")
+        _abi.check(lib.rq_set_option(h, k.strip().encode(), int(v)))
 
     sharded = world > 1 or args.force_sharded
     if sharded:

@@ -284,6 +284,7 @@ int rq_set_option(rq_handle_t h, const char* name, int64_t value) {
     else if (n == "ru_big") hh.ru_big = value != 0;
     else if (n == "inner_kernel") hh.inner_kernel = value != 0;
     else if (n == "inner_ktiles") hh.inner_ktiles = (int)value;
+    else if (n == "inner32") hh.inner32 = value != 0;
     else if (n == "gemm_vec16") hh.gemm_vec16 = value != 0;
     else if (n == "debug_timers") {
       hh.dbg = value ? (long long*)hh.buf("dbg_timers", 64 * 8, nullptr) : nullptr;

@@ -353,7 +353,8 @@ void Factor::stages(int64_t i0, int64_t bw, Counters& c, bool defer_trailing, bo
       }
       return;
     }
-    if (!g_ready)   // else panel_overlap_inner() assembled G = Y^T C
+    if (!g_ready &&   // else panel_overlap_inner() assembled G = Y^T C
+        !inner_gemm(h_, bw, nt2, mm, Yb, p_.ldy, C, p_.ldw, G_, bw, s_, st_, 0, kProfInner))
       gemm(h_, true, false, bw, nt2, mm, 1.0, Yb, p_.ldy, C, p_.ldw, 0.0, G_, bw, s_, st_,
            kProfInner);
     gemm(h_, true, false, bw, nt2, bw, 1.0, T_, b_, G_, bw, 0.0, X_, bw, s_, st_);
@@ -382,11 +383,15 @@ void Factor::stages(int64_t i0, int64_t bw, Counters& c, bool defer_trailing, bo
     return;
   }
   // G = Yb^T A[i0:, i0+bw:] - (Yb^T Y[i0:, :i0]) W[i0+bw:, :i0]^T
-  gemm(h_, true, false, bw, nt2, mm, 1.0, Yb, p_.ldy, p_.work + i0 + (i0 + bw) * p_.ldw, p_.ldw,
-       0.0, G_, bw, s_, st_, kProfInner);
+  if (!inner_gemm(h_, bw, nt2, mm, Yb, p_.ldy, p_.work + i0 + (i0 + bw) * p_.ldw, p_.ldw, G_, bw,
+                  s_, st_, 0, kProfInner))
+    gemm(h_, true, false, bw, nt2, mm, 1.0, Yb, p_.ldy, p_.work + i0 + (i0 + bw) * p_.ldw, p_.ldw,
+         0.0, G_, bw, s_, st_, kProfInner);
   c.gemm_flops += 2 * mm * bw * nt2;
   if (i0) {
-    gemm(h_, true, false, bw, i0, mm, 1.0, Yb, p_.ldy, p_.Y + i0, p_.ldy, 0.0, Z_, bw, s_, st_);
+    if (!inner_gemm(h_, bw, i0, mm, Yb, p_.ldy, p_.Y + i0, p_.ldy, Z_, bw, s_, st_, 0,
+                    kProfSmallGemm))
+      gemm(h_, true, false, bw, i0, mm, 1.0, Yb, p_.ldy, p_.Y + i0, p_.ldy, 0.0, Z_, bw, s_, st_);
     gemm(h_, false, true, bw, nt2, i0, -1.0, Z_, bw, p_.W + i0 + bw, p_.ldW, 1.0, G_, bw, s_, st_);
     c.gemm_flops += 2 * mm * bw * i0 + 2 * bw * i0 * nt2;
   }
@@ -819,7 +824,8 @@ void qr_blocked(Handle& h, int64_t m, int64_t n, int64_t k, int64_t b, double* w
       // apply_block_reflection(transpose=True) (kernels.py:166-181)
       double* C = work + i0 + (i0 + bw) * ldw;
       const double* Yb = Y + i0 + i0 * ldy;
-      gemm(h, true, false, bw, nc, mm, 1.0, Yb, ldy, C, ldw, 0.0, G, bw, s);
+      if (!inner_gemm(h, bw, nc, mm, Yb, ldy, C, ldw, G, bw, s, nullptr, 0, kProfInner))
+        gemm(h, true, false, bw, nc, mm, 1.0, Yb, ldy, C, ldw, 0.0, G, bw, s);
       gemm(h, true, false, bw, nc, bw, 1.0, T, b, G, bw, 0.0, X, bw, s);
       gemm(h, false, false, mm, nc, bw, -1.0, Yb, ldy, X, bw, 1.0, C, ldw, s);
       if (c) {
@@ -852,7 +858,8 @@ void q_columns(Handle& h, int64_t m, int64_t nref, int64_t cols, const double* Y
     const double* Yb = Y + i0 + i0 * ldy;
     t_factor(h, Yb, ldy, mm, bw, tau + i0, T, b, s);
     double* C = Q + i0 + i0 * ldq;
-    gemm(h, true, false, bw, nc, mm, 1.0, Yb, ldy, C, ldq, 0.0, G, bw, s);
+    if (!inner_gemm(h, bw, nc, mm, Yb, ldy, C, ldq, G, bw, s, nullptr, 0, kProfInner))
+      gemm(h, true, false, bw, nc, mm, 1.0, Yb, ldy, C, ldq, 0.0, G, bw, s);
     gemm(h, false, false, bw, nc, bw, 1.0, T, b, G, bw, 0.0, X, bw, s);
     gemm(h, false, false, mm, nc, bw, -1.0, Yb, ldy, X, bw, 1.0, C, ldq, s);
   }

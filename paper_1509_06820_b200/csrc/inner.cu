@@ -14,11 +14,16 @@ namespace rq {
 
 namespace {
 
-constexpr int kIT = 256;               // 8 warps: 2 (m) x 4 (n)
-constexpr int kIM = 64, kIN = 128, kIK = 32, kIS = 4;
+// IM = 64: 8 warps, 2 (m) x 4 (n); IM = 32 (b = 32, cfg4): 4 warps, 1 x 4
+template <int IM> struct InnerCfg {
+  static constexpr int kIT = IM == 64 ? 256 : 128;
+  static constexpr int kWM = IM / 32;   // warps along m
+};
+constexpr int kIN = 128, kIK = 32, kIS = 4;
 constexpr int kILd = kIK + 4;          // As[m][k], Bs[n][k]
-constexpr int kIStA = kIM * kILd, kIStB = kIN * kILd;
-constexpr size_t kISmem = (size_t)kIS * (kIStA + kIStB) * sizeof(double);
+constexpr int kIStB = kIN * kILd;
+template <int IM>
+constexpr size_t inner_smem() { return (size_t)kIS * (IM * kILd + kIStB) * sizeof(double); }
 
 struct InnerArgs {
   int64_t N, K;
@@ -34,13 +39,16 @@ struct InnerArgs {
 // Not persistent: beside the fast panel the hardware scheduler moves the
 // remaining CTAs onto the panel's SMs once it ends (a persistent grid sized
 // to the free SMs measured slower in the driver for that reason).
-__global__ void __launch_bounds__(kIT, 1) inner_kernel(InnerArgs a) {
+template <int IM>
+__global__ void __launch_bounds__(InnerCfg<IM>::kIT, 1) inner_kernel(InnerArgs a) {
+  constexpr int kIM = IM, kIT = InnerCfg<IM>::kIT, kWM = InnerCfg<IM>::kWM;
+  constexpr int kIStA = kIM * kILd;
   if (aborted(a.st)) return;
   extern __shared__ __align__(16) double sm[];
   double* As = sm;                   // [kIS][kIM][kILd]
   double* Bs = As + kIS * kIStA;     // [kIS][kIN][kILd]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm0 = (warp & 1) * 32, wn0 = (warp >> 1) * 32;
+  const int wm0 = (warp % kWM) * 32, wn0 = (warp / kWM) * 32;
   const int fr = lane >> 2, fk = lane & 3;
   const int j = blockIdx.x % a.tn, z = blockIdx.x / a.tn;
   const int64_t N = a.N, ldp = a.ldp, ldc = a.ldc, n0 = (int64_t)j * kIN;
@@ -122,12 +130,15 @@ bool inner_gemm(Handle& h, int64_t M, int64_t N, int64_t K, const double* P, int
                 const double* C, int64_t ldc, double* H, int64_t ldh, cudaStream_t s,
                 const Status* st, int max_ctas, int cat) {
   (void)max_ctas;
-  if (!h.inner_kernel || M != kIM || N <= 0 || K < 4096) return false;
+  if (!h.inner_kernel || (M != 64 && M != 32) || N <= 0 || K < 4096) return false;
+  if (M == 32 && !h.inner32) return false;
   if (((uintptr_t)P & 15) || (ldp & 1) || ((uintptr_t)C & 15) || (ldc & 1)) return false;
   static bool attr = false;
   if (!attr) {
-    RQ_CUDA(cudaFuncSetAttribute(inner_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)kISmem));
+    RQ_CUDA(cudaFuncSetAttribute(inner_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)inner_smem<64>()));
+    RQ_CUDA(cudaFuncSetAttribute(inner_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)inner_smem<32>()));
     attr = true;
   }
   const int64_t tn = (N + kIN - 1) / kIN;
@@ -147,7 +158,10 @@ bool inner_gemm(Handle& h, int64_t M, int64_t N, int64_t K, const double* P, int
     g.C = H; g.ldc = ldh; g.alpha = 1.0; g.beta = 0.0;
     g.splits = (int)spl; g.partial = a.out; g.st = st;
   }
-  inner_kernel<<<(unsigned)(tn * spl), kIT, kISmem, s>>>(a);
+  if (M == 64)
+    inner_kernel<64><<<(unsigned)(tn * spl), InnerCfg<64>::kIT, inner_smem<64>(), s>>>(a);
+  else
+    inner_kernel<32><<<(unsigned)(tn * spl), InnerCfg<32>::kIT, inner_smem<32>(), s>>>(a);
   RQ_CHECK_LAUNCH();
   count_launch();
   if (spl > 1) {

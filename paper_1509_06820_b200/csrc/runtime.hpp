@@ -125,6 +125,7 @@ class Handle {
   bool ru_big = true;        // rank update: 128 x 64 tiles, C through registers
   bool inner_kernel = true;  // H = P^T C: tall-skinny split-K kernel (csrc/inner.cu)
   int inner_ktiles = 16;     // ... k-tiles (32 deep) per CTA
+  bool inner32 = true;       // ... also for 32-row blocks (b = 32)
   int overlap_sel_ctas = 0;   // SMs for the overlapped select (0 = size heuristic)
   bool gemm_vec16 = true;
   long long* dbg = nullptr;  // optional device phase-timer buffer (debug)
