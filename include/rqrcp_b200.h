@@ -181,6 +181,12 @@ int rq_q_columns(rq_handle_t h, int64_t m, int64_t nref, int64_t cols, const dou
                  void* stream);
 
 /* ||A||_F into a device scalar */
+/* column_norms (kernels.py:184-186; qrcp.py:258 qr_presorted): out[j] =
+ * ||A[:, j]||_2, bit-identical to np.linalg.norm(A, axis=0) on an F-order
+ * array (sequential = 0: numpy's pairwise sum) or a C-order one
+ * (sequential = 1: row-order sum).  Device pointers. */
+int rq_column_norms(rq_handle_t h, const double* A, int64_t m, int64_t n, int64_t lda,
+                    int sequential, double* out, void* stream);
 int rq_frob_norm(rq_handle_t h, const double* A, int64_t m, int64_t n, int64_t lda,
                  double* out, void* stream);
 

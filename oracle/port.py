@@ -619,6 +619,21 @@ def qr_blocked(A, k=None, b=32, ctr=None):
     return Y, tau, work[:k, :].copy()
 
 
+def column_norms(A):
+    """np.linalg.norm(A, axis=0) (kernels.py:184-186); the summation order
+    follows A's memory layout, as numpy's does."""
+    return np.linalg.norm(A, axis=0)
+
+
+def qr_presorted(A, k=None, b=32, ctr=None):
+    """Blocked QR after a stable descending sort of the initial column norms
+    (qrcp.py:255-268); returns (Y, tau, R, order)."""
+    A = np.asarray(A, dtype=np.float64)
+    order = np.argsort(-column_norms(A), kind="stable")
+    Y, tau, R = qr_blocked(A[:, order], k=k, b=b, ctr=ctr)
+    return Y, tau, R, order
+
+
 def lq_factor(Z, b=32, ctr=None):
     """Z = L V^T through QR of Z^T (truncated.py:177-184)."""
     Z = np.asarray(Z, dtype=np.float64)

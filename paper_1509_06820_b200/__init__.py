@@ -19,6 +19,7 @@ from .factorization import (
     q_columns,
     t_factor,
 )
+from .qrcp import column_norms, qr_blocked, qr_presorted
 from .randomized import DegenerateSampleError, RandomizedConfig, rqrcp, rsrqrcp, ssrqrcp
 from .rng import RngState, gaussian_matrix
 from .truncated import lq_factor, qr_blocked_device, trqrcp, tuxv
@@ -38,10 +39,13 @@ __all__ = [
     "TruncatedFactorization",
     "TuxvFactorization",
     "build_t_matrix",
+    "column_norms",
     "gaussian_matrix",
     "lq_factor",
     "q_columns",
+    "qr_blocked",
     "qr_blocked_device",
+    "qr_presorted",
     "rqrcp",
     "rsrqrcp",
     "ssrqrcp",

@@ -70,6 +70,7 @@ SIGNATURES = {
     "rq_qr_blocked": (C.c_int, [vp, i64, i64, i64, i64, dp, i64, dp, i64, dp, C.POINTER(i64),
                                 vp]),
     "rq_q_columns": (C.c_int, [vp, i64, i64, i64, dp, i64, dp, i64, dp, i64, vp]),
+    "rq_column_norms": (C.c_int, [vp, dp, i64, i64, i64, C.c_int, dp, vp]),
     "rq_frob_norm": (C.c_int, [vp, dp, i64, i64, i64, dp, vp]),
     "rq_launch_count": (C.c_int64, []),
     "rq_set_option": (C.c_int, [vp, C.c_char_p, i64]),

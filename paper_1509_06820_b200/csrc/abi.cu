@@ -245,6 +245,14 @@ int rq_q_columns(rq_handle_t h, int64_t m, int64_t nref, int64_t cols, const dou
   });
 }
 
+int rq_column_norms(rq_handle_t h, const double* A, int64_t m, int64_t n, int64_t lda,
+                    int sequential, double* out, void* stream) {
+  return guarded([&] {
+    need(m >= 0 && n >= 0 && lda >= std::max<int64_t>(m, 1), "bad shape");
+    rq::column_norms(H(h), A, m, n, lda, sequential != 0, out, S(stream));
+  });
+}
+
 int rq_frob_norm(rq_handle_t h, const double* A, int64_t m, int64_t n, int64_t lda,
                  double* out, void* stream) {
   return guarded([&] { rq::frob_norm(H(h), A, m, n, lda, out, S(stream)); });

@@ -279,6 +279,10 @@ void apply_swaps(Handle& h, const int64_t* piv, int64_t got_max, int64_t i0,
                  const SwapTargets& t, Status* st, cudaStream_t s);
 
 // misc
+// np.linalg.norm(A, axis=0) bit for bit (pairwise per column, or sequential
+// in row order when mirroring a C-order host array)
+void column_norms(Handle& h, const double* A, int64_t m, int64_t n, int64_t lda, bool sequential,
+                  double* out, cudaStream_t s);
 void frob_norm(Handle& h, const double* A, int64_t m, int64_t n, int64_t lda, double* out,
                cudaStream_t s);
 void copy2d(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows,

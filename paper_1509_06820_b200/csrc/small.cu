@@ -507,6 +507,25 @@ __global__ void __launch_bounds__(256, 1) su_prep_wide_kernel(const double* __re
   }
 }
 
+// column_norms (kernels.py:184-186) = np.linalg.norm(A, axis=0), bit for bit:
+// numpy sums the rounded squares pairwise along a contiguous (F-order) column
+// and strictly in row order across a C-order array (axis 0 is then the outer
+// loop), so the caller names the layout it mirrors.
+__global__ void col_norms_kernel(const double* __restrict__ A, int64_t m, int64_t n, int64_t lda,
+                                 int sequential, double* __restrict__ out) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const double* x = A + j * lda;
+  double s;
+  if (sequential) {
+    s = 0.0;
+    for (int64_t i = 0; i < m; ++i) s = __dadd_rn(s, __dmul_rn(x[i], x[i]));
+  } else {
+    s = pairwise_sumsq(x, (int)m, 1);
+  }
+  out[j] = sqrt(s);
+}
+
 int grid_for(int64_t total, int num_sms) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 16LL * num_sms));
 }
@@ -658,6 +677,17 @@ void apply_swaps(Handle& h, const int64_t* piv, int64_t got_max, int64_t i0,
     attr = std::max<size_t>(smem, 48 * 1024);
   }
   swap_fused_kernel<<<std::max(uw + ur + uf, 1), 256, smem, s>>>(piv, i0, t, st, uw, ur);
+  RQ_CHECK_LAUNCH();
+  count_launch();
+}
+
+void column_norms(Handle& h, const double* A, int64_t m, int64_t n, int64_t lda, bool sequential,
+                  double* out, cudaStream_t s) {
+  if (n <= 0) return;
+  if (m > 0x7fffffff) throw InvalidArg("column_norms: too many rows");
+  ProfScope prof(h, kProfMisc, 2.0 * m * n, 8.0 * m * n, s);
+  col_norms_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(A, m, n, lda, sequential ? 1 : 0,
+                                                               out);
   RQ_CHECK_LAUNCH();
   count_launch();
 }

@@ -150,6 +150,43 @@ def _store(name, driver, A, k, block, padding, seed, full, f, recipe=""):
     np.savez_compressed(os.path.join(OUT, name + ".npz"), **rec)
 
 
+def make_qr(rq):
+    # qr_blocked / qr_presorted (qrcp.py:222-268) and column_norms
+    # (kernels.py:184-186); C-order and F-order inputs (numpy's norm sums in a
+    # layout-dependent order), tied norms, a partial rank
+    rec = {}
+    g = np.random.default_rng(77)
+    qcases = {
+        "gaussC": (np.ascontiguousarray(g.standard_normal((120, 90))), None, 32),
+        "gaussF": (np.asfortranarray(g.standard_normal((150, 70))), 50, 16),
+        "lowrank": (np.ascontiguousarray(_lowrank(5, 100, 80, 12)), None, 32),
+    }
+    # exact ties without rank deficiency: entry sign flips keep every square
+    # and its summation position, so the three copies' norms are equal bitwise
+    T = g.standard_normal((64, 20))
+    D1, D2 = (np.where(g.standard_normal((64, 1)) < 0, -1.0, 1.0) for _ in range(2))
+    qcases["ties"] = (np.ascontiguousarray(np.hstack([T, D1 * T[:, ::-1], D2 * T])), None, 8)
+    for key, (A, k, b) in qcases.items():
+        ctr = rq.OpCounters()
+        f = rq.qr_presorted(A, k, b, ctr)
+        fb = rq.qr_blocked(A, k, b, rq.OpCounters())
+        rec[f"{key}_A"] = A
+        rec[f"{key}_forder"] = np.array(int(A.flags.f_contiguous and not A.flags.c_contiguous))
+        rec[f"{key}_k"] = np.array(-1 if k is None else k)
+        rec[f"{key}_b"] = np.array(b)
+        rec[f"{key}_norms"] = rq.column_norms(A)
+        rec[f"{key}_perm"] = np.asarray(f.perm.forward)
+        rec[f"{key}_R"] = f.R
+        rec[f"{key}_Y"] = f.reflectors.Y
+        rec[f"{key}_tau"] = f.reflectors.tau
+        rec[f"{key}_trailing"] = f.trailing
+        rec[f"{key}_counters"] = np.array([ctr.gemm_flops, ctr.level2_flops, ctr.bytes_touched])
+        rec[f"{key}_blocked_R"] = fb.R
+        rec[f"{key}_blocked_counters"] = np.array([fb.counters.gemm_flops, fb.counters.level2_flops,
+                                                   fb.counters.bytes_touched])
+    np.savez_compressed(os.path.join(OUT, "kat_qr_presorted.npz"), **rec)
+
+
 def main():
     sys.path.insert(0, REF)
     import rqrcp as rq  # the reference package
@@ -229,6 +266,8 @@ def main():
         rec[f"p{s}_l2"] = ctr.level2_flops
     np.savez_compressed(os.path.join(OUT, "kat_panel.npz"), **rec)
 
+    make_qr(rq)
+
     for name, driver, build, k, block, padding, seed, full in CASES + [CFG1]:
         recipe = build if isinstance(build, str) else ""
         A = build_recipe(build) if recipe else build()
@@ -239,4 +278,9 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["qr"]:   # only the qr_presorted fixture
+        sys.path.insert(0, REF)
+        import rqrcp as _rq
+        make_qr(_rq)
+    else:
+        main()

@@ -166,3 +166,35 @@ def test_trqrcp_tuxv_vs_oracle_mid_size():
     ot = port.tuxv(A, 128, 32, 8, 0)
     ft = P.tuxv(A, 128, cfg)
     np.testing.assert_allclose(ft.singular_values(), ot.singular_values(), rtol=1e-9)
+
+
+def test_qr_blocked_presorted_vs_reference():
+    """qr_blocked / qr_presorted / column_norms on the GPU (qrcp.py:222-268,
+    kernels.py:184-186) against the reference's fixture: bit-identical column
+    norms for the caller's layout (so tied norms sort identically), the same
+    permutation and counters, R within 1e-10."""
+    import paper_1509_06820_b200 as P
+    rec = G.load("kat_qr_presorted")
+    for key in sorted({k.split("_")[0] for k in rec}):
+        A = rec[f"{key}_A"]
+        if int(rec[f"{key}_forder"]):
+            A = np.asfortranarray(A)
+        k = int(rec[f"{key}_k"])
+        k = None if k < 0 else k
+        b = int(rec[f"{key}_b"])
+        np.testing.assert_array_equal(P.column_norms(A), rec[f"{key}_norms"], err_msg=key)
+        f = P.qr_presorted(A, k, b)
+        np.testing.assert_array_equal(np.asarray(f.perm.forward), rec[f"{key}_perm"], err_msg=key)
+        scale = np.linalg.norm(rec[f"{key}_R"])
+        assert np.linalg.norm(f.R - rec[f"{key}_R"]) <= 1e-10 * scale, key
+        assert np.linalg.norm(f.trailing - rec[f"{key}_trailing"]) <= 1e-10 * scale, key
+        c = f.counters
+        assert [c.gemm_flops, c.level2_flops, c.bytes_touched] == list(rec[f"{key}_counters"]), key
+        fb = P.qr_blocked(A, k, b)
+        assert np.linalg.norm(fb.R - rec[f"{key}_blocked_R"]) <= 1e-10 * scale, key
+        cb = fb.counters
+        assert [cb.gemm_flops, cb.level2_flops, cb.bytes_touched] == \
+            list(rec[f"{key}_blocked_counters"]), key
+        q = f.q_factor()
+        Ap = A[:, f.perm.forward]
+        assert np.linalg.norm(Ap[:, :f.rank] - q @ f.R[:, :f.rank]) <= 1e-12 * np.linalg.norm(A), key

@@ -149,3 +149,28 @@ def test_explicit_omega_equals_seeded_stream():
     f2 = port.rqrcp(A, 24, 8, 4, 4, omega=om)
     np.testing.assert_array_equal(f1.perm.forward, f2.perm.forward)
     np.testing.assert_array_equal(f1.R, f2.R)
+
+
+def test_qr_presorted_kats():
+    """qr_blocked / qr_presorted / column_norms (qrcp.py:222-268,
+    kernels.py:184-186): the oracle reproduces the reference's fixture bit for
+    bit on the generating host (C-order, F-order, tied norms, partial rank)."""
+    rec = G.load("kat_qr_presorted")
+    for key in sorted({k.split("_")[0] for k in rec}):
+        A = rec[f"{key}_A"]
+        if int(rec[f"{key}_forder"]):
+            A = np.asfortranarray(A)
+        k = int(rec[f"{key}_k"])
+        k = None if k < 0 else k
+        b = int(rec[f"{key}_b"])
+        np.testing.assert_array_equal(port.column_norms(A), rec[f"{key}_norms"])
+        ctr = port.Counters()
+        Y, tau, R, order = port.qr_presorted(A, k, b, ctr)
+        np.testing.assert_array_equal(order, rec[f"{key}_perm"])
+        np.testing.assert_array_equal(R, rec[f"{key}_R"])
+        np.testing.assert_array_equal(tau, rec[f"{key}_tau"])
+        assert [ctr.gemm_flops, ctr.level2_flops, ctr.bytes_touched] == list(rec[f"{key}_counters"])
+        cb = port.Counters()
+        _, _, Rb = port.qr_blocked(A, k, b, cb)
+        np.testing.assert_array_equal(Rb, rec[f"{key}_blocked_R"])
+        assert [cb.gemm_flops, cb.level2_flops, cb.bytes_touched] == list(rec[f"{key}_blocked_counters"])
