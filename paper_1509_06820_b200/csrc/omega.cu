@@ -21,7 +21,9 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <condition_variable>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -138,6 +140,57 @@ void decode_range(Decoder& d, uint64_t from, uint64_t until, Chunk& c) {
   c.end = p;
 }
 
+// Fork-join worker pool kept across calls: creating 15 threads per call cost
+// ~0.4 ms of a ~1.8 ms cfg2 draw.  run(T, f) executes f(0..T-1), f(0) on the
+// caller.
+class Pool {
+ public:
+  void run(int T, const std::function<void(int)>& f) {
+    std::unique_lock<std::mutex> lk(m_);
+    while ((int)th_.size() < T - 1) {
+      const int idx = (int)th_.size() + 1;
+      th_.emplace_back([this, idx] { worker(idx); });
+      th_.back().detach();
+    }
+    job_ = &f;
+    active_ = T;
+    pending_ = T - 1;
+    ++gen_;
+    cv_.notify_all();
+    lk.unlock();
+    f(0);
+    lk.lock();
+    done_.wait(lk, [this] { return pending_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  void worker(int idx) {
+    int seen = 0;
+    std::unique_lock<std::mutex> lk(m_);
+    for (;;) {
+      cv_.wait(lk, [&] { return gen_ != seen; });
+      seen = gen_;
+      if (idx >= active_) continue;
+      const std::function<void(int)>* f = job_;
+      lk.unlock();
+      (*f)(idx);
+      lk.lock();
+      if (--pending_ == 0) done_.notify_one();
+    }
+  }
+  std::mutex m_;
+  std::condition_variable cv_, done_;
+  std::vector<std::thread> th_;
+  const std::function<void(int)>* job_ = nullptr;
+  int gen_ = 0, active_ = 0, pending_ = 0;
+};
+
+Pool& pool() {
+  static Pool* p = new Pool();   // never destroyed: detached workers outlive static destructors
+  return *p;
+}
+
 }  // namespace
 }  // namespace rq
 
@@ -164,15 +217,10 @@ extern "C" int rq_omega_fill(uint64_t k0, uint64_t k1, uint64_t raw, double* out
   std::lock_guard<std::mutex> lock(mu);
   if ((int)pool_chunks.size() < T) pool_chunks.resize(T);
   std::vector<Chunk>& ch = pool_chunks;
-  {
-    std::vector<std::thread> pool;
-    for (int t = 0; t < T; ++t)
-      pool.emplace_back([&, t] {
-        Decoder d(k0, k1);
-        decode_range(d, raw + t * D, raw + (t + 1) * D, ch[t]);
-      });
-    for (auto& th : pool) th.join();
-  }
+  pool().run(T, [&](int t) {
+    Decoder d(k0, k1);
+    decode_range(d, raw + t * D, raw + (t + 1) * D, ch[t]);
+  });
   // fix-up: chunk t's true first start is chunk t-1's end
   Decoder d(k0, k1);
   std::vector<size_t> first(T, 0);
@@ -203,18 +251,25 @@ extern "C" int rq_omega_fill(uint64_t k0, uint64_t k1, uint64_t raw, double* out
     c = std::move(fix);
     first[t] = 0;
   }
-  // concatenate; extend sequentially if the chunks fell short
+  // concatenate (in parallel); extend sequentially if the chunks fell short
+  std::vector<int64_t> off(T + 1, 0), take(T, 0);
   int64_t n = 0;
+  int tl = -1;
   for (int t = 0; t < T && n < count; ++t) {
     const size_t avail = ch[t].n - first[t];
-    const int64_t take = std::min<int64_t>((int64_t)avail, count - n);
-    std::memcpy(out + n, ch[t].val.data() + first[t], (size_t)take * sizeof(double));
-    n += take;
-    if (n == count) {
-      const size_t last = first[t] + (size_t)take;   // index after the count-th normal
-      *raw_end = last < ch[t].n ? ch[t].start[last] : ch[t].end;
-      return 0;
-    }
+    take[t] = std::min<int64_t>((int64_t)avail, count - n);
+    off[t] = n;
+    n += take[t];
+    tl = t;
+  }
+  pool().run(T, [&](int t) {
+    if (take[t] > 0)
+      std::memcpy(out + off[t], ch[t].val.data() + first[t], (size_t)take[t] * sizeof(double));
+  });
+  if (n == count && tl >= 0) {
+    const size_t last = first[tl] + (size_t)take[tl];   // index after the count-th normal
+    *raw_end = last < ch[tl].n ? ch[tl].start[last] : ch[tl].end;
+    return 0;
   }
   uint64_t p = ch[T - 1].end;
   for (; n < count; ++n) p = d.decode(p, out[n]);
