@@ -68,6 +68,8 @@ class Factor {
   // or a declined fast panel): the synchronous path then goes straight to the
   // exact panel, whose verdict the fast one would only have declined to give
   bool near_floor_ = false;
+  bool floor_seen_ = false;            // any noise-floor trigger: one block of lookahead
+  unsigned int* fin_done_ = nullptr;   // block_finish's CTA counter (degenerate verdict)
   Counters c_;
   int64_t m_ = 0, n_ = 0, k_ = 0, b_ = 0, ell_ = 0;
 
@@ -344,6 +346,8 @@ void Factor::stages(int64_t i0, int64_t bw, Counters& c, bool defer_trailing, bo
       f.X = X_; f.Bn = B_; f.ldb = ell_;
       f.Pz = p_.work + i0 + bw + i0 * p_.ldw;
       f.st = st_; f.pre = pre_;
+      f.done_ctr = h_.degen_commit ? fin_done_ : nullptr;
+      f.i0 = i0;
       if (!block_finish(h_, f, s_)) throw std::runtime_error("block_finish: unsupported shape");
       c.gemm_flops += 2 * mm * bw * nt2 + bw * bw * nt2 + 2 * bw * bw * nt2;
       touch(c, mm * nt2 + mm * bw + bw * nt2);
@@ -438,8 +442,11 @@ bool Factor::panel_overlap_inner(int64_t i0, int64_t bw) {
                i0 + bw < k_ && h_.overlap_select;
   double* a12 = fin_ready_ ? (double*)h_.buf("fin_A12", (size_t)2 * b_ * b_ * 8, s_) : nullptr;
   const int qp = panel_split(mm, nt2, bw);
+  // with block_finish a clearly degenerate R11 is committed (the block stays
+  // committed in the reference, randomized.py:253-258) and block_finish
+  // raises the resample
   panel_fast(h_, mm, bw, o.Rdst, p_.ldw, o, tol_, st_, s_, true, i0, qp, true, &Mrm, &ldm, S_, ell_,
-             msu, a12);
+             msu, a12, 0, 0, fin_ready_ && h_.degen_commit);
   msu_ready_ = true;
   const double* Pb = p_.work + i0 + bw + i0 * p_.ldw;
   const double* Cb = p_.work + i0 + bw + (i0 + bw) * p_.ldw;
@@ -594,7 +601,7 @@ bool Factor::slow_block(int64_t& i0, bool resampled, int64_t& rank, bool resume_
     c_.gemm_flops += pc.gemm_flops;
     c_.bytes_touched += pc.bytes_touched;
     const int64_t usable = read_status().usable;
-    if (usable < got) near_floor_ = true;
+    if (usable < got) near_floor_ = floor_seen_ = true;
     if (usable < got && !resampled) {
       fresh_sample(i0);
       c_.resamples += 1;
@@ -615,7 +622,8 @@ bool Factor::slow_block(int64_t& i0, bool resampled, int64_t& rank, bool resume_
       Counters uc;
       update(i0, bw, false, uc);
       if (read_status().degenerate) {
-        near_floor_ = true;
+        floor_seen_ = true;
+        if (!h_.degen_commit) near_floor_ = true;
         fresh_sample(i0);
         c_.resamples += 1;
       } else {
@@ -634,6 +642,8 @@ FactorResult Factor::run() {
   if (ell_ > m_) throw InvalidArg("sample rows exceed matrix rows");
   if (b_ < 1 || b_ > 256) throw InvalidArg("block must be in [1, 256]");
   st_ = (Status*)h_.buf("st", sizeof(Status), s_);
+  fin_done_ = (unsigned int*)h_.buf("fin_done", 64, s_);
+  RQ_CUDA(cudaMemsetAsync(fin_done_, 0, 64, s_));
   pre_ = (Status*)h_.buf("st_pre", sizeof(Status), s_);
   hst_ = (Status*)h_.host_pinned("hst", sizeof(Status), s_);
   hring_ = (int*)h_.host_pinned("hring", 64 * sizeof(int), s_);
@@ -686,7 +696,8 @@ FactorResult Factor::run() {
     stream_out(pend.empty() ? i0 : pend.front().i0, false);   // committed columns
     // near the noise floor triggers fire block after block: queue one block
     // ahead only, so a rewind discards fewer (early-exiting) launches
-    const int ahead = near_floor_ ? std::max(1, std::min(kLookahead, h_.floor_lookahead)) : kLookahead;
+    const int ahead =
+        floor_seen_ ? std::max(1, std::min(kLookahead, h_.floor_lookahead)) : kLookahead;
     if (!pend.empty() && (stopped || i0 >= k_ || (int)pend.size() >= ahead)) {
       Pending e = pend.front();
       RQ_CUDA(cudaEventSynchronize(ev_[e.slot]));
@@ -714,6 +725,11 @@ FactorResult Factor::run() {
         msu_ready_ = fin_ready_ = false;
         RQ_CUDA(cudaMemsetAsync(&st_->abort, 0, sizeof(int), s_));
         if (code == kAbortDegenerate || code == kAbortPanelFast || code == kAbortPanelRank)
+          floor_seen_ = true;
+        // a degenerate verdict no longer dooms the fast panel (it commits a
+        // clearly degenerate R11); a declined fast panel or a rank cut does
+        if (code == kAbortPanelFast || code == kAbortPanelRank ||
+            (code == kAbortDegenerate && !h_.degen_commit))
           near_floor_ = true;
         if (code == kAbortDegenerate) {
           i0 = X + bwX;

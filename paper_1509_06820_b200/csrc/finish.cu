@@ -177,6 +177,22 @@ __global__ void __launch_bounds__(kFinT, 1) block_finish_kernel(FinishArgs a) {
     const int n = e / r22, r = B + e % r22;
     a.Bn[r + (c0 + n) * a.ldb] = a.S[r + (c0 + n) * a.lds];
   }
+  if (a.done_ctr != nullptr) {
+    // randomized.py:117 raised: the block stays committed (R12 above, the
+    // trailing update on its snapshot predicate), the sample update is void
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      if (atomicAdd(a.done_ctr, 1u) == gridDim.x - 1) {
+        *a.done_ctr = 0;
+        if (*((volatile const int*)&a.st->degenerate) != 0) {
+          a.st->abort_i0 = a.i0;
+          __threadfence();
+          a.st->abort = kAbortDegenerate;
+        }
+      }
+    }
+  }
 }
 
 template <int B>

@@ -59,6 +59,7 @@ struct FastArgs {
   double* msu;                      // out (if S11): M = S11 R11^{-1}, b x b column-major
   double* a12;                      // out (if T): A1 = Y1 T, A2 = M T, b x b column-major each
   int64_t l2_extra;                 // extra level-2 count on commit (second half of a wider panel)
+  int degen_commit;                 // commit a clearly degenerate R11 (Status.degenerate = 1)
   int usable_total;                 // Status.usable on commit (0: the panel width)
   int64_t i0;
   int64_t nchunks;
@@ -191,7 +192,7 @@ __global__ void __launch_bounds__(kFT, 1) panel_fast_kernel(FastArgs a) {
     return;
   }
   extern __shared__ __align__(16) double sm[];
-  __shared__ int s_fail;
+  __shared__ int s_fail, s_degen;
   __shared__ double s_sign[kFMaxBw], s_c[kFMaxBw], s_dinv[kFMaxBw];
   auto lane_of = [](int t) { return t & 31; };
   const int tid = threadIdx.x;
@@ -517,12 +518,18 @@ __global__ void __launch_bounds__(kFT, 1) panel_fast_kernel(FastArgs a) {
       if (l < n && i <= l) u = (i == l) ? -(fabs(s_c[i]) + 1.0) : s_sign[l] * Q1[i * ld + l];
       Q1[i * ld + l] = u;
     }
+    if (tid == 0) s_degen = 0;
+    __syncthreads();
     for (int j = tid; j < n; j += kFT) {
       s_dinv[j] = -__drcp_rn(fabs(s_c[j]) + 1.0);
       const double rjj = fabs(Rt[j * ld + j]);
-      if ((a.tol >= 0.0 && !(rjj > kFastMargin * a.tol)) ||
-          (a.guard >= 0.0 && !(rjj > kFastMargin * a.guard)))
-        s_fail = 1;
+      if (a.tol >= 0.0 && !(rjj > kFastMargin * a.tol)) s_fail = 1;
+      if (a.guard >= 0.0 && !(rjj > kFastMargin * a.guard)) {
+        // below the sample update's degenerate guard (randomized.py:117):
+        // committable only when clearly below (the verdict cannot flip)
+        if (a.degen_commit && rjj * kFastMargin < a.guard) s_degen = 1;
+        else s_fail = 1;
+      }
     }
     __syncthreads();
     sub(6);
@@ -567,7 +574,7 @@ __global__ void __launch_bounds__(kFT, 1) panel_fast_kernel(FastArgs a) {
           const int l = e / n, i = e - l * n;
           a.msu[i + (int64_t)l * n] = s_sign[l] * (W5[i * ld + l] - W4[i * ld + l]);
         }
-        if (tid == 0) a.st->degenerate = 0;
+        if (tid == 0) a.st->degenerate = s_degen;
         __syncthreads();
       }
       if (a.T != nullptr) {
@@ -663,7 +670,7 @@ const int* panel_fast(Handle& h, int64_t mm, int64_t bw, const double* P, int64_
                       bool abort_on_decline, int64_t i0, int max_ctas, bool defer_zero,
                       const double** m_rowmajor, int64_t* m_ld, const double* S11,
                       int64_t lds11, double* msu, double* a12, int64_t l2_extra,
-                      int usable_total) {
+                      int usable_total, bool degen_commit) {
   if (!panel_fast_eligible(h, mm, bw)) return nullptr;
   const int n8 = (int)((bw + 7) / 8 * 8);
   const int ld = n8 + 1;
@@ -689,6 +696,7 @@ const int* panel_fast(Handle& h, int64_t mm, int64_t bw, const double* P, int64_
   a.a12 = out.T != nullptr ? a12 : nullptr;
   a.l2_extra = l2_extra;
   a.usable_total = usable_total;
+  a.degen_commit = (degen_commit && S11 != nullptr) ? 1 : 0;
   a.i0 = i0;
   a.bar = (unsigned int*)h.buf("pf_bar", 64, s);
   static void* zeroed = nullptr;

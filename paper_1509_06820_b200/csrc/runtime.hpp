@@ -105,6 +105,7 @@ class Handle {
   int floor_lookahead = 1;                  // speculative blocks queued once near the noise floor
   bool t_inverse = true;                    // T factor as a DMMA triangular inverse (nb <= 64)
   bool panel_halves = true;                 // 65..128-wide speculative panels as two fast halves
+  bool degen_commit = true;                 // fast panel commits clearly degenerate R11 (block_finish resamples)
 
   bool use_rank_update = true;
   bool fast_panel = true;   // CholeskyQR2 + Householder reconstruction panel (panel_fast.cu)
@@ -225,7 +226,7 @@ const int* panel_fast(Handle& h, int64_t mm, int64_t bw, const double* P, int64_
                       bool defer_zero = false, const double** m_rowmajor = nullptr,
                       int64_t* m_ld = nullptr, const double* S11 = nullptr,
                       int64_t lds11 = 0, double* msu = nullptr, double* a12 = nullptr,
-                      int64_t l2_extra = 0, int usable_total = 0);
+                      int64_t l2_extra = 0, int usable_total = 0, bool degen_commit = false);
 
 // Rest of a speculative RQRCP block after a committed fast panel, one CTA per
 // 64-column tile of the trailing matrix (csrc/finish.cu):
@@ -244,6 +245,11 @@ struct FinishArgs {
   double* Bn; int64_t ldb;          // ell x nt2
   double* Pz;                       // panel rows below the diagonal: (mm - b) x b, ld ldw
   Status* st; Status* pre;
+  // optional: the fast panel committed a clearly degenerate R11 (Status.degenerate):
+  // the last CTA to finish raises kAbortDegenerate at block i0 (after block 0's
+  // snapshot in `pre`, so the trailing update still runs)
+  unsigned int* done_ctr;
+  int64_t i0;
 };
 bool block_finish(Handle& h, const FinishArgs& f, cudaStream_t s);
 
