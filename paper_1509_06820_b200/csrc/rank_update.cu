@@ -619,8 +619,10 @@ __global__ void __launch_bounds__(kRuThreads, 1) rank_update_big_kernel(RuArgs a
         epi(prev, t - 1, 2 * ks);
         epi(prev, t - 1, 2 * ks + 1);
       }
-      if (has_prev && ks == 8) stage_c(t);   // own slots, after their last read
+      if (KS > 8 && has_prev && ks == 8) stage_c(t);   // own slots, after their last read
     }
+    // K = 32 (8 k-steps): the epilogue took every step, stage after the loop
+    if (KS <= 8 && has_prev) stage_c(t);
     if (more && (t + 1) / tn != t / tn) {   // next tile starts a new Y block
       __syncthreads();
       load_y((t + 1) / tn);

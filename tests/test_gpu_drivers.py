@@ -139,7 +139,7 @@ def test_validation_errors_match_reference():
         P.RandomizedConfig(block=0)
 
 
-@pytest.mark.parametrize("n,b", [(2048, 64), (1536, 128)])
+@pytest.mark.parametrize("n,b", [(2048, 64), (1536, 128), (3072, 32)])
 def test_rqrcp_larger_vs_oracle(n, b):
     import paper_1509_06820_b200 as P
     A = np.random.default_rng(n).standard_normal((n, n))
@@ -198,3 +198,21 @@ def test_qr_blocked_presorted_vs_reference():
         q = f.q_factor()
         Ap = A[:, f.perm.forward]
         assert np.linalg.norm(Ap[:, :f.rank] - q @ f.R[:, :f.rank]) <= 1e-12 * np.linalg.norm(A), key
+
+
+def test_tuxv_tall_vs_oracle():
+    """TUXV whose blocked QRs (b = 32) run on tall 12000-row blocks: several
+    trailing-update tiles per CTA (the cfg4 shape class)."""
+    import paper_1509_06820_b200 as P
+    g = np.random.default_rng(4)
+    m, n, r = 12000, 3000, 128
+    U = np.linalg.qr(g.standard_normal((m, r + 32)))[0]
+    V = np.linalg.qr(g.standard_normal((n, r + 32)))[0]
+    s = 1.0 / (1.0 + np.arange(r + 32)) ** 2
+    A = np.asfortranarray((U * s) @ V.T)
+    cfg = P.RandomizedConfig(block=32, padding=8, seed=0)
+    o = port.tuxv(A, r, 32, 8, 0)
+    f = P.tuxv(A, r, cfg)
+    np.testing.assert_allclose(f.singular_values(), o.singular_values(), rtol=1e-8)
+    frob = np.linalg.norm(A)
+    assert abs(np.linalg.norm(A - f.approx()) - np.linalg.norm(A - o.approx())) <= 1e-3 * frob

@@ -218,3 +218,16 @@ def test_t_factor_inverse_matches_recurrence(nb):
     assert np.linalg.norm(got - ref) <= 1e-13 * scale
     assert np.linalg.norm(rec - ref) <= 1e-13 * scale
     np.testing.assert_array_equal(got[np.tril_indices(nb, -1)], 0.0)
+
+
+@pytest.mark.parametrize("M,N,K", [(20000, 224, 32), (5000, 1000, 32), (20000, 224, 64),
+                                   (4100, 3000, 64), (8192, 256, 128), (300, 100, 32)])
+def test_rank_update_multi_tile(M, N, K):
+    """C -= Y X through the persistent rank-b kernels when a CTA owns several
+    tiles (tall trailing blocks; K = 128 as two 64-deep passes), against
+    the fp64 numpy product."""
+    from paper_1509_06820_b200.primitives import gemm
+    g = np.random.default_rng(M + N + K)
+    Y, X, C0 = g.standard_normal((M, K)), g.standard_normal((K, N)), g.standard_normal((M, N))
+    out = gemm(_dev(Y), _dev(X), _dev(C0), alpha=-1.0, beta=1.0).cpu().numpy()
+    assert np.abs(out - (C0 - Y @ X)).max() <= 64 * K * np.finfo(float).eps * 10
