@@ -3,7 +3,7 @@ the GPU factorization (native driver) and oracle/port.py (the reference's
 numpy algorithm) on the same A bytes and seed.  Reports identical pivots,
 ||R - R_oracle|| / ||R_oracle||, the residual of the GPU factorization on a
 column sample, and the counters.
-Usage: python tools/full_parity.py cfg2 out.json"""
+Usage: python tools/full_parity.py cfg2 out.json [m=.. n=.. block=..]"""
 import json
 import os
 import sys
@@ -18,7 +18,11 @@ import paper_1509_06820_b200 as P
 from oracle import port
 
 name = sys.argv[1]
-cfg = bench.CONFIGS[name]
+cfg = dict(bench.CONFIGS[name])
+for kv in sys.argv[3:]:   # overrides, e.g. m=8192 n=8192 block=32
+    k_, v_ = kv.split("=")
+    cfg[k_] = int(v_)
+    name += f" {k_}={v_}"
 dev = torch.device("cuda", 0)
 A_d = bench.device_matrix(cfg["kind"], cfg["m"], cfg["n"], dev, seed=0)
 A = A_d.cpu().numpy()
