@@ -187,6 +187,31 @@ def make_qr(rq):
     np.savez_compressed(os.path.join(OUT, "kat_qr_presorted.npz"), **rec)
 
 
+def make_harness(rq):
+    """harness.py callers: counter CSV (byte-stable), pivot
+    trace CSV, sigma CSV and quality curves of the reference on one
+    synthetic matrix."""
+    import io
+    from rqrcp import harness as H
+    A = H.synthetic_matrix("stepped", 120, 96, seed=3)
+    cfg = rq.RandomizedConfig(block=16, padding=8, seed=0)
+    algos = ("qr", "qr_presorted", "rqrcp", "rsrqrcp", "ssrqrcp", "trqrcp", "tuxv")
+    buf = io.StringIO(newline="")
+    H.write_bench_csv(H.bench(A, algos, k=24, config=cfg), buf, timing=False)
+    fbuf = io.StringIO(newline="")
+    H.write_factor_csv(rq.rqrcp(A, None, cfg), fbuf)
+    tbuf = io.StringIO(newline="")
+    H.write_tuxv_csv(rq.tuxv(A, 20, cfg), tbuf)
+    ranks = [8, 16, 24, 32, 40]
+    qalgos = ("qr_presorted", "rqrcp", "rsrqrcp", "trqrcp", "tuxv")
+    curve = H.quality_sweep(A, ranks, qalgos, cfg)
+    rec = {"A": A, "bench_csv": np.array(buf.getvalue()), "factor_csv": np.array(fbuf.getvalue()),
+           "tuxv_csv": np.array(tbuf.getvalue()), "ranks": np.array(ranks)}
+    for a in qalgos:
+        rec["curve_" + a] = np.asarray(curve.relerr[a])
+    np.savez_compressed(os.path.join(OUT, "kat_harness.npz"), **rec)
+
+
 def main():
     sys.path.insert(0, REF)
     import rqrcp as rq  # the reference package
@@ -267,6 +292,7 @@ def main():
     np.savez_compressed(os.path.join(OUT, "kat_panel.npz"), **rec)
 
     make_qr(rq)
+    make_harness(rq)
 
     for name, driver, build, k, block, padding, seed, full in CASES + [CFG1]:
         recipe = build if isinstance(build, str) else ""
@@ -278,9 +304,9 @@ def main():
 
 
 if __name__ == "__main__":
-    if sys.argv[1:] == ["qr"]:   # only the qr_presorted fixture
+    if sys.argv[1:] in (["qr"], ["harness"]):   # one fixture only
         sys.path.insert(0, REF)
         import rqrcp as _rq
-        make_qr(_rq)
+        (make_qr if sys.argv[1] == "qr" else make_harness)(_rq)
     else:
         main()

@@ -216,3 +216,41 @@ def test_tuxv_tall_vs_oracle():
     np.testing.assert_allclose(f.singular_values(), o.singular_values(), rtol=1e-8)
     frob = np.linalg.norm(A)
     assert abs(np.linalg.norm(A - f.approx()) - np.linalg.norm(A - o.approx())) <= 1e-3 * frob
+
+
+def test_harness_callers_vs_reference():
+    """The GPU harness (harness.py:89-241 callers): the counter CSV is byte-
+    identical to the reference's, the pivot trace has the same pivots, sigma
+    estimates and quality curves agree to rounding."""
+    import csv
+    import io
+    from paper_1509_06820_b200 import harness as H
+    import paper_1509_06820_b200 as P
+    rec = G.load("kat_harness")
+    A = rec["A"]
+    cfg = P.RandomizedConfig(block=16, padding=8, seed=0)
+    algos = ("qr", "qr_presorted", "rqrcp", "rsrqrcp", "ssrqrcp", "trqrcp", "tuxv")
+    buf = io.StringIO(newline="")
+    H.write_bench_csv(H.bench(A, algos, k=24, config=cfg), buf, timing=False)
+    assert buf.getvalue() == str(rec["bench_csv"])
+    fbuf = io.StringIO(newline="")
+    H.write_factor_csv(P.rqrcp(A, None, cfg), fbuf)
+    mine = list(csv.reader(io.StringIO(fbuf.getvalue())))
+    theirs = list(csv.reader(io.StringIO(str(rec["factor_csv"]))))
+    assert len(mine) == len(theirs) and mine[-1] == theirs[-1]   # counters comment
+    for a, b in zip(mine[1:-1], theirs[1:-1]):
+        assert a[:2] == b[:2]
+        assert abs(float(a[2]) - float(b[2])) <= 1e-12 * abs(float(theirs[1][2]))
+    tbuf = io.StringIO(newline="")
+    H.write_tuxv_csv(P.tuxv(A, 20, cfg), tbuf)
+    mt = list(csv.reader(io.StringIO(tbuf.getvalue())))
+    tt = list(csv.reader(io.StringIO(str(rec["tuxv_csv"]))))
+    assert mt[-1] == tt[-1]
+    np.testing.assert_allclose([float(r[1]) for r in mt[1:-1]], [float(r[1]) for r in tt[1:-1]],
+                               rtol=1e-9)
+    ranks = [int(x) for x in rec["ranks"]]
+    qalgos = ("qr_presorted", "rqrcp", "rsrqrcp", "trqrcp", "tuxv")
+    curve = H.quality_sweep(A, ranks, qalgos, cfg)
+    for a in qalgos:
+        np.testing.assert_allclose(curve.relerr[a], rec["curve_" + a], rtol=1e-6, atol=1e-14,
+                                   err_msg=a)
