@@ -21,7 +21,7 @@ name = sys.argv[1]
 cfg = dict(bench.CONFIGS[name])
 for kv in sys.argv[3:]:   # overrides, e.g. m=8192 n=8192 block=32
     k_, v_ = kv.split("=")
-    cfg[k_] = int(v_)
+    cfg[k_] = v_ if k_ in ("driver", "kind") else int(v_)
     name += f" {k_}={v_}"
 dev = torch.device("cuda", 0)
 A_d = bench.device_matrix(cfg["kind"], cfg["m"], cfg["n"], dev, seed=0)
@@ -30,8 +30,12 @@ A = np.asfortranarray(A)
 conf = P.RandomizedConfig(block=cfg["block"], padding=cfg["padding"], seed=0)
 drv = cfg["driver"]
 run_gpu = {"rqrcp": lambda: P.rqrcp(A_d, cfg["k"], conf), "trqrcp": lambda: P.trqrcp(A_d, cfg["k"], conf),
-           "tuxv": lambda: P.tuxv(A_d, cfg["k"], conf)}[drv]
+           "tuxv": lambda: P.tuxv(A_d, cfg["k"], conf),
+           "rsrqrcp": lambda: P.rsrqrcp(A_d, cfg["k"], conf),
+           "ssrqrcp": lambda: P.ssrqrcp(A_d, cfg["k"], conf)}[drv]
 run_cpu = {"rqrcp": lambda: port.rqrcp(A, cfg["k"], cfg["block"], cfg["padding"], 0),
+           "rsrqrcp": lambda: port.rsrqrcp(A, cfg["k"], cfg["block"], cfg["padding"], 0),
+           "ssrqrcp": lambda: port.ssrqrcp(A, cfg["k"], cfg["block"], cfg["padding"], 0),
            "trqrcp": lambda: port.trqrcp(A, cfg["k"], cfg["block"], cfg["padding"], 0),
            "tuxv": lambda: port.tuxv(A, cfg["k"], cfg["block"], cfg["padding"], 0)}[drv]
 t = time.perf_counter()
@@ -68,7 +72,7 @@ else:
     out["counters_gpu"] = [int(c.gemm_flops), int(c.level2_flops), int(c.resamples)]
     out["counters_oracle"] = [int(o.counters.gemm_flops), int(o.counters.level2_flops),
                               int(o.counters.resamples)]
-    if drv == "rqrcp":
+    if drv in ("rqrcp", "rsrqrcp") and cfg["k"] is None:
         # residual ||A P - Q R|| on 64 sampled columns (dense Q formed on the device)
         g = np.random.default_rng(1)
         cols = np.sort(g.choice(cfg["n"], 64, replace=False))
