@@ -661,8 +661,10 @@ __global__ void __launch_bounds__(kFT, 1) panel_fast_kernel(FastArgs a) {
 
 bool panel_fast_eligible(const Handle& h, int64_t mm, int64_t bw) {
   if (!h.fast_panel || bw < 2 || bw > kFMaxBw || mm < 2 * bw) return false;
+  // the kernel's layouts (log2 strides, the recursive block inverse) need a
+  // power-of-two padded width: n8 in {8, 16, 32, 64}
   const int n8 = (int)((bw + 7) / 8 * 8);
-  return !(kFT / n8 > 32 || 32 % (kFT / n8) != 0);   // n8 in {8, 16, 32, 64}
+  return n8 == 8 || n8 == 16 || n8 == 32 || n8 == 64;
 }
 
 const int* panel_fast(Handle& h, int64_t mm, int64_t bw, const double* P, int64_t ldp,

@@ -254,3 +254,23 @@ def test_harness_callers_vs_reference():
     for a in qalgos:
         np.testing.assert_allclose(curve.relerr[a], rec["curve_" + a], rtol=1e-6, atol=1e-14,
                                    err_msg=a)
+
+
+@pytest.mark.parametrize("m,n,b,k,variant", [(1200, 1100, 56, None, "rqrcp"), (900, 820, 50, None, "rqrcp"),
+                                             (1000, 948, 64, None, "rqrcp"), (2000, 1600, 120, 120, "ssrqrcp"),
+                                             (1300, 1300, 40, 600, "trqrcp")])
+def test_panel_widths_vs_oracle(m, n, b, k, variant):
+    """Panel widths whose padded width is not a power of two (b = 40, 50, 56,
+    a 52-wide last block, the 56-wide second half of a 120-wide panel) take
+    the exact panel, never the fast one's power-of-two layouts."""
+    import paper_1509_06820_b200 as P
+    A = np.random.default_rng(m + n + b).standard_normal((m, n))
+    cfg = P.RandomizedConfig(block=32 if variant == "ssrqrcp" else b, padding=8, seed=0)
+    run = {"rqrcp": lambda M: (P.rqrcp(M, k, cfg), port.rqrcp(M, k, b, 8, 0)),
+           "ssrqrcp": lambda M: (P.ssrqrcp(M, k, cfg), port.ssrqrcp(M, k, 32, 8, 0)),
+           "trqrcp": lambda M: (P.trqrcp(M, k, cfg), port.trqrcp(M, k, b, 8, 0))}[variant]
+    f, o = run(A)
+    np.testing.assert_array_equal(np.asarray(f.perm.forward), o.perm.forward)
+    assert np.linalg.norm(f.R - o.R) <= 1e-10 * np.linalg.norm(o.R)
+    assert (f.counters.gemm_flops, f.counters.level2_flops) == \
+        (o.counters.gemm_flops, o.counters.level2_flops)
