@@ -56,3 +56,19 @@ def test_sharded_world1_matches_native(group, name):
     assert np.linalg.norm(R - f.R) <= 1e-12 * max(np.linalg.norm(f.R), 1e-300)
     np.testing.assert_array_equal(np.array(s.swaps).reshape(-1, 2),
                                   np.array(f.perm.swaps).reshape(-1, 2))
+
+
+@pytest.mark.parametrize("m,n,b", [(2048, 1800, 64), (1500, 1500, 48), (1200, 1000, 128)])
+def test_sharded_world1_larger_vs_oracle(group, m, n, b):
+    """Larger and odd block widths through the sharded driver against the CPU
+    oracle (pivots identical, R to 1e-10)."""
+    import torch
+    import paper_1509_06820_b200 as P
+    from oracle import port
+    from paper_1509_06820_b200.parallel import rqrcp_sharded
+    A = np.random.default_rng(m + b).standard_normal((m, n))
+    cfg = P.RandomizedConfig(block=b, padding=8, seed=0)
+    o = port.rqrcp(A, None, b, 8, 0)
+    s = rqrcp_sharded(torch.from_numpy(np.asfortranarray(A)).cuda(), m, n, None, cfg)
+    np.testing.assert_array_equal(s.perm, o.perm.forward)
+    assert np.linalg.norm(s.R.cpu().numpy() - o.R) <= 1e-10 * np.linalg.norm(o.R)
