@@ -20,24 +20,25 @@ namespace rq {
 namespace {
 
 constexpr int kFinT = 256;   // 8 warps: 2 (m) x 4 (n), warp tile 32 x 16
-constexpr int kFinN = 64;    // columns per CTA
+// columns per CTA: 64, or 32 when 64-wide tiles would leave SMs idle (the
+// three products are DMMA-throughput bound per SM: ~2 MFLOP per 64-wide tile)
 constexpr int kFinLd = 68;   // k-major A operands: [k][m], row stride (doubles)
 
 // acc(64 x 64 tile, this warp's 32 x 16) += A B: A-fragment (m, k) at
 // Ak[k * kFinLd + m] (k-major), B-fragment (k, n) at Bn[n * ldb + k] (n-major,
 // ldb = 8 mod 16 words apart per n: conflict-free 64-bit fragment loads);
 // fragments double-buffered in registers
-template <int K>
-RQ_DEV void tile_prod(const double* Ak, const double* Bn, int ldb, double (&acc)[4][2][2]) {
+template <int K, int YN>
+RQ_DEV void tile_prod(const double* Ak, const double* Bn, int ldb, double (&acc)[4][YN][2]) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wm0 = (warp & 1) * 32, wn0 = (warp >> 1) * 16;
+  const int wm0 = (warp & 1) * 32, wn0 = (warp >> 1) * 8 * YN;
   const int fr = lane >> 2, fk = lane & 3;
-  double af[2][4], bf[2][2];
+  double af[2][4], bf[2][YN];
   auto load = [&](int k4, int p) {
 #pragma unroll
     for (int x = 0; x < 4; ++x) af[p][x] = Ak[(k4 + fk) * kFinLd + wm0 + x * 8 + fr];
 #pragma unroll
-    for (int y = 0; y < 2; ++y) bf[p][y] = Bn[(wn0 + y * 8 + fr) * ldb + k4 + fk];
+    for (int y = 0; y < YN; ++y) bf[p][y] = Bn[(wn0 + y * 8 + fr) * ldb + k4 + fk];
   };
   load(0, 0);
 #pragma unroll
@@ -47,15 +48,16 @@ RQ_DEV void tile_prod(const double* Ak, const double* Bn, int ldb, double (&acc)
 #pragma unroll
     for (int x = 0; x < 4; ++x)
 #pragma unroll
-      for (int y = 0; y < 2; ++y) dmma884(acc[x][y], af[p][x], bf[p][y]);
+      for (int y = 0; y < YN; ++y) dmma884(acc[x][y], af[p][x], bf[p][y]);
   }
 }
 
-RQ_DEV void zero_acc(double (&acc)[4][2][2]) {
+template <int YN>
+RQ_DEV void zero_acc(double (&acc)[4][YN][2]) {
 #pragma unroll
   for (int x = 0; x < 4; ++x)
 #pragma unroll
-    for (int y = 0; y < 2; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+    for (int y = 0; y < YN; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
 }
 
 // column segment of `len` doubles (len even) global -> shared, 16-byte copies
@@ -69,8 +71,9 @@ RQ_DEV void stage_col(double* dst, const double* src, int len, bool ok, int lane
   }
 }
 
-template <int B>
+template <int B, int NW>
 __global__ void __launch_bounds__(kFinT, 1) block_finish_kernel(FinishArgs a) {
+  constexpr int kFinN = NW, YN = NW / 32;
   if (blockIdx.x == 0 && threadIdx.x == 0 && a.pre != nullptr)
     a.pre->abort = *((volatile const int*)&a.st->abort);   // predicate of the trailing update
   if (aborted(a.st)) return;
@@ -83,7 +86,7 @@ __global__ void __launch_bounds__(kFinT, 1) block_finish_kernel(FinishArgs a) {
   double* MS = YT + B * kFinLd;      // [B][kFinLd]   MS[k][m] = Msu(m, k)
   double* SS = AK;                   // [64][LS]      S12 per column, after phase 1
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int wm0 = (warp & 1) * 32, wn0 = (warp >> 1) * 16;
+  const int wm0 = (warp & 1) * 32, wn0 = (warp >> 1) * 8 * YN;
   const int fr = lane >> 2, fk = lane & 3;
   const int64_t c0 = (int64_t)blockIdx.x * kFinN;
   const int nc = (int)imin64(kFinN, a.nt2 - c0);
@@ -118,10 +121,10 @@ __global__ void __launch_bounds__(kFinT, 1) block_finish_kernel(FinishArgs a) {
   }
   cp_async_wait<0>();
   __syncthreads();
-  double acc[4][2][2];
+  double acc[4][YN][2];
   // ---- X = [A1; A2]^T [C_top; H]
   zero_acc(acc);
-  tile_prod<2 * B>(AK, BN, LB, acc);
+  tile_prod<2 * B, YN>(AK, BN, LB, acc);
   __syncthreads();   // AK and the H part of BN are free
   for (int n = warp; n < kFinN; n += kFinT / 32) {       // S12, lands during phase 2
     const bool ok = n < nc;
@@ -131,7 +134,7 @@ __global__ void __launch_bounds__(kFinT, 1) block_finish_kernel(FinishArgs a) {
 #pragma unroll
   for (int x = 0; x < 4; ++x)
 #pragma unroll
-    for (int y = 0; y < 2; ++y)
+    for (int y = 0; y < YN; ++y)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int m = wm0 + x * 8 + fr, n = wn0 + y * 8 + 2 * fk + e;
@@ -143,11 +146,11 @@ __global__ void __launch_bounds__(kFinT, 1) block_finish_kernel(FinishArgs a) {
   __syncthreads();
   // ---- R12 = C_top - Y_top X  (C_top part of BN overwritten in place by its owner)
   zero_acc(acc);
-  tile_prod<B>(YT, BN + B, LB, acc);
+  tile_prod<B, YN>(YT, BN + B, LB, acc);
 #pragma unroll
   for (int x = 0; x < 4; ++x)
 #pragma unroll
-    for (int y = 0; y < 2; ++y)
+    for (int y = 0; y < YN; ++y)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int m = wm0 + x * 8 + fr, n = wn0 + y * 8 + 2 * fk + e;
@@ -161,11 +164,11 @@ __global__ void __launch_bounds__(kFinT, 1) block_finish_kernel(FinishArgs a) {
   __syncthreads();
   // ---- B_new = [S12 - Msu R12; S22]
   zero_acc(acc);
-  tile_prod<B>(MS, BN, LB, acc);
+  tile_prod<B, YN>(MS, BN, LB, acc);
 #pragma unroll
   for (int x = 0; x < 4; ++x)
 #pragma unroll
-    for (int y = 0; y < 2; ++y)
+    for (int y = 0; y < YN; ++y)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int m = wm0 + x * 8 + fr, n = wn0 + y * 8 + 2 * fk + e;
@@ -195,28 +198,34 @@ __global__ void __launch_bounds__(kFinT, 1) block_finish_kernel(FinishArgs a) {
   }
 }
 
-template <int B>
-void launch_finish(const FinishArgs& f, int grid, cudaStream_t s) {
-  constexpr size_t smem =
-      ((size_t)4 * B * kFinLd + (size_t)kFinN * (2 * B + 4)) * sizeof(double);
+template <int B, int NW>
+void launch_finish(const FinishArgs& f, cudaStream_t s) {
+  constexpr size_t smem = ((size_t)4 * B * kFinLd + (size_t)NW * (2 * B + 4)) * sizeof(double);
   static bool attr = false;
   if (!attr) {
-    RQ_CUDA(cudaFuncSetAttribute(block_finish_kernel<B>,
+    RQ_CUDA(cudaFuncSetAttribute(block_finish_kernel<B, NW>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  block_finish_kernel<B><<<grid, kFinT, smem, s>>>(f);
+  const int grid = (int)((f.nt2 + NW - 1) / NW);
+  block_finish_kernel<B, NW><<<grid, kFinT, smem, s>>>(f);
 }
 
 }  // namespace
 
 bool block_finish(Handle& h, const FinishArgs& f, cudaStream_t s) {
   if ((f.b != 32 && f.b != 64) || f.nt2 <= 0 || f.ell < f.b) return false;
-  const int grid = (int)((f.nt2 + kFinN - 1) / kFinN);
   ProfScope prof(h, kProfSmallGemm, 2.0 * f.b * f.nt2 * (2.0 * f.b + f.b + f.b),
                  8.0 * (4.0 * f.b * f.nt2 + (double)f.ell * f.nt2), s);
-  if (f.b == 64) launch_finish<64>(f, grid, s);
-  else launch_finish<32>(f, grid, s);
+  // 32-wide tiles while 64-wide ones would not fill the SMs
+  const bool narrow = h.finish_narrow && (f.nt2 + 63) / 64 < h.num_sms;
+  if (f.b == 64) {
+    if (narrow) launch_finish<64, 32>(f, s);
+    else launch_finish<64, 64>(f, s);
+  } else {
+    if (narrow) launch_finish<32, 32>(f, s);
+    else launch_finish<32, 64>(f, s);
+  }
   RQ_CHECK_LAUNCH();
   count_launch();
   return true;

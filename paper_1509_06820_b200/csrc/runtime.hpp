@@ -106,6 +106,7 @@ class Handle {
   bool t_inverse = true;                    // T factor as a DMMA triangular inverse (nb <= 64)
   bool panel_halves = true;                 // 65..128-wide speculative panels as two fast halves
   bool degen_commit = true;                 // fast panel commits clearly degenerate R11 (block_finish resamples)
+  bool finish_narrow = true;                // block_finish: 32-column tiles when 64 would leave SMs idle
 
   bool use_rank_update = true;
   bool fast_panel = true;   // CholeskyQR2 + Householder reconstruction panel (panel_fast.cu)
