@@ -140,7 +140,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -156,7 +156,7 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
 
     def __exit__(self, *exc):
         if self.proc is not None:
@@ -167,10 +167,25 @@ class ClockSampler:
                 self.proc.kill()
             self.t.join(timeout=2)
 
-    def summary(self):
+    def window(self, t0, t1):
+        """Summary of the samples taken between host times t0 and t1 (the
+        sampler runs across the whole bench, so its start-up and the NVML
+        queries' first costs fall in the warm-up, not in a timed pass)."""
+        lines = list(self.lines)
+        pad = 0.0
+        win = [(t, ln) for t, ln in lines if t0 <= t <= t1]
+        while len(win) < 3 and pad < 0.2:   # a short pass: widen to the nearest samples
+            pad += 0.04
+            win = [(t, ln) for t, ln in lines if t0 - pad <= t <= t1 + pad]
+        out = self.summary(win)
+        if pad:
+            out["window_padded_ms"] = round(1e3 * pad)
+        return out
+
+    def summary(self, lines=None):
         sm, smax, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for _, ln in (self.lines if lines is None else lines):
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 8:
                 continue
@@ -320,6 +335,9 @@ def main():
         A = None
     else:
         step = run_ours
+    # clocks are sampled by one nvidia-smi process for the whole run (started
+    # before the warm-up); each timed pass reports the samples of its window
+    sampler = ClockSampler(local).__enter__()
     for _ in range(args.warmup):
         f = step(P, cfg, A, None)
     barrier()
@@ -333,20 +351,22 @@ def main():
         _abi.check(lib.rq_profile_enable(h, 1 if profile else 0))
         l0 = lib.rq_launch_count()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with ClockSampler(local) as clk_:
-            barrier()
-            e0.record(stream)
-            for _ in range(args.steps):
-                f_ = step(P, cfg, A, None)
-            e1.record(stream)
-            barrier()
+        barrier()
+        t0 = time.time()
+        e0.record(stream)
+        for _ in range(args.steps):
+            f_ = step(P, cfg, A, None)
+        e1.record(stream)
+        barrier()
+        t1 = time.time()
         _abi.check(lib.rq_profile_enable(h, 0))
-        return f_, e0.elapsed_time(e1), lib.rq_launch_count() - l0, clk_
+        return f_, e0.elapsed_time(e1), lib.rq_launch_count() - l0, sampler.window(t0, t1)
 
     # headline pass without per-launch events, then the same K steps again
     # with them (kernel shares and the roofline's per-launch durations)
     f, ms, launches, clk = timed_pass(False)
     f, ms_prof, _, clk_prof = timed_pass(True)
+    sampler.__exit__(None, None, None)
     n_cat = len(_abi.PROF_NAMES)
     L = (C.c_int64 * n_cat)()
     MS = (C.c_double * n_cat)()
@@ -444,9 +464,9 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),
-            "clocks": clk.summary(),
+            "clocks": clk,
             "kernels": kernels,
-            "profiled_pass": {"ms_per_step": ms_prof / args.steps, "clocks": clk_prof.summary(),
+            "profiled_pass": {"ms_per_step": ms_prof / args.steps, "clocks": clk_prof,
                               "note": "same K steps re-run with CUDA events around every "
                                       "library launch; `kernels` and `roofline` come from it"},
             "counters": {"gemm_flops": res_counters.gemm_flops,
