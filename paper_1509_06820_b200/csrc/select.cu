@@ -230,8 +230,66 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
     if (warp == 0) {
       const unsigned long long wk = slot_max(j % 3);
       const int owner = wk ? (int)omap[key_pos(wk)] : -1;
-      double xv[5];  // ell <= 160
+      double xv[5];  // ell <= 160 (longer samples: the loop form below)
       double xnorm = -1.0;
+      if (ell > 160) {
+        // same arithmetic through shared memory: lane l sums rows l, l+32, ...
+        // (ascending), then the warp tree -- the order of the register form
+        const double* xc = nullptr;
+        if (owner >= 0) {
+          if constexpr (kCluster)
+            xc = cg::this_cluster().map_shared_rank(ccol, owner) + par * cstride;
+          else
+            xc = a.gcol + ((size_t)par * P + owner) * cstride;
+          for (int i = lane; i < ell; i += 32) vbuf[i] = kCluster ? xc[i] : __ldcg(xc + i);
+          xnorm = kCluster ? xc[ell] : __ldcg(xc + ell);
+        }
+        __syncwarp();
+        const bool halt = owner < 0 || !(xnorm > tol);  // qrcp.py:69-71
+        if (!halt) {
+          double sq = 0.0;
+          for (int i = lane; i < ell; i += 32)
+            if (i >= j) sq = __fma_rn(vbuf[i], vbuf[i], sq);
+          sq = warp_sum(sq);
+          const double alpha = vbuf[j];
+          __syncwarp();
+          const double norm = sqrt(sq);
+          double beta = 0.0, tau = 0.0, den = 1.0;
+          const bool zero = norm == 0.0;
+          if (!zero) {
+            beta = alpha >= 0.0 ? -norm : norm;
+            den = __dsub_rn(alpha, beta);
+            tau = __ddiv_rn(__dsub_rn(beta, alpha), beta);
+          }
+          const double rinv = zero ? 1.0 : __drcp_rn(den);
+          for (int i = lane; i < ell; i += 32)
+            if (i >= j) {
+              const double v = (i == j) ? 1.0 : (zero ? vbuf[i] : __dmul_rn(vbuf[i], rinv));
+              vbuf[i] = v;
+              tvbuf[i] = __dmul_rn(tau, v);
+            }
+          if (lane == 0) {
+            s_step[0] = beta;
+            s_step[1] = tau;
+          }
+        }
+        if (lane == 0) {
+          s_stepi[0] = halt ? -1 : owner;
+          s_stepi[1] = key_pos(wk);
+          if (!halt) {
+            const int pp = key_pos(wk);
+            const unsigned char oj = omap[j];
+            omap[j] = omap[pp];
+            omap[pp] = oj;
+          }
+          s_bkey = 0ull;
+          if constexpr (kCluster) {
+            for (int q = 0; q < P; ++q) s_key[(j + 2) % 3][q] = 0ull;
+          } else if (me == 0) {
+            a.gkey[(j + 2) % 3] = 0ull;
+          }
+        }
+      } else {   // ell <= 160: the column in registers
       if (owner >= 0) {
         const double* xc;
         if constexpr (kCluster) {
@@ -309,6 +367,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
           a.gkey[(j + 2) % 3] = 0ull;
         }
       }
+      }   // ell <= 160
     }
     __syncthreads();
     mark(0);
@@ -928,7 +987,7 @@ void select_pivots(Handle& h, int64_t ell, int64_t nt, int64_t want, const doubl
   if (want < 1 || want > std::min(ell, nt))
     throw InvalidArg("cannot select " + std::to_string(want) + " pivots from a " +
                      std::to_string(ell) + " x " + std::to_string(nt) + " sample");
-  if (ell > 160) throw InvalidArg("sample rows > 160 not supported by the pivot kernel");
+  if (ell > 1024) throw InvalidArg("sample rows > 1024 not supported by the pivot kernel");
   if (nt > 65535) throw InvalidArg("sample wider than 65535 columns");
   const bool grid = h.force_select == 1 ||
                     (h.force_select == 0 && nt > h.select_cluster_max_cols);

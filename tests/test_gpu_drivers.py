@@ -274,3 +274,17 @@ def test_panel_widths_vs_oracle(m, n, b, k, variant):
     assert np.linalg.norm(f.R - o.R) <= 1e-10 * np.linalg.norm(o.R)
     assert (f.counters.gemm_flops, f.counters.level2_flops) == \
         (o.counters.gemm_flops, o.counters.level2_flops)
+
+
+@pytest.mark.parametrize("k", [160, 200, 256])
+def test_ssrqrcp_wide_sample_vs_oracle(k):
+    """ssrqrcp's single block takes k pivots from a (k + p)-row sample: sample
+    rows past 160 go through the shared-memory pivot kernel's loop form."""
+    import paper_1509_06820_b200 as P
+    A = np.random.default_rng(k).standard_normal((1500, 1200))
+    f = P.ssrqrcp(A, k, P.RandomizedConfig(block=32, padding=8, seed=0))
+    o = port.ssrqrcp(A, k, 32, 8, 0)
+    np.testing.assert_array_equal(np.asarray(f.perm.forward), o.perm.forward)
+    assert np.linalg.norm(f.R - o.R) <= 1e-10 * np.linalg.norm(o.R)
+    assert (f.counters.gemm_flops, f.counters.level2_flops) == \
+        (o.counters.gemm_flops, o.counters.level2_flops)
