@@ -19,6 +19,14 @@ from .factorization import (
     q_columns,
     t_factor,
 )
+from .matio import (
+    MatrixFormatError,
+    PgmFormatError,
+    load_matrix_market,
+    load_pgm,
+    save_matrix_market,
+    save_pgm,
+)
 from .qrcp import column_norms, qr_blocked, qr_presorted
 from .randomized import DegenerateSampleError, RandomizedConfig, rqrcp, rsrqrcp, ssrqrcp
 from .rng import RngState, gaussian_matrix
@@ -32,7 +40,9 @@ __all__ = [
     "BlockReflectors",
     "DegenerateSampleError",
     "Factorization",
+    "MatrixFormatError",
     "OpCounters",
+    "PgmFormatError",
     "Permutation",
     "RandomizedConfig",
     "RngState",
@@ -41,6 +51,8 @@ __all__ = [
     "build_t_matrix",
     "column_norms",
     "gaussian_matrix",
+    "load_matrix_market",
+    "load_pgm",
     "lq_factor",
     "q_columns",
     "qr_blocked",
@@ -48,6 +60,8 @@ __all__ = [
     "qr_presorted",
     "rqrcp",
     "rsrqrcp",
+    "save_matrix_market",
+    "save_pgm",
     "ssrqrcp",
     "t_factor",
     "trqrcp",

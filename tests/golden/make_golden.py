@@ -212,6 +212,67 @@ def make_harness(rq):
     np.savez_compressed(os.path.join(OUT, "kat_harness.npz"), **rec)
 
 
+MATIO_CASES = {
+    "mm_array": b"%%MatrixMarket matrix array real general\n2 3\n1\n2\n3\n4\n5\n6\n",
+    "mm_sym": b"%%MatrixMarket matrix array real symmetric\n3 3\n1\n2\n3\n4\n5\n6\n",
+    "mm_coord_dup": b"%%MatrixMarket matrix coordinate real general\n% c\n3 3 4\n1 1 1.5\n2 3 2\n"
+                    b"1 1 0.25\n3 1 -1\n",
+    "mm_coord_sym": b"%%MatrixMarket matrix coordinate integer symmetric\n3 3 5\n1 1 1\n2 1 2\n"
+                    b"1 2 3\n3 2 4e-1\n2 1 0.1\n",
+    "mm_field": b"%%MatrixMarket matrix array complex general\n2 2\n1\n2\n3\n4\n",
+    "mm_count": b"%%MatrixMarket matrix array real general\n2 2\n1\n2\n3\n",
+    "mm_index": b"%%MatrixMarket matrix coordinate real general\n2 2 1\n3 1 1.0\n",
+    "mm_nan": b"%%MatrixMarket matrix array real general\n1 2\n1\nnan\n",
+    "mm_header": b"%MatrixMarket matrix array real general\n1 1\n1\n",
+    "mm_rect_sym": b"%%MatrixMarket matrix array real symmetric\n2 3\n1\n",
+    "mm_size": b"%%MatrixMarket matrix array real general\n2 x\n",
+    "mm_empty": b"",
+    "mm_nosize": b"%%MatrixMarket matrix array real general\n% only comment\n",
+    "mm_coord_bad": b"%%MatrixMarket matrix coordinate real general\n2 2 1\n1 1\n",
+    "pgm_p2": b"P2\n# c\n3 2\n255\n0 128 255\n1 2 3\n",
+    "pgm_p5_16": b"P5\n2 2\n65535\n\x00\x01\x00\x02\xff\xff\x00\x03",
+    "pgm_p5_inline": b"P5 2 1 255\n\x05\x06",
+    "pgm_magic": b"P3\n1 1\n1\n1\n",
+    "pgm_trunc": b"P5\n2 2\n255\n\x01\x02",
+    "pgm_maxval": b"P2\n1 1\n70000\n1\n",
+    "pgm_sample": b"P2\n1 1\n10\n11\n",
+    "pgm_width": b"P2\nx 1\n1\n",
+    "pgm_eoh": b"P2\n1",
+}
+
+
+def make_matio(rq):
+    """matio.py loaders on valid and malformed files: the parsed matrix, or
+    the error class and message (path replaced by {path})."""
+    import tempfile
+    from rqrcp import matio as M
+    rec = {}
+    d = tempfile.mkdtemp()
+    for name, raw in MATIO_CASES.items():
+        fn = os.path.join(d, name)
+        with open(fn, "wb") as fh:
+            fh.write(raw)
+        rec[name + "_bytes"] = np.frombuffer(raw, dtype=np.uint8)
+        try:
+            out = (M.load_matrix_market if name.startswith("mm") else M.load_pgm)(fn)
+            rec[name + "_out"] = out
+        except ValueError as e:
+            rec[name + "_err"] = np.array(type(e).__name__ + ": " + str(e).replace(fn, "{path}"))
+    g = np.random.default_rng(5)
+    A = g.standard_normal((7, 5))
+    M.save_matrix_market(A, os.path.join(d, "save.mtx"))
+    rec["save_A"] = A
+    rec["save_mtx"] = np.frombuffer(open(os.path.join(d, "save.mtx"), "rb").read(), dtype=np.uint8)
+    img = np.clip(g.uniform(-0.2, 1.2, (6, 9)), -1, 2)
+    rec["save_img"] = img
+    for asc in (0, 1):
+        for mv in (255, 1000):
+            fn = os.path.join(d, f"s{asc}{mv}.pgm")
+            M.save_pgm(img, fn, mv, bool(asc))
+            rec[f"save_pgm_{asc}_{mv}"] = np.frombuffer(open(fn, "rb").read(), dtype=np.uint8)
+    np.savez_compressed(os.path.join(OUT, "kat_matio.npz"), **rec)
+
+
 def main():
     sys.path.insert(0, REF)
     import rqrcp as rq  # the reference package
@@ -293,6 +354,7 @@ def main():
 
     make_qr(rq)
     make_harness(rq)
+    make_matio(rq)
 
     for name, driver, build, k, block, padding, seed, full in CASES + [CFG1]:
         recipe = build if isinstance(build, str) else ""
@@ -304,9 +366,9 @@ def main():
 
 
 if __name__ == "__main__":
-    if sys.argv[1:] in (["qr"], ["harness"]):   # one fixture only
+    if sys.argv[1:] in (["qr"], ["harness"], ["matio"]):   # one fixture only
         sys.path.insert(0, REF)
         import rqrcp as _rq
-        (make_qr if sys.argv[1] == "qr" else make_harness)(_rq)
+        {"qr": make_qr, "harness": make_harness, "matio": make_matio}[sys.argv[1]](_rq)
     else:
         main()

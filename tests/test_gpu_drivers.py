@@ -288,3 +288,18 @@ def test_ssrqrcp_wide_sample_vs_oracle(k):
     assert np.linalg.norm(f.R - o.R) <= 1e-10 * np.linalg.norm(o.R)
     assert (f.counters.gemm_flops, f.counters.level2_flops) == \
         (o.counters.gemm_flops, o.counters.level2_flops)
+
+
+def test_matrix_market_to_device_factorization(tmp_path):
+    """A MatrixMarket file parsed straight into column-major device memory
+    (matio.py loaders with device=) and factored there."""
+    import paper_1509_06820_b200 as P
+    from paper_1509_06820_b200 import matio
+    A = np.random.default_rng(9).standard_normal((300, 200))
+    matio.save_matrix_market(A, tmp_path / "a.mtx")
+    Ad = matio.load_matrix_market(tmp_path / "a.mtx", device="cuda")
+    assert Ad.is_cuda and Ad.stride() == (1, 300)
+    f = P.rqrcp(Ad, None, P.RandomizedConfig(block=32, padding=8, seed=0))
+    o = port.rqrcp(A, None, 32, 8, 0)
+    np.testing.assert_array_equal(f.perm.forward.cpu().numpy() if hasattr(f.perm.forward, "cpu")
+                                  else np.asarray(f.perm.forward), o.perm.forward)
