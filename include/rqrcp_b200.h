@@ -232,7 +232,8 @@ int64_t rq_launch_count(void);
 #define RQ_PROF_SAMPLE_UPDATE 6
 #define RQ_PROF_SWAP 7
 #define RQ_PROF_MISC 8
-#define RQ_PROF_NUM 9
+#define RQ_PROF_LIB_GEMM 9   /* cuBLAS DGEMM for plain scratch products (not this library's kernels) */
+#define RQ_PROF_NUM 10
 
 int rq_profile_enable(rq_handle_t h, int on);
 int rq_profile_reset(rq_handle_t h);

@@ -86,7 +86,7 @@ SIGNATURES = {
 }
 
 PROF_NAMES = ["sketch", "inner", "update", "small_gemm", "select", "panel", "sample_update",
-              "swap", "misc"]
+              "swap", "misc", "lib_gemm"]
 
 _lib = None
 _lock = threading.Lock()

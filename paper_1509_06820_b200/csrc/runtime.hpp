@@ -48,6 +48,7 @@ enum ProfCat {
   kProfSampleUpd,    // sample update
   kProfSwap,         // swap replay
   kProfMisc,         // copies, norms, fills
+  kProfLibGemm,      // cuBLAS DGEMM (plain scratch products, blas.cu)
   kProfNum
 };
 struct ProfStat {
@@ -107,6 +108,8 @@ class Handle {
   bool panel_halves = true;                 // 65..128-wide speculative panels as two fast halves
   bool degen_commit = true;                 // fast panel commits clearly degenerate R11 (block_finish resamples)
   bool finish_narrow = true;                // block_finish: 32-column tiles when 64 would leave SMs idle
+  bool use_cublas = true;                   // plain scratch GEMMs through cuBLAS DGEMM (blas.cu)
+  void* cublas = nullptr;                   // cublasHandle_t, created on first use
 
   bool use_rank_update = true;
   bool fast_panel = true;   // CholeskyQR2 + Householder reconstruction panel (panel_fast.cu)
@@ -256,6 +259,14 @@ bool block_finish(Handle& h, const FinishArgs& f, cudaStream_t s);
 
 // H (64 x N, ld ldh) = P^T C with P (K x 64) and C (K x N) column-major,
 // on at most max_ctas SMs (csrc/inner.cu); false when the shape does not qualify
+// cuBLAS DGEMM for a plain GEMM into a scratch operand (blas.cu): no Status
+// predicate, so never for state a speculative rewind must preserve; false
+// when disabled or not applicable (the caller then uses gemm())
+bool gemm_lib(Handle& h, bool ta, bool tb, int64_t m, int64_t n, int64_t k, double alpha,
+              const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
+              int64_t ldc, cudaStream_t s, int cat);
+void release_blas(Handle& h);
+
 bool inner_gemm(Handle& h, int64_t M, int64_t N, int64_t K, const double* P, int64_t ldp,
                 const double* C, int64_t ldc, double* H, int64_t ldh, cudaStream_t s,
                 const Status* st, int max_ctas, int cat);
