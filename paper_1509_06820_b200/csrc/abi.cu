@@ -286,6 +286,7 @@ int rq_set_option(rq_handle_t h, const char* name, int64_t value) {
     else if (n == "use_cublas") hh.use_cublas = value != 0;
     else if (n == "overlap_select") hh.overlap_select = value != 0;
     else if (n == "overlap_sel_ctas") hh.overlap_sel_ctas = (int)value;
+    else if (n == "sel_balance") hh.sel_balance = (int)value;
     else if (n == "su_gemm") hh.su_gemm = value != 0;
     else if (n == "overlap_inner") hh.overlap_inner = value != 0;
     else if (n == "overlap_panel_ctas") hh.overlap_panel_ctas = (int)value;

@@ -512,7 +512,17 @@ int Factor::overlap_split(int64_t i0, int64_t bw) const {
     const int64_t per = ell_ <= 72 ? 3 * 64 : 64;   // v5 columns per CTA
     const int cap = (sms * 80) / 148;
     const int64_t need = (nt1 + per - 1) / per;
-    if (need <= cap) P = std::max<int64_t>(P, need);
+    if (need <= cap) {
+      P = std::max<int64_t>(P, need);
+    } else {
+      // shared-memory v4: its step time grows with the columns per CTA
+      // (~ell*nt1/P), the update's with its rows (~mm*nt1/(sms-P)); balance
+      // the two per block.  Constant fitted on cfg5 (32768^2, ell = 136):
+      // fixed 16/24/32/44/60 CTAs gave select 2366/1689/1307/949/680 ms and
+      // update 1072/1140/1216/1356/1591 ms per factorization
+      const double mm = (double)(m_ - i0 - bw);
+      P = (int)(sms / (1.0 + 1e-6 * h_.sel_balance * mm * 136.0 / (double)ell_) + 0.5);
+    }
     if (nt1 <= 72 * 64) P = std::max(P, cap);
   }
   return std::max(16, std::min(P, sms - 16));
