@@ -863,8 +863,11 @@ void qr_blocked(Handle& h, int64_t m, int64_t n, int64_t k, int64_t b, double* w
       if (!gemm_lib(h, true, false, bw, nc, mm, 1.0, Yb, ldy, C, ldw, 0.0, G, bw, s, kProfInner) &&
           !inner_gemm(h, bw, nc, mm, Yb, ldy, C, ldw, G, bw, s, nullptr, 0, kProfInner))
         gemm(h, true, false, bw, nc, mm, 1.0, Yb, ldy, C, ldw, 0.0, G, bw, s);
-      gemm(h, true, false, bw, nc, bw, 1.0, T, b, G, bw, 0.0, X, bw, s);
-      gemm(h, false, false, mm, nc, bw, -1.0, Yb, ldy, X, bw, 1.0, C, ldw, s);
+      if (!gemm_lib(h, true, false, bw, nc, bw, 1.0, T, b, G, bw, 0.0, X, bw, s, kProfSmallGemm))
+        gemm(h, true, false, bw, nc, bw, 1.0, T, b, G, bw, 0.0, X, bw, s);
+      if (!gemm_lib(h, false, false, mm, nc, bw, -1.0, Yb, ldy, X, bw, 1.0, C, ldw, s,
+                    kProfSmallGemm))
+        gemm(h, false, false, mm, nc, bw, -1.0, Yb, ldy, X, bw, 1.0, C, ldw, s);
       if (c) {
         c->gemm_flops += 4 * mm * bw * nc + bw * bw * nc;
         c->bytes_touched += 8 * (2 * mm * nc + mm * bw + bw * nc);
@@ -898,8 +901,11 @@ void q_columns(Handle& h, int64_t m, int64_t nref, int64_t cols, const double* Y
     if (!gemm_lib(h, true, false, bw, nc, mm, 1.0, Yb, ldy, C, ldq, 0.0, G, bw, s, kProfInner) &&
         !inner_gemm(h, bw, nc, mm, Yb, ldy, C, ldq, G, bw, s, nullptr, 0, kProfInner))
       gemm(h, true, false, bw, nc, mm, 1.0, Yb, ldy, C, ldq, 0.0, G, bw, s);
-    gemm(h, false, false, bw, nc, bw, 1.0, T, b, G, bw, 0.0, X, bw, s);
-    gemm(h, false, false, mm, nc, bw, -1.0, Yb, ldy, X, bw, 1.0, C, ldq, s);
+    if (!gemm_lib(h, false, false, bw, nc, bw, 1.0, T, b, G, bw, 0.0, X, bw, s, kProfSmallGemm))
+      gemm(h, false, false, bw, nc, bw, 1.0, T, b, G, bw, 0.0, X, bw, s);
+    if (!gemm_lib(h, false, false, mm, nc, bw, -1.0, Yb, ldy, X, bw, 1.0, C, ldq, s,
+                  kProfSmallGemm))
+      gemm(h, false, false, mm, nc, bw, -1.0, Yb, ldy, X, bw, 1.0, C, ldq, s);
   }
 }
 
