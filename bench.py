@@ -19,6 +19,7 @@ with CUDA events, max over ranks.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -349,6 +350,10 @@ def main():
         around every kernel launch (per-family durations for the roofline)."""
         _abi.check(lib.rq_profile_reset(h))
         _abi.check(lib.rq_profile_enable(h, 1 if profile else 0))
+        # no Python garbage collection pauses between the K calls (a gen-2
+        # pass with torch loaded idles the GPU for tens of ms)
+        gc.collect()
+        gc.disable()
         l0 = lib.rq_launch_count()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         barrier()
@@ -357,18 +362,32 @@ def main():
         # headline pass's launches
         torch.cuda.nvtx.range_push("timed" if not profile else "profiled")
         e0.record(stream)
+        marks = []   # per-step events (idle gaps between calls show up here)
+        f_ = None
         for _ in range(args.steps):
+            f_ = None   # the previous result is released before the next call
             f_ = step(P, cfg, A, None)
+            marks.append(torch.cuda.Event(enable_timing=True))
+            marks[-1].record(stream)
         e1.record(stream)
         torch.cuda.nvtx.range_pop()
         barrier()
         t1 = time.time()
         _abi.check(lib.rq_profile_enable(h, 0))
+        gc.enable()
+        steps_ms = [round(a_.elapsed_time(b_), 3) for a_, b_ in zip([e0] + marks[:-1], marks)]
+        timed_pass.steps_ms = steps_ms
         return f_, e0.elapsed_time(e1), lib.rq_launch_count() - l0, sampler.window(t0, t1)
 
     # headline pass without per-launch events, then the same K steps again
     # with them (kernel shares and the roofline's per-launch durations)
+    # the warm-up's last result would otherwise stay alive through the timed
+    # pass: three result sets at once make the caching allocator grow (cudaMalloc)
+    # inside the second timed call
+    f = None
     f, ms, launches, clk = timed_pass(False)
+    f = None
+    steps_ms = timed_pass.steps_ms
     f, ms_prof, _, clk_prof = timed_pass(True)
     sampler.__exit__(None, None, None)
     n_cat = len(_abi.PROF_NAMES)
@@ -480,6 +499,7 @@ def main():
             "gpu_launches": int(launches),
             "clocks": clk,
             "kernels": kernels,
+            "steps_ms": steps_ms,
             "profiled_pass": {"ms_per_step": ms_prof / args.steps, "clocks": clk_prof,
                               "note": "same K steps re-run with CUDA events around every "
                                       "library launch; `kernels` and `roofline` come from it"},
