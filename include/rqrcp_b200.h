@@ -212,7 +212,12 @@ int rq_omega_fill(uint64_t k0, uint64_t k1, uint64_t raw, double* out, int64_t c
  * "overlap_sel_ctas" (next block's select beside the trailing update),
  * "su_gemm", "overlap_inner", "overlap_panel_ctas" (inner product beside the
  * fast panel), "block_finish" (X, R12 and the sample update fused per column
- * tile), "profile_trace", "debug_timers" */
+ * tile), "sel_balance" (x 1e-6: SM share of a shared-memory select beside the
+ * trailing update, from the trailing rows), "use_cublas" (1 = plain scratch
+ * products through cuBLAS DGEMM, 0 = the in-tree DMMA GEMM), "omega_ahead",
+ * "floor_lookahead", "t_inverse", "panel_halves", "degen_commit",
+ * "finish_narrow", "inner32", "panel_rows_per_cta", "profile_trace",
+ * "debug_timers"; unknown names return RQ_ERR_INVALID */
 int rq_set_option(rq_handle_t h, const char* name, int64_t value);
 
 /* debug: phase timers written by the kernels when "debug_timers" is set */
