@@ -419,9 +419,9 @@ def main():
         ach = FL[i] / (MS[i] * 1e-3) / 1e12
         pk = peak["dmma_f64_tflops"] if peak else 37.2
         kname = {"update": "rank_update_big_kernel<b> (C -= Y X, K = b, persistent 128x64 tiles)",
-                 "inner": "inner_kernel<b> / gemm_f64_kernel (G = Y^T C, split-K)",
-                 "sketch": "gemm_f64_kernel (B = Omega A)",
-                 "small_gemm": "gemm_f64_kernel (small products)"}.get(dom, dom)
+                 "inner": "tc_gemm_kernel (G = Y^T C, split-K)",
+                 "sketch": "tc_gemm_kernel (B = Omega A)",
+                 "small_gemm": "tc_gemm_kernel (small products)"}.get(dom, dom)
         roofline = {"bound": "tensor", "kernel": kname, "achieved": ach,
                     "peak": pk, "unit": "TFLOP/s", "frac": ach / pk,
                     "traffic": traffic_from_profiles(dom),
@@ -431,15 +431,6 @@ def main():
                     "algorithmic_flops_per_launch": FL[i] / max(L[i], 1),
                     "avg_launch_us": MS[i] * 1e3 / max(L[i], 1),
                     "share": kernels[dom]["share"]}
-        if "lib_gemm" in kernels:
-            # plain scratch products go to cuBLAS DGEMM; reported beside our
-            # own dominant kernel (never as it), with its share of the step
-            j = _abi.PROF_NAMES.index("lib_gemm")
-            lach = FL[j] / (MS[j] * 1e-3) / 1e12
-            roofline["library_gemm"] = {"kernel": "cuBLAS DGEMM (sketch, TRQRCP/unoverlapped G, "
-                                                  "TUXV and dense-Q products)",
-                                        "achieved": lach, "frac": lach / pk,
-                                        "share": kernels["lib_gemm"]["share"]}
     res_counters = f.counters
     if sharded:
         from paper_1509_06820_b200.factorization import OpCounters

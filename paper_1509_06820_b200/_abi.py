@@ -86,7 +86,7 @@ SIGNATURES = {
 }
 
 PROF_NAMES = ["sketch", "inner", "update", "small_gemm", "select", "panel", "sample_update",
-              "swap", "misc", "lib_gemm"]
+              "swap", "misc"]
 
 _lib = None
 _lock = threading.Lock()

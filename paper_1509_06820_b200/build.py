@@ -77,7 +77,7 @@ def build(force=False, verbose=False, extra=()):
     objs = [os.path.join(OBJ, os.path.basename(s)[:-3] + ".o") for s in srcs]
     if force or todo or _stale(LIB, objs):
         cmd = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", *objs, _npyrandom(), "-o", LIB,
-               "-lcudart_static", "-lcublas", "-Xlinker", "-rpath=/usr/local/cuda/lib64",
+               "-lcudart_static", "-Xlinker", "-rpath=/usr/local/cuda/lib64",
                "-lrt", "-lpthread", "-ldl", "-lm"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

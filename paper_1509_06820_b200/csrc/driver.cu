@@ -200,11 +200,9 @@ void Factor::first_sample() {
     draw_omega(ell_, m_);
     om = om_d_;
   }
-  // the sketch is a plain GEMM outside the speculative chain (library DGEMM)
-  if (!gemm_lib(h_, false, false, ell_, n_, m_, 1.0, om, ell_, p_.work, p_.ldw, 0.0, B_, ell_, s_,
-                kProfSketch))
-    gemm(h_, false, false, ell_, n_, m_, 1.0, om, ell_, p_.work, p_.ldw, 0.0, B_, ell_, s_, nullptr,
-         kProfSketch);
+  // the sketch is a plain GEMM outside the speculative chain (tc_gemm.cu)
+  gemm(h_, false, false, ell_, n_, m_, 1.0, om, ell_, p_.work, p_.ldw, 0.0, B_, ell_, s_, nullptr,
+       kProfSketch);
   c_.gemm_flops += 2 * ell_ * m_ * n_;
   touch(c_, ell_ * m_ + m_ * n_ + ell_ * n_);
 }
@@ -215,11 +213,8 @@ void Factor::fresh_sample(int64_t i0) {
   const int64_t mm = m_ - i0, nt = n_ - i0;
   const double* om = omega_take(ell_, mm);
   const double* At = p_.work + i0 + i0 * p_.ldw;
-  // fresh_sample runs synchronously (after sync()): a plain library GEMM
-  if (!gemm_lib(h_, false, false, ell_, nt, mm, 1.0, om, ell_, At, p_.ldw, 0.0, B_, ell_, s_,
-                kProfSketch))
-    gemm(h_, false, false, ell_, nt, mm, 1.0, om, ell_, At, p_.ldw, 0.0, B_, ell_, s_, nullptr,
-         kProfSketch);
+  gemm(h_, false, false, ell_, nt, mm, 1.0, om, ell_, At, p_.ldw, 0.0, B_, ell_, s_, nullptr,
+       kProfSketch);
   c_.gemm_flops += 2 * ell_ * mm * nt;
   touch(c_, ell_ * mm + mm * nt + ell_ * nt);
   if (p_.truncated && i0) {
@@ -267,6 +262,9 @@ bool Factor::panel_halves(int64_t i0, int64_t got) {
   double* Y2 = Y1 + 64 + 64 * p_.ldy;
   double* G = (double*)h_.buf("ph_G", (size_t)64 * 128 * 8, s_);
   double* X = G + 64 * 64;
+  // the first half commits in place; keep the selected columns so a decline
+  // of the second half rewinds to them (restored below, on the device)
+  halves_guard(h_, P1, p_.ldw, mm, got, st_, false, i0, Y1, p_.ldy, p_.tau + i0, s_);
   PanelOut o1{};
   o1.Y = Y1; o1.ldy = p_.ldy; o1.tau = p_.tau + i0;
   o1.T = T_; o1.ldt = b_;
@@ -300,6 +298,7 @@ bool Factor::panel_halves(int64_t i0, int64_t got) {
   gemm(h_, false, false, 64, h2, 64, -1.0, T_, b_, X, 64, 0.0, T_ + 64 * b_, b_, s_, st_,
        kProfPanel);
   fill2d(T_ + 64, b_, h2, 64, 0.0, s_, st_);
+  halves_guard(h_, P1, p_.ldw, mm, got, st_, true, i0, Y1, p_.ldy, p_.tau + i0, s_);
   return true;
 }
 
@@ -364,8 +363,6 @@ void Factor::stages(int64_t i0, int64_t bw, Counters& c, bool defer_trailing, bo
       return;
     }
     if (!g_ready &&   // else panel_overlap_inner() assembled G = Y^T C
-        !gemm_lib(h_, true, false, bw, nt2, mm, 1.0, Yb, p_.ldy, C, p_.ldw, 0.0, G_, bw, s_,
-                  kProfInner) &&
         !inner_gemm(h_, bw, nt2, mm, Yb, p_.ldy, C, p_.ldw, G_, bw, s_, st_, 0, kProfInner))
       gemm(h_, true, false, bw, nt2, mm, 1.0, Yb, p_.ldy, C, p_.ldw, 0.0, G_, bw, s_, st_,
            kProfInner);
@@ -395,9 +392,7 @@ void Factor::stages(int64_t i0, int64_t bw, Counters& c, bool defer_trailing, bo
     return;
   }
   // G = Yb^T A[i0:, i0+bw:] - (Yb^T Y[i0:, :i0]) W[i0+bw:, :i0]^T
-  if (!gemm_lib(h_, true, false, bw, nt2, mm, 1.0, Yb, p_.ldy, p_.work + i0 + (i0 + bw) * p_.ldw,
-                p_.ldw, 0.0, G_, bw, s_, kProfInner) &&
-      !inner_gemm(h_, bw, nt2, mm, Yb, p_.ldy, p_.work + i0 + (i0 + bw) * p_.ldw, p_.ldw, G_, bw,
+  if (!inner_gemm(h_, bw, nt2, mm, Yb, p_.ldy, p_.work + i0 + (i0 + bw) * p_.ldw, p_.ldw, G_, bw,
                   s_, st_, 0, kProfInner))
     gemm(h_, true, false, bw, nt2, mm, 1.0, Yb, p_.ldy, p_.work + i0 + (i0 + bw) * p_.ldw, p_.ldw,
          0.0, G_, bw, s_, st_, kProfInner);
@@ -860,14 +855,10 @@ void qr_blocked(Handle& h, int64_t m, int64_t n, int64_t k, int64_t b, double* w
       // apply_block_reflection(transpose=True) (kernels.py:166-181)
       double* C = work + i0 + (i0 + bw) * ldw;
       const double* Yb = Y + i0 + i0 * ldy;
-      if (!gemm_lib(h, true, false, bw, nc, mm, 1.0, Yb, ldy, C, ldw, 0.0, G, bw, s, kProfInner) &&
-          !inner_gemm(h, bw, nc, mm, Yb, ldy, C, ldw, G, bw, s, nullptr, 0, kProfInner))
+      if (!inner_gemm(h, bw, nc, mm, Yb, ldy, C, ldw, G, bw, s, nullptr, 0, kProfInner))
         gemm(h, true, false, bw, nc, mm, 1.0, Yb, ldy, C, ldw, 0.0, G, bw, s);
-      if (!gemm_lib(h, true, false, bw, nc, bw, 1.0, T, b, G, bw, 0.0, X, bw, s, kProfSmallGemm))
-        gemm(h, true, false, bw, nc, bw, 1.0, T, b, G, bw, 0.0, X, bw, s);
-      if (!gemm_lib(h, false, false, mm, nc, bw, -1.0, Yb, ldy, X, bw, 1.0, C, ldw, s,
-                    kProfSmallGemm))
-        gemm(h, false, false, mm, nc, bw, -1.0, Yb, ldy, X, bw, 1.0, C, ldw, s);
+      gemm(h, true, false, bw, nc, bw, 1.0, T, b, G, bw, 0.0, X, bw, s);
+      gemm(h, false, false, mm, nc, bw, -1.0, Yb, ldy, X, bw, 1.0, C, ldw, s);
       if (c) {
         c->gemm_flops += 4 * mm * bw * nc + bw * bw * nc;
         c->bytes_touched += 8 * (2 * mm * nc + mm * bw + bw * nc);
@@ -898,14 +889,10 @@ void q_columns(Handle& h, int64_t m, int64_t nref, int64_t cols, const double* Y
     const double* Yb = Y + i0 + i0 * ldy;
     t_factor(h, Yb, ldy, mm, bw, tau + i0, T, b, s);
     double* C = Q + i0 + i0 * ldq;
-    if (!gemm_lib(h, true, false, bw, nc, mm, 1.0, Yb, ldy, C, ldq, 0.0, G, bw, s, kProfInner) &&
-        !inner_gemm(h, bw, nc, mm, Yb, ldy, C, ldq, G, bw, s, nullptr, 0, kProfInner))
+    if (!inner_gemm(h, bw, nc, mm, Yb, ldy, C, ldq, G, bw, s, nullptr, 0, kProfInner))
       gemm(h, true, false, bw, nc, mm, 1.0, Yb, ldy, C, ldq, 0.0, G, bw, s);
-    if (!gemm_lib(h, false, false, bw, nc, bw, 1.0, T, b, G, bw, 0.0, X, bw, s, kProfSmallGemm))
-      gemm(h, false, false, bw, nc, bw, 1.0, T, b, G, bw, 0.0, X, bw, s);
-    if (!gemm_lib(h, false, false, mm, nc, bw, -1.0, Yb, ldy, X, bw, 1.0, C, ldq, s,
-                  kProfSmallGemm))
-      gemm(h, false, false, mm, nc, bw, -1.0, Yb, ldy, X, bw, 1.0, C, ldq, s);
+    gemm(h, false, false, bw, nc, bw, 1.0, T, b, G, bw, 0.0, X, bw, s);
+    gemm(h, false, false, mm, nc, bw, -1.0, Yb, ldy, X, bw, 1.0, C, ldq, s);
   }
 }
 
@@ -939,9 +926,7 @@ TuxvResult run_tuxv(Handle& h, const TuxvParams& p) {
   int64_t j = 1;
   while (true) {
     // Zc = A V[:, :r]; U, X from qr_blocked(Zc)
-    if (!gemm_lib(h, false, false, m, r, n, 1.0, p.A, p.lda, p.V, p.ldv, 0.0, Zt, m, s,
-                  kProfSmallGemm))
-      gemm(h, false, false, m, r, n, 1.0, p.A, p.lda, p.V, p.ldv, 0.0, Zt, m, s);
+    gemm(h, false, false, m, r, n, 1.0, p.A, p.lda, p.V, p.ldv, 0.0, Zt, m, s);
     c.gemm_flops += 2 * m * n * r;
     c.bytes_touched += 8 * (m * n + n * r + m * r);
     qr_blocked(h, m, r, r, b, Zt, m, Yq, m, tq, &c, s);
@@ -950,9 +935,7 @@ TuxvResult run_tuxv(Handle& h, const TuxvParams& p) {
     out.x_lower = 0;
     if (j >= p.j_max) break;
     // Zr = U^T A (r x n); X, V = lq_factor(Zr)
-    if (!gemm_lib(h, true, false, r, n, m, 1.0, p.U, p.ldu, p.A, p.lda, 0.0, Z, r, s,
-                  kProfSmallGemm))
-      gemm(h, true, false, r, n, m, 1.0, p.U, p.ldu, p.A, p.lda, 0.0, Z, r, s);
+    gemm(h, true, false, r, n, m, 1.0, p.U, p.ldu, p.A, p.lda, 0.0, Z, r, s);
     c.gemm_flops += 2 * m * n * r;
     c.bytes_touched += 8 * (m * r + r * n);
     transpose(Z, r, Zt, n, r, n, s);

@@ -100,6 +100,8 @@ void gemm(Handle& h, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double a
   if (ta && !tb && M == 64 && alpha == 1.0 && beta == 0.0 &&
       inner_gemm(h, M, N, K, A, lda, B, ldb, C, ldc, s, st, 0, cat))
     return;
+  if (K > 0 && tc_gemm(h, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, s, st, cat))
+    return;
   // algorithmic traffic: read A, B (+ C when beta != 0), write C
   const double bytes = 8.0 * ((double)M * K + (double)K * N + (double)M * N * (beta != 0.0 ? 2 : 1));
   ProfScope prof(h, cat, 2.0 * (double)M * N * K, bytes, s);

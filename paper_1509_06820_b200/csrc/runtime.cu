@@ -107,7 +107,6 @@ cudaStream_t Handle::omega_stream() {
 }
 
 Handle::~Handle() {
-  release_blas(*this);
   if (omega_ != nullptr) {
     cudaStreamDestroy(omega_);
     cudaEventDestroy(ev_omega);

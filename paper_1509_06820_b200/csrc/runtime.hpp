@@ -48,7 +48,6 @@ enum ProfCat {
   kProfSampleUpd,    // sample update
   kProfSwap,         // swap replay
   kProfMisc,         // copies, norms, fills
-  kProfLibGemm,      // cuBLAS DGEMM (plain scratch products, blas.cu)
   kProfNum
 };
 struct ProfStat {
@@ -108,8 +107,9 @@ class Handle {
   bool panel_halves = true;                 // 65..128-wide speculative panels as two fast halves
   bool degen_commit = true;                 // fast panel commits clearly degenerate R11 (block_finish resamples)
   bool finish_narrow = true;                // block_finish: 32-column tiles when 64 would leave SMs idle
-  bool use_cublas = true;                   // plain scratch GEMMs through cuBLAS DGEMM (blas.cu)
-  void* cublas = nullptr;                   // cublasHandle_t, created on first use
+  bool use_tc = true;                       // plain GEMMs through tc_gemm (tc_gemm.cu)
+  int tc_variant = -1;                      // tc_gemm tile family override (-1 = by shape)
+  int tc_splits = 0;                        // tc_gemm split-K override (0 = by shape)
 
   bool use_rank_update = true;
   bool fast_panel = true;   // CholeskyQR2 + Householder reconstruction panel (panel_fast.cu)
@@ -177,6 +177,12 @@ class Handle {
 void gemm(Handle& h, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha,
           const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
           int64_t ldc, cudaStream_t s, const Status* st = nullptr, int cat = kProfSmallGemm);
+
+// second-generation DMMA GEMM (tc_gemm.cu); false when disabled or op(A) and
+// op(B) are both transposed (the caller then uses gemm_f64_kernel)
+bool tc_gemm(Handle& h, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha,
+             const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
+             int64_t ldc, cudaStream_t s, const Status* st, int cat);
 
 // persistent C -= Y X for K <= 64 (rank_update.cu); false if not applicable
 bool rank_update(Handle& h, int64_t M, int64_t N, int64_t K, const double* Y, int64_t ldy,
@@ -260,13 +266,6 @@ bool block_finish(Handle& h, const FinishArgs& f, cudaStream_t s);
 
 // H (64 x N, ld ldh) = P^T C with P (K x 64) and C (K x N) column-major,
 // on at most max_ctas SMs (csrc/inner.cu); false when the shape does not qualify
-// cuBLAS DGEMM for a plain GEMM into a scratch operand (blas.cu): no Status
-// predicate, so never for state a speculative rewind must preserve; false
-// when disabled or not applicable (the caller then uses gemm())
-bool gemm_lib(Handle& h, bool ta, bool tb, int64_t m, int64_t n, int64_t k, double alpha,
-              const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
-              int64_t ldc, cudaStream_t s, int cat);
-void release_blas(Handle& h);
 
 bool inner_gemm(Handle& h, int64_t M, int64_t N, int64_t K, const double* P, int64_t ldp,
                 const double* C, int64_t ldc, double* H, int64_t ldh, cudaStream_t s,
@@ -306,6 +305,10 @@ void frob_norm(Handle& h, const double* A, int64_t m, int64_t n, int64_t lda, do
                cudaStream_t s);
 void copy2d(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows,
             int64_t cols, cudaStream_t s, const Status* st = nullptr);
+// snapshot (restore = false) / conditional restore of a two-half panel's
+// columns, reflectors and level-2 counters (small.cu halves_guard_kernel)
+void halves_guard(Handle& h, double* work, int64_t ldw, int64_t mm, int64_t cols, Status* st,
+                  bool restore, int64_t i0, double* Y, int64_t ldy, double* tau, cudaStream_t s);
 void fill2d(double* dst, int64_t ldd, int64_t rows, int64_t cols, double v, cudaStream_t s,
             const Status* st = nullptr);
 void transpose(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows,

@@ -341,6 +341,46 @@ __global__ void copy2d_kernel(const double* src, int64_t lds, double* dst, int64
     dst[r + c * ldd] = src[r + c * lds];
   }
 }
+// Two-half panel guard (driver.cu panel_halves).  The reference eliminates a
+// panel on a copy and commits it only once its whole R diagonal is confirmed
+// (randomized.py:221-239); the two-half panel writes its first half in place
+// before the second half is factored.  restore = 0: snapshot the selected
+// columns and the level-2 counters (skipped when the queue already aborted).
+// restore = 1: if the block's fast panel declined (Status.abort ==
+// kAbortPanelFast at i0), put the columns and counters back and clear the
+// first half's reflectors, so the rewind redoes the panel on the original
+// columns exactly as the reference would.
+__global__ void halves_guard_kernel(double* work, int64_t ldw, int64_t mm, int64_t cols,
+                                    double* snap, int64_t* sst, Status* st, int restore,
+                                    int64_t i0, double* Y, int64_t ldy, double* tau) {
+  if (!restore) {
+    if (aborted(st)) return;
+  } else {
+    const int code = *((volatile const int*)&st->abort);
+    if (code != kAbortPanelFast || st->abort_i0 != i0) return;
+  }
+  const int64_t total = mm * cols;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t e = t0; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e % mm, c = e / mm;
+    if (!restore) {
+      snap[e] = work[r + c * ldw];
+    } else {
+      work[r + c * ldw] = snap[e];
+      Y[r + c * ldy] = 0.0;
+    }
+  }
+  if (t0 == 0) {
+    if (!restore) {
+      sst[0] = st->level2;
+      sst[1] = st->l2bytes;
+    } else {
+      st->level2 = sst[0];
+      st->l2bytes = sst[1];
+    }
+  }
+  if (restore && t0 < cols) tau[t0] = 0.0;
+}
 __global__ void fill2d_kernel(double* dst, int64_t ldd, int64_t rows, int64_t cols, double v,
                               const Status* st) {
   if (aborted(st)) return;
@@ -707,6 +747,16 @@ void copy2d(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t ro
             int64_t cols, cudaStream_t s, const Status* st) {
   if (rows <= 0 || cols <= 0) return;
   copy2d_kernel<<<grid_for(rows * cols, 148), 256, 0, s>>>(src, lds, dst, ldd, rows, cols, st);
+  RQ_CHECK_LAUNCH();
+  count_launch();
+}
+
+void halves_guard(Handle& h, double* work, int64_t ldw, int64_t mm, int64_t cols, Status* st,
+                  bool restore, int64_t i0, double* Y, int64_t ldy, double* tau, cudaStream_t s) {
+  double* snap = (double*)h.buf("halves_snap", (size_t)mm * cols * 8, s);
+  int64_t* sst = (int64_t*)h.buf("halves_sst", 16, s);
+  halves_guard_kernel<<<grid_for(mm * cols, 148), 256, 0, s>>>(work, ldw, mm, cols, snap, sst, st,
+                                                               restore ? 1 : 0, i0, Y, ldy, tau);
   RQ_CHECK_LAUNCH();
   count_launch();
 }
