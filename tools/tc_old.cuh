@@ -29,14 +29,14 @@
 // STAGES-deep cp.async ring.  K is split across blockIdx.z when the output
 // grid cannot fill the SMs; partial planes are summed in a fixed order
 // (gemm_reduce_kernel), so results are deterministic run to run.
-#pragma once
+
 
 #include "gemm.cuh"
 
 namespace rq {
 
 template <bool TA, bool TB, int BM, int BN, int BK, int WM, int WN, int STAGES>
-struct TcCfg {
+struct TcCfgOld {
   static constexpr int kWarpsM = BM / WM, kWarpsN = BN / WN;
   static constexpr int kThreads = kWarpsM * kWarpsN * 32;
   static constexpr int FM = WM / 8, FN = WN / 8;
@@ -55,20 +55,20 @@ struct TcCfg {
 
 // logical row of fragment a held by lane row fr (see the header comment)
 template <bool TA>
-RQ_DEV int tc_row(int wm0, int a, int fr) {
+RQ_DEV int tc_row_old(int wm0, int a, int fr) {
   return TA ? wm0 + 8 * a + fr : wm0 + 16 * (a >> 1) + 2 * fr + (a & 1);
 }
 // logical column of fragment b, MMA column j
 template <bool TB>
-RQ_DEV int tc_col(int wn0, int b, int j) {
+RQ_DEV int tc_col_old(int wn0, int b, int j) {
   return TB ? wn0 + 16 * (b >> 1) + 2 * j + (b & 1) : wn0 + 8 * b + j;
 }
 
 template <bool TA, bool TB, int BM, int BN, int BK, int WM, int WN, int STAGES, int VEC,
           int MINB = 1, bool DBUF = true>
-__global__ void __launch_bounds__(TcCfg<TA, TB, BM, BN, BK, WM, WN, STAGES>::kThreads, MINB)
-    tc_gemm_kernel(GemmArgs g) {
-  using Cfg = TcCfg<TA, TB, BM, BN, BK, WM, WN, STAGES>;
+__global__ void __launch_bounds__(TcCfgOld<TA, TB, BM, BN, BK, WM, WN, STAGES>::kThreads, MINB)
+    tc_gemm_kernel_old(GemmArgs g) {
+  using Cfg = TcCfgOld<TA, TB, BM, BN, BK, WM, WN, STAGES>;
   constexpr int NT = Cfg::kThreads, FM = Cfg::FM, FN = Cfg::FN;
   constexpr int LDA = Cfg::kLdA, LDB = Cfg::kLdB;
   if (aborted(g.st)) return;
@@ -199,48 +199,23 @@ __global__ void __launch_bounds__(TcCfg<TA, TB, BM, BN, BK, WM, WN, STAGES>::kTh
 
   // epilogue: acc[a][b][e] = C[tc_row(a, fr)][tc_col(b, 2 fk + e)]
   const bool split = g.splits > 1;
-  if (!split && g.beta != 0.0) {
-    // the old C values of a fragment row are loaded together before any of
-    // them is stored (one memory round trip per row instead of one per
-    // element: each store would otherwise order the next load behind it)
-#pragma unroll
-    for (int a = 0; a < FM; ++a) {
-      const int64_t r = m0 + tc_row<TA>(wm0, a, fr);
-      if (r >= g.M) continue;
-      double old[FN][2];
-#pragma unroll
-      for (int b = 0; b < FN; ++b)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int64_t c = n0 + tc_col<TB>(wn0, b, 2 * fk + e);
-          old[b][e] = c < g.N ? __ldcg(g.C + r + c * g.ldc) : 0.0;
-        }
-#pragma unroll
-      for (int b = 0; b < FN; ++b)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int64_t c = n0 + tc_col<TB>(wn0, b, 2 * fk + e);
-          if (c < g.N) g.C[r + c * g.ldc] = gemm_combine(acc[a][b][e], old[b][e], g.alpha, g.beta);
-        }
-    }
-    return;
-  }
   double* P = split ? g.partial + (size_t)blockIdx.z * (size_t)(g.M * g.N) : nullptr;
 #pragma unroll
   for (int a = 0; a < FM; ++a) {
-    const int64_t r = m0 + tc_row<TA>(wm0, a, fr);
+    const int64_t r = m0 + tc_row_old<TA>(wm0, a, fr);
     if (r >= g.M) continue;
 #pragma unroll
     for (int b = 0; b < FN; ++b) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int64_t c = n0 + tc_col<TB>(wn0, b, 2 * fk + e);
+        const int64_t c = n0 + tc_col_old<TB>(wn0, b, 2 * fk + e);
         if (c >= g.N) continue;
         if (split) {
           P[r + c * g.M] = acc[a][b][e];
         } else {
           double* cp = g.C + r + c * g.ldc;
-          *cp = gemm_combine(acc[a][b][e], 0.0, g.alpha, 0.0);
+          const double old = g.beta == 0.0 ? 0.0 : *cp;
+          *cp = gemm_combine(acc[a][b][e], old, g.alpha, g.beta);
         }
       }
     }

@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "tc_gemm.cuh"
+#include "tc_old.cuh"
 
 using namespace rq;
 
@@ -104,8 +105,9 @@ void run(const char* cfgname, Kern kern, int threads, size_t smem, int BM, int B
   g.kchunk = best > 1 ? kc : s.K;
   g.splits = best > 1 ? (int)((s.K + kc - 1) / kc) : 1;
   g.partial = g_partial;
+  const bool oned = std::string(cfgname).rfind("tc<", 0) == 0;
   auto launch = [&] {
-    dim3 grid((unsigned)gm, (unsigned)gn, (unsigned)g.splits);
+    dim3 grid = oned ? dim3((unsigned)(gm * gn * g.splits)) : dim3((unsigned)gm, (unsigned)gn, (unsigned)g.splits);
     kern<<<grid, threads, smem>>>(g);
     if (g.splits > 1) gemm_reduce_kernel<<<148 * 8, 256>>>(g);
   };
@@ -142,6 +144,11 @@ void run(const char* cfgname, Kern kern, int threads, size_t smem, int BM, int B
       tc_gemm_kernel<TA, TB, BM, BN, BK, WM, WN, ST, 2, MINB, DBUF>,                            \
       TcCfg<TA, TB, BM, BN, BK, WM, WN, ST>::kThreads, TcCfg<TA, TB, BM, BN, BK, WM, WN, ST>::kSmem, \
       BM, BN, BK, s, A, B, reps, cub_ms)
+#define TCO(TA, TB, BM, BN, BK, WM, WN, ST, MINB, DBUF)                                          \
+  run("tcold<" #BM "x" #BN "x" #BK ",w" #WM "x" #WN ",s" #ST ",minb" #MINB ",db" #DBUF ">",       \
+      tc_gemm_kernel_old<TA, TB, BM, BN, BK, WM, WN, ST, 2, MINB, DBUF>,                            \
+      TcCfgOld<TA, TB, BM, BN, BK, WM, WN, ST>::kThreads, TcCfgOld<TA, TB, BM, BN, BK, WM, WN, ST>::kSmem, \
+      BM, BN, BK, s, A, B, reps, cub_ms)
 #define OLD(TA, TB, BM, BN, BK, WM, WN, ST)                                                      \
   run("old<" #BM "x" #BN "x" #BK ",w" #WM "x" #WN ",s" #ST ">",                                 \
       gemm_f64_kernel<TA, TB, BM, BN, BK, WM, WN, ST, 2>,                                        \
@@ -170,28 +177,15 @@ void sweep(const Shape& s, const double* A, const double* B, int reps, int which
   cudaEventElapsedTime(&cub_ms, e0, e1);
   cub_ms /= reps;
   if (which == 0) {   // generic large
+    TCO(TA, TB, 64, 64, 16, 32, 32, 3, 3, false);
     TC(TA, TB, 64, 64, 16, 32, 32, 3, 3, false);
-    TC(TA, TB, 64, 64, 16, 32, 32, 4, 3, false);
-    TC(TA, TB, 64, 64, 16, 32, 32, 3, 4, false);
-    TC(TA, TB, 64, 64, 32, 32, 32, 3, 3, false);
-    TC(TA, TB, 64, 128, 16, 32, 64, 3, 2, false);
-    TC(TA, TB, 64, 128, 16, 32, 64, 3, 2, true);
-    TC(TA, TB, 64, 128, 16, 32, 64, 4, 2, false);
+    TCO(TA, TB, 128, 64, 16, 64, 32, 3, 2, false);
     TC(TA, TB, 128, 64, 16, 64, 32, 3, 2, false);
-    TC(TA, TB, 64, 32, 16, 32, 16, 4, 5, false);
-    TC(TA, TB, 64, 64, 16, 32, 16, 3, 2, false);
-  } else {             // skinny M = 72 / 136
-    OLD(TA, TB, 80, 64, 16, 16, 32, 3);
-    TC(TA, TB, 80, 64, 16, 16, 32, 3, 3, false);
-    TC(TA, TB, 80, 32, 16, 16, 32, 4, 4, false);
-    TC(TA, TB, 80, 32, 16, 16, 16, 4, 3, false);
-    TC(TA, TB, 144, 32, 16, 16, 32, 4, 3, false);
-    TC(TA, TB, 144, 32, 16, 48, 16, 4, 3, false);
-    TC(TA, TB, 144, 64, 16, 48, 32, 3, 2, false);
-    TC(TA, TB, 48, 128, 16, 16, 64, 3, 2, false);
-    TC(TA, TB, 48, 64, 16, 16, 32, 4, 4, false);
-    TC(TA, TB, 64, 32, 16, 32, 16, 4, 5, false);
-    TC(TA, TB, 80, 64, 32, 16, 32, 3, 3, false);
+  } else {
+    TCO(TA, TB, 48, 64, 16, 16, 32, 4, 4, false);
+    TC(TA, TB, 48, 64, 16, 16, 32, 4, 3, false);
+    TCO(TA, TB, 80, 64, 16, 16, 32, 3, 3, false);
+    TC(TA, TB, 80, 64, 16, 16, 32, 3, 2, false);
   }
 }
 
