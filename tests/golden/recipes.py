@@ -9,8 +9,16 @@ kernels, which is why every golden stores the sha256 of its A."""
 from __future__ import annotations
 
 import hashlib
+import os
+import subprocess
+import sys
+import tempfile
 
 import numpy as np
+
+# the OpenBLAS kernel family and thread count the goldens were generated with
+# (threadpoolctl in the build container: architecture SkylakeX, 8 threads)
+GOLDEN_BLAS = {"OPENBLAS_CORETYPE": "SkylakeX", "OPENBLAS_NUM_THREADS": "8"}
 
 # name -> (driver, k, block, padding, description)
 CONFIGS = {
@@ -52,3 +60,28 @@ def build(name: str) -> np.ndarray:
     if name == "cfg5":
         return np.asfortranarray(np.random.default_rng(0).standard_normal((32768, 32768)))
     raise KeyError(name)
+
+
+def _avx512():
+    try:
+        return " avx512f" in open("/proc/cpuinfo").read()
+    except OSError:
+        return False
+
+
+def build_as_golden(name: str) -> np.ndarray:
+    """build(name) in a subprocess whose OpenBLAS uses the golden host's
+    kernel family and thread count, so LAPACK-built recipes reproduce the
+    golden's bytes on another host (the kernel choice is made when the
+    library loads, hence the fresh process).  Falls back to build() when the
+    CPU cannot run those kernels."""
+    if name in ("cfg1", "cfg5") or not _avx512():
+        return build(name)
+    with tempfile.TemporaryDirectory() as d:
+        out = os.path.join(d, "A.npy")
+        env = dict(os.environ, **GOLDEN_BLAS)
+        code = ("import sys, numpy as np; sys.path.insert(0, %r); import recipes; "
+                "np.save(%r, recipes.build(%r))" % (os.path.dirname(os.path.abspath(__file__)),
+                                                    out, name))
+        subprocess.run([sys.executable, "-c", code], check=True, env=env)
+        return np.asfortranarray(np.load(out))

@@ -303,3 +303,35 @@ def test_matrix_market_to_device_factorization(tmp_path):
     o = port.rqrcp(A, None, 32, 8, 0)
     np.testing.assert_array_equal(f.perm.forward.cpu().numpy() if hasattr(f.perm.forward, "cpu")
                                   else np.asarray(f.perm.forward), o.perm.forward)
+
+
+def test_b128_second_half_decline_rewinds_to_original_columns():
+    """A 128-wide block whose rank drop lands in its second 64 columns
+    (1100 x 1700, rank 366 + 1e-9 noise: block 256..383 drops at column 110
+    of 128).  The two-half fast panel commits its first half in place before
+    the second half declines; the rewind must redo the panel on the ORIGINAL
+    selected columns, as the reference eliminates a panel on a copy
+    (randomized.py:221-239).  Bars: identical pivots and R rows up to the
+    noise floor, plus the residual."""
+    import paper_1509_06820_b200 as P
+    g = np.random.default_rng(147)
+    m, n, r = 1100, 1700, 366
+    A = g.standard_normal((m, r)) @ g.standard_normal((r, n)) + 1e-9 * g.standard_normal((m, n))
+    cfg = P.RandomizedConfig(block=128, padding=8, seed=0)
+    f = P.rqrcp(A, None, cfg)
+    o = port.rqrcp(A, None, 128, 8, 0)
+    frob = float(np.linalg.norm(A))
+    d = np.abs(np.diag(o.R))
+    r_sig = int(np.argmax(d <= NOISE * EPS * frob)) if (d <= NOISE * EPS * frob).any() else d.size
+    assert r_sig >= r - 2
+    pf = np.asarray(f.perm.forward)
+    np.testing.assert_array_equal(pf[:r_sig], o.perm.forward[:r_sig])
+    mine = f.perm.restore(f.R)[:r_sig]
+    theirs = np.zeros((o.R.shape[0], n))
+    theirs[:, o.perm.forward] = o.R
+    assert np.linalg.norm(mine - theirs[:r_sig]) <= 1e-10 * np.linalg.norm(theirs[:r_sig])
+    rebuilt = np.zeros(A.shape)
+    rebuilt[: f.rank] = f.R
+    rebuilt[f.rank:, f.rank:] = f.trailing
+    res = np.linalg.norm(A[:, pf] - f.q_factor(full=True) @ rebuilt)
+    assert res <= 1e-12 * frob
