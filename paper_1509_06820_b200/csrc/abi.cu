@@ -1,5 +1,6 @@
 // extern "C" boundary (include/rqrcp_b200.h): argument checks, exception ->
 // status-code mapping, and the thin adapters onto the native drivers.
+#include <mutex>
 #include <string>
 
 #include "../../include/rqrcp_b200.h"
@@ -7,6 +8,7 @@
 
 struct rq_handle_s {
   rq::Handle* h;
+  std::recursive_mutex mu;
 };
 
 namespace {
@@ -32,6 +34,33 @@ int guarded(F&& f) {
     g_err = "unknown error";
     return RQ_ERR_INTERNAL;
   }
+}
+
+// Every call on a handle runs with the handle's device current and puts the
+// caller's current device back afterwards (a process may drive several GPUs,
+// one handle each; PyTorch keeps its own notion of the current device).
+struct DeviceScope {
+  int prev = -1;
+  explicit DeviceScope(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) RQ_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceScope() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// calls on one handle are serialised: its named scratch buffers and Status
+// word are shared by every call on that device
+template <class F>
+int guarded_on(rq_handle_t h, F&& f) {
+  return guarded([&] {
+    if (h == nullptr || h->h == nullptr) throw rq::InvalidArg("null handle");
+    std::lock_guard<std::recursive_mutex> lock(h->mu);
+    DeviceScope dev(h->h->device);
+    f();
+  });
 }
 
 cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
@@ -98,6 +127,7 @@ int rq_create(int device, rq_handle_t* out) {
     need(out != nullptr, "null output");
     auto* h = new rq_handle_s;
     try {
+      DeviceScope dev(device);   // the caller's current device is left as it was
       h->h = new rq::Handle(device);
     } catch (...) {
       delete h;
@@ -110,13 +140,16 @@ int rq_create(int device, rq_handle_t* out) {
 int rq_destroy(rq_handle_t h) {
   return guarded([&] {
     if (!h) return;
-    delete h->h;
+    {
+      DeviceScope dev(h->h->device);
+      delete h->h;
+    }
     delete h;
   });
 }
 
 int rq_factor(rq_handle_t h, const rq_factor_args* args, rq_factor_result* out) {
-  return guarded([&] {
+  return guarded_on(h, [&] {
     need(args && out, "null argument");
     rq::FactorParams p = to_params(*args);
     rq::FactorResult r = rq::run_factor(H(h), p);
@@ -125,7 +158,7 @@ int rq_factor(rq_handle_t h, const rq_factor_args* args, rq_factor_result* out) 
 }
 
 int rq_tuxv(rq_handle_t h, const rq_tuxv_args* args, rq_tuxv_result* out) {
-  return guarded([&] {
+  return guarded_on(h, [&] {
     need(args && out, "null argument");
     need(args->f.variant == RQ_TRQRCP, "tuxv runs on TRQRCP");
     need(args->j_max >= 1, "j_max must be >= 1");
@@ -145,7 +178,7 @@ int rq_tuxv(rq_handle_t h, const rq_tuxv_args* args, rq_tuxv_result* out) {
 int rq_gemm(rq_handle_t h, int transa, int transb, int64_t m, int64_t n, int64_t k,
             double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
             double beta, double* C, int64_t ldc, void* stream) {
-  return guarded([&] {
+  return guarded_on(h, [&] {
     need(m >= 0 && n >= 0 && k >= 0, "negative dimension");
     need(ldc >= std::max<int64_t>(1, m), "ldc too small");
     rq::gemm(H(h), transa != 0, transb != 0, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc,
@@ -155,7 +188,7 @@ int rq_gemm(rq_handle_t h, int transa, int transb, int64_t m, int64_t n, int64_t
 
 int rq_sketch(rq_handle_t h, int64_t ell, int64_t m, int64_t n, const double* omega,
               int64_t ldo, const double* A, int64_t lda, double* B, int64_t ldb, void* stream) {
-  return guarded([&] {
+  return guarded_on(h, [&] {
     need(ell >= 1, "sample must have at least one row");
     rq::gemm(H(h), false, false, ell, n, m, 1.0, omega, ldo, A, lda, 0.0, B, ldb, S(stream));
   });
@@ -165,7 +198,7 @@ int rq_select_pivots(rq_handle_t h, int64_t ell, int64_t nt, int64_t want, const
                      int64_t ldb, double* S_, int64_t lds, int64_t* piv, double* Ys,
                      int64_t ldys, double* taus, int64_t* got, int64_t* level2,
                      void* stream) {
-  return guarded([&] {
+  return guarded_on(h, [&] {
     rq::Handle& hh = H(h);
     cudaStream_t s = S(stream);
     auto* st = (rq::Status*)hh.buf("abi_st", sizeof(rq::Status), s);
@@ -183,7 +216,7 @@ int rq_select_pivots(rq_handle_t h, int64_t ell, int64_t nt, int64_t want, const
 int rq_panel_qr(rq_handle_t h, int64_t mm, int64_t bw, double* P, int64_t ldp, double* Y,
                 int64_t ldy, double* tau, double* T, int64_t ldt, double tol, int64_t* usable,
                 int64_t* level2, void* stream) {
-  return guarded([&] {
+  return guarded_on(h, [&] {
     rq::Handle& hh = H(h);
     cudaStream_t s = S(stream);
     auto* st = (rq::Status*)hh.buf("abi_st", sizeof(rq::Status), s);
@@ -200,14 +233,14 @@ int rq_panel_qr(rq_handle_t h, int64_t mm, int64_t bw, double* P, int64_t ldp, d
 
 int rq_t_factor(rq_handle_t h, const double* Y, int64_t ldy, int64_t mm, int64_t nb,
                 const double* tau, double* T, int64_t ldt, void* stream) {
-  return guarded([&] { rq::t_factor(H(h), Y, ldy, mm, nb, tau, T, ldt, S(stream)); });
+  return guarded_on(h, [&] { rq::t_factor(H(h), Y, ldy, mm, nb, tau, T, ldt, S(stream)); });
 }
 
 int rq_sample_update(rq_handle_t h, int64_t ell, int64_t b, int64_t n2, const double* S_,
                      int64_t lds, const double* R11, const double* R12, int64_t ldr,
                      double frob, double* Bnew, int64_t ldb, int32_t* degenerate,
                      void* stream) {
-  return guarded([&] {
+  return guarded_on(h, [&] {
     rq::Handle& hh = H(h);
     cudaStream_t s = S(stream);
     auto* st = (rq::Status*)hh.buf("abi_st", sizeof(rq::Status), s);
@@ -223,7 +256,7 @@ int rq_sample_update(rq_handle_t h, int64_t ell, int64_t b, int64_t n2, const do
 int rq_qr_blocked(rq_handle_t h, int64_t m, int64_t n, int64_t k, int64_t b, double* A,
                   int64_t lda, double* Y, int64_t ldy, double* tau, int64_t* counters,
                   void* stream) {
-  return guarded([&] {
+  return guarded_on(h, [&] {
     need(k >= 0 && k <= std::min(m, n), "rank outside [0, min(m, n)]");
     need(b >= 1, "block size must be >= 1");
     rq::Counters c;
@@ -239,7 +272,7 @@ int rq_qr_blocked(rq_handle_t h, int64_t m, int64_t n, int64_t k, int64_t b, dou
 int rq_q_columns(rq_handle_t h, int64_t m, int64_t nref, int64_t cols, const double* Y,
                  int64_t ldy, const double* tau, int64_t b, double* Q, int64_t ldq,
                  void* stream) {
-  return guarded([&] {
+  return guarded_on(h, [&] {
     need(b >= 1, "block size must be >= 1");
     rq::q_columns(H(h), m, nref, cols, Y, ldy, tau, b, Q, ldq, S(stream));
   });
@@ -247,7 +280,7 @@ int rq_q_columns(rq_handle_t h, int64_t m, int64_t nref, int64_t cols, const dou
 
 int rq_column_norms(rq_handle_t h, const double* A, int64_t m, int64_t n, int64_t lda,
                     int sequential, double* out, void* stream) {
-  return guarded([&] {
+  return guarded_on(h, [&] {
     need(m >= 0 && n >= 0 && lda >= std::max<int64_t>(m, 1), "bad shape");
     rq::column_norms(H(h), A, m, n, lda, sequential != 0, out, S(stream));
   });
@@ -255,13 +288,13 @@ int rq_column_norms(rq_handle_t h, const double* A, int64_t m, int64_t n, int64_
 
 int rq_frob_norm(rq_handle_t h, const double* A, int64_t m, int64_t n, int64_t lda,
                  double* out, void* stream) {
-  return guarded([&] { rq::frob_norm(H(h), A, m, n, lda, out, S(stream)); });
+  return guarded_on(h, [&] { rq::frob_norm(H(h), A, m, n, lda, out, S(stream)); });
 }
 
 int64_t rq_launch_count(void) { return rq::launch_count(); }
 
 int rq_set_option(rq_handle_t h, const char* name, int64_t value) {
-  return guarded([&] {
+  return guarded_on(h, [&] {
     need(name != nullptr, "null option name");
     rq::Handle& hh = H(h);
     const std::string n(name);
@@ -309,7 +342,7 @@ int rq_set_option(rq_handle_t h, const char* name, int64_t value) {
 }
 
 int rq_debug_read(rq_handle_t h, int64_t* out, int n) {
-  return guarded([&] {
+  return guarded_on(h, [&] {
     rq::Handle& hh = H(h);
     need(hh.dbg != nullptr, "debug timers not enabled");
     RQ_CUDA(cudaDeviceSynchronize());
@@ -318,15 +351,15 @@ int rq_debug_read(rq_handle_t h, int64_t* out, int n) {
 }
 
 int rq_profile_enable(rq_handle_t h, int on) {
-  return guarded([&] { H(h).profiling = on != 0; });
+  return guarded_on(h, [&] { H(h).profiling = on != 0; });
 }
 
 int rq_profile_reset(rq_handle_t h) {
-  return guarded([&] { H(h).prof_reset(); });
+  return guarded_on(h, [&] { H(h).prof_reset(); });
 }
 
 int rq_profile_read(rq_handle_t h, int64_t* launches, double* ms, double* flops, double* bytes) {
-  return guarded([&] {
+  return guarded_on(h, [&] {
     rq::Handle& hh = H(h);
     hh.prof_collect();
     for (int i = 0; i < rq::kProfNum; ++i) {
@@ -342,7 +375,7 @@ int rq_profile_read(rq_handle_t h, int64_t* launches, double* ms, double* flops,
 
 int rq_profile_trace(rq_handle_t h, int64_t cap, int32_t* cat, double* start_ms, double* end_ms,
                      int64_t* count) {
-  return guarded([&] {
+  return guarded_on(h, [&] {
     rq::Handle& hh = H(h);
     hh.prof_collect();
     const int64_t nrec = (int64_t)hh.trace.size();

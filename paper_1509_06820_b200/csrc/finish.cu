@@ -201,12 +201,8 @@ __global__ void __launch_bounds__(kFinT, 1) block_finish_kernel(FinishArgs a) {
 template <int B, int NW>
 void launch_finish(const FinishArgs& f, cudaStream_t s) {
   constexpr size_t smem = ((size_t)4 * B * kFinLd + (size_t)NW * (2 * B + 4)) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    RQ_CUDA(cudaFuncSetAttribute(block_finish_kernel<B, NW>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  kernel_attr((const void*)block_finish_kernel<B, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+              (int)smem);
   const int grid = (int)((f.nt2 + NW - 1) / NW);
   block_finish_kernel<B, NW><<<grid, kFinT, smem, s>>>(f);
 }

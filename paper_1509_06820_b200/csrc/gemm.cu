@@ -25,12 +25,7 @@ template <bool TA, bool TB, int BM, int BN, int BK, int WM, int WN, int ST, int 
 void launch_cfg(Handle& h, GemmArgs g, cudaStream_t s) {
   using Cfg = GemmCfg<TA, TB, BM, BN, BK, WM, WN, ST>;
   auto kern = gemm_f64_kernel<TA, TB, BM, BN, BK, WM, WN, ST, VEC>;
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
-    RQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)Cfg::kSmem));
-    attr_set = true;
-  }
+  kernel_attr((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
   const int64_t gm = (g.M + BM - 1) / BM, gn = (g.N + BN - 1) / BN;
   const int64_t tiles = gm * gn;
   g.splits = 1;

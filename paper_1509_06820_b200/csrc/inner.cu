@@ -136,13 +136,11 @@ bool inner_gemm(Handle& h, int64_t M, int64_t N, int64_t K, const double* P, int
   if (!h.inner_kernel || (M != 64 && M != 32) || N <= 0 || K < 4096) return false;
   if (M == 32 && !h.inner32) return false;
   if (((uintptr_t)P & 15) || (ldp & 1) || ((uintptr_t)C & 15) || (ldc & 1)) return false;
-  static bool attr = false;
-  if (!attr) {
-    RQ_CUDA(cudaFuncSetAttribute(inner_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)inner_smem<64>()));
-    RQ_CUDA(cudaFuncSetAttribute(inner_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)inner_smem<32>()));
-    attr = true;
+  {
+    kernel_attr((const void*)inner_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                (int)inner_smem<64>());
+                kernel_attr((const void*)inner_kernel<32>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)inner_smem<32>());
   }
   const int64_t tn = (N + kIN - 1) / kIN;
   const int64_t nkt = (K + kIK - 1) / kIK;

@@ -382,30 +382,15 @@ void panel_qr(Handle& h, int64_t mm, int64_t bw, const double* P, int64_t ldp,
       a.bar = (unsigned int*)h.buf("pan_bar", 64, s);
       a.gpub = (double*)h.buf("pan_gpub", (size_t)2 * Q * 2 * bw * 8, s);
       RQ_CUDA(cudaMemsetAsync(a.bar, 0, 64, s));
-      static size_t attr = 0;
-      if (smem > attr) {
-        RQ_CUDA(cudaFuncSetAttribute(panel_kernel<false>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)std::max<size_t>(smem, 48 * 1024)));
-        attr = std::max<size_t>(smem, 48 * 1024);
-      }
+      kernel_attr((const void*)panel_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                  (int)std::max<size_t>(smem, 48 * 1024));
       void* args[] = {&a};
       RQ_CUDA(cudaLaunchCooperativeKernel((void*)panel_kernel<false>, dim3(Q), dim3(kPanThreads),
                                           args, smem, s));
     } else {
-      static bool attr_init = false;
-      static size_t attr = 0;
-      if (!attr_init) {
-        RQ_CUDA(cudaFuncSetAttribute(panel_kernel<true>,
-                                     cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        attr_init = true;
-      }
-      if (smem > attr) {
-        RQ_CUDA(cudaFuncSetAttribute(panel_kernel<true>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)std::max<size_t>(smem, 48 * 1024)));
-        attr = std::max<size_t>(smem, 48 * 1024);
-      }
+      kernel_attr((const void*)panel_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      kernel_attr((const void*)panel_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                  (int)std::max<size_t>(smem, 48 * 1024));
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(Q);
       cfg.blockDim = dim3(kPanThreads);

@@ -713,12 +713,8 @@ const int* panel_fast(Handle& h, int64_t mm, int64_t bw, const double* P, int64_
   if (m_rowmajor != nullptr) *m_rowmajor = a.gmat + 3 * nn;
   if (m_ld != nullptr) *m_ld = n8;
   a.dbg = h.dbg;
-  static size_t attr = 0;
-  if (smem > attr) {
-    RQ_CUDA(cudaFuncSetAttribute(panel_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)std::max<size_t>(smem, 48 * 1024)));
-    attr = std::max<size_t>(smem, 48 * 1024);
-  }
+  kernel_attr((const void*)panel_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+              (int)std::max<size_t>(smem, 48 * 1024));
   {
     ProfScope prof(h, kProfPanel, 6.0 * mm * bw * bw, 24.0 * mm * bw, s);
     void* args[] = {&a};

@@ -463,12 +463,8 @@ __global__ void __launch_bounds__(kRuThreads, 2) rank_update_k2_kernel(RuArgs a)
 template <int K>
 void launch_rank_update_k2(Handle& h, const RuArgs& a, int grid, cudaStream_t s) {
   constexpr size_t smem = (size_t)(K * kLdA + kTN * (K + 4) + kTN * kLdC) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    RQ_CUDA(cudaFuncSetAttribute(rank_update_k2_kernel<K>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  kernel_attr((const void*)rank_update_k2_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+              (int)smem);
   rank_update_k2_kernel<K><<<grid, kRuThreads, smem, s>>>(a);
 }
 
@@ -653,24 +649,16 @@ template <int K>
 void launch_rank_update_big(Handle& h, const RuArgs& a, int grid, cudaStream_t s) {
   constexpr size_t smem =
       ((size_t)K * (kBM + 4) + 2 * (size_t)kBN * (K + 4)) * sizeof(double) + 16 * kRuThreads * 16;
-  static bool attr = false;
-  if (!attr) {
-    RQ_CUDA(cudaFuncSetAttribute(rank_update_big_kernel<K>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+      kernel_attr((const void*)rank_update_big_kernel<K>,
+                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   rank_update_big_kernel<K><<<grid, kRuThreads, smem, s>>>(a);
 }
 
 template <int K>
 void launch_rank_update_k(Handle& h, const RuArgs& a, int grid, cudaStream_t s) {
   constexpr size_t smem = (size_t)2 * (K * kLdA + kTN * (K + 4) + kTN * kLdC) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    RQ_CUDA(cudaFuncSetAttribute(rank_update_k_kernel<K>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  kernel_attr((const void*)rank_update_k_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+              (int)smem);
   rank_update_k_kernel<K><<<grid, kRuThreads, smem, s>>>(a);
 }
 
@@ -681,12 +669,8 @@ bool rank_update(Handle& h, int64_t M, int64_t N, int64_t K, const double* Y, in
                  const Status* st, int cat, int max_ctas, Status* snap, const double* Csrc,
                  int64_t ldcs, int extra_rows) {
   if (K < 4 || (K > kKMax && K != 128) || (K % 4) != 0 || M <= 0 || N <= 0) return false;
-  static bool attr = false;
-  if (!attr) {
-    RQ_CUDA(cudaFuncSetAttribute(rank_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)kRuSmem));
-    attr = true;
-  }
+  kernel_attr((const void*)rank_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+              (int)kRuSmem);
   const auto al = [](const double* p, int64_t ld) { return ((uintptr_t)p & 15) == 0 && ld % 2 == 0; };
   RuArgs a{M, N, (int)K, Y, ldy, X, ldx, C, ldc, st,
            (h.gemm_vec16 && al(Y, ldy) && al(X, ldx) && al(C, ldc) &&

@@ -1,6 +1,8 @@
 // Host runtime: handle, workspace arena, launch counter and the optional
 // CUDA-event profiler used by bench.py.
 #include <atomic>
+#include <mutex>
+#include <tuple>
 
 #include "runtime.hpp"
 
@@ -8,6 +10,22 @@ namespace rq {
 
 namespace {
 std::atomic<int64_t> g_launches{0};
+std::mutex g_attr_mu;
+std::map<std::tuple<const void*, int, int>, int> g_attrs;
+}
+
+void kernel_attr(const void* func, cudaFuncAttribute attr, int value) {
+  int dev = 0;
+  RQ_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(g_attr_mu);
+  const auto key = std::make_tuple(func, dev, (int)attr);
+  auto it = g_attrs.find(key);
+  if (it != g_attrs.end() &&
+      (attr == cudaFuncAttributeMaxDynamicSharedMemorySize ? it->second >= value
+                                                            : it->second == value))
+    return;
+  RQ_CUDA(cudaFuncSetAttribute(func, attr, value));
+  g_attrs[key] = value;
 }
 
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }

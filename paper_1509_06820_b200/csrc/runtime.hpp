@@ -55,6 +55,11 @@ struct ProfStat {
   double ms = 0.0, flops = 0.0, bytes = 0.0;
 };
 
+// cudaFuncSetAttribute memoised per (kernel, device, attribute): kernel
+// attributes are per device, and one process may drive several GPUs (one
+// handle each).  Dynamic shared memory is only ever raised.
+void kernel_attr(const void* func, cudaFuncAttribute attr, int value);
+
 // total kernel launches issued by the library (all handles)
 void count_launch(int n = 1);
 int64_t launch_count();

@@ -903,17 +903,9 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_reg_kernel(SelArgs a) {
 template <bool kCluster, int RPL, int CPG>
 void launch_reg(Handle& h, int P, size_t smem, SelArgs& a, cudaStream_t s) {
   auto kern = select_reg_kernel<kCluster, RPL, CPG>;
-  static size_t attr = 0;
-  static bool cl = false;
-  if (kCluster && !cl) {
-    RQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    cl = true;
-  }
-  if (smem > attr) {
-    RQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)std::max<size_t>(smem, 48 * 1024)));
-    attr = std::max<size_t>(smem, 48 * 1024);
-  }
+  if (kCluster) kernel_attr((const void*)kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  kernel_attr((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+              (int)std::max<size_t>(smem, 48 * 1024));
   if constexpr (!kCluster) {
     void* args[] = {&a};
     RQ_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(P), dim3(kSelThreads), args, smem, s));
@@ -1034,30 +1026,16 @@ void select_pivots(Handle& h, int64_t ell, int64_t nt, int64_t want, const doubl
     a.gcol = (double*)h.buf("sel_gcol", (size_t)2 * P * (ell + 1) * 8, s);
     a.gsq = (double*)h.buf("sel_gsq", (size_t)P * 8, s);
     RQ_CUDA(cudaMemsetAsync(a.bar, 0, 64, s));
-    static size_t attr = 0;
-    if (smem > attr) {
-      RQ_CUDA(cudaFuncSetAttribute(select_kernel<false>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)std::max<size_t>(smem, 48 * 1024)));
-      attr = std::max<size_t>(smem, 48 * 1024);
-    }
+    kernel_attr((const void*)select_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                (int)std::max<size_t>(smem, 48 * 1024));
     void* args[] = {&a};
     RQ_CUDA(cudaLaunchCooperativeKernel((void*)select_kernel<false>, dim3(P), dim3(kSelThreads),
                                         args, smem, s));
     return;
   }
-  static bool attr_init = false;
-  static size_t attr = 0;
-  if (!attr_init) {
-    RQ_CUDA(cudaFuncSetAttribute(select_kernel<true>,
-                                 cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    attr_init = true;
-  }
-  if (smem > attr) {
-    RQ_CUDA(cudaFuncSetAttribute(select_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)std::max<size_t>(smem, 48 * 1024)));
-    attr = std::max<size_t>(smem, 48 * 1024);
-  }
+  kernel_attr((const void*)select_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  kernel_attr((const void*)select_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+              (int)std::max<size_t>(smem, 48 * 1024));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(P);
   cfg.blockDim = dim3(kSelThreads);

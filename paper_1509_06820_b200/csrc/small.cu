@@ -597,12 +597,8 @@ void sample_update(Handle& h, int64_t ell, int64_t b, int64_t n2, const double* 
     const double th = kEps34 * frob;
     const int ab = abort_on_degenerate ? 1 : 0;
     const size_t psm = ((size_t)4 * b * (b + 1) + b) * 8;
-    static bool pattr = false;
-    if (!pattr) {
-      RQ_CUDA(cudaFuncSetAttribute(su_prep_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)(((size_t)4 * 64 * 65 + 64) * 8)));
-      pattr = true;
-    }
+    kernel_attr((const void*)su_prep_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                (int)(((size_t)4 * 64 * 65 + 64) * 8));
     if (b == 16) su_prep_kernel<16><<<1, 256, psm, s>>>(S, lds, R11, ldr, th, M, st, ab, i0);
     else if (b == 32) su_prep_kernel<32><<<1, 256, psm, s>>>(S, lds, R11, ldr, th, M, st, ab, i0);
     else su_prep_kernel<64><<<1, 256, psm, s>>>(S, lds, R11, ldr, th, M, st, ab, i0);
@@ -628,12 +624,8 @@ void sample_update(Handle& h, int64_t ell, int64_t b, int64_t n2, const double* 
     double* M = (double*)h.buf("su_M", (size_t)128 * 128 * 8, s);
     const int ab = abort_on_degenerate ? 1 : 0;
     constexpr size_t wsm = (size_t)3 * 64 * 65 * 8;
-    static bool wattr = false;
-    if (!wattr) {
-      RQ_CUDA(cudaFuncSetAttribute(su_prep_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)wsm));
-      wattr = true;
-    }
+    kernel_attr((const void*)su_prep_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                (int)wsm);
     double* Ri22 = Ri + 64 + (size_t)64 * 128;
     fill2d(Ri + 64, 128, 64, 64, 0.0, s, st);   // the zero block below A^-1
     su_prep_wide_kernel<<<1, 256, wsm, s>>>(R11, ldr, 128, kEps34 * frob, Ri, Ri22, 128, st, ab,
@@ -666,12 +658,8 @@ void sample_update(Handle& h, int64_t ell, int64_t b, int64_t n2, const double* 
     const double th = kEps34 * frob;
     const int ab = abort_on_degenerate ? 1 : 0;
     const size_t dsm = (size_t)(2 * b * b + b) * 8;
-    static bool attr64 = false;
-    if (!attr64) {
-      RQ_CUDA(cudaFuncSetAttribute(sample_update_reg_kernel<64>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024));
-      attr64 = true;
-    }
+    kernel_attr((const void*)sample_update_reg_kernel<64>,
+                cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
     if (b == 16)
       sample_update_reg_kernel<16><<<blocks, 128, dsm, s>>>((int)ell, n2, S, lds, R11, R12, ldr,
                                                             th, Bnew, ldb, st, ab, i0);
@@ -685,13 +673,8 @@ void sample_update(Handle& h, int64_t ell, int64_t b, int64_t n2, const double* 
     return;
   }
   const size_t smem = ((size_t)b * b + (size_t)b * kSuThreads) * 8;
-  static size_t attr = 0;
-  if (smem > attr) {
-    RQ_CUDA(cudaFuncSetAttribute(sample_update_kernel,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)std::max<size_t>(smem, 48 * 1024)));
-    attr = std::max<size_t>(smem, 48 * 1024);
-  }
+  kernel_attr((const void*)sample_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+              (int)std::max<size_t>(smem, 48 * 1024));
   if (smem > h.smem_optin) throw InvalidArg("sample update block too wide");
   const int blocks = (int)std::max<int64_t>(1, (n2 + kSuThreads - 1) / kSuThreads);
   ProfScope prof(h, kProfSampleUpd, 3.0 * b * b * n2, 8.0 * (2 * ell * n2 + b * b), s);
@@ -710,12 +693,8 @@ void apply_swaps(Handle& h, const int64_t* piv, int64_t got_max, int64_t i0,
   const int ur = t.Rf ? (int)((t.rf_rows + kSwapRows - 1) / kSwapRows) : 0;
   const int uf = t.Wf ? (int)((t.wf_cols + kSwapRows - 1) / kSwapRows) : 0;
   const size_t smem = (size_t)2 * got_max * kSwapRows * 8;
-  static size_t attr = 0;
-  if (smem > attr) {
-    RQ_CUDA(cudaFuncSetAttribute(swap_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)std::max<size_t>(smem, 48 * 1024)));
-    attr = std::max<size_t>(smem, 48 * 1024);
-  }
+  kernel_attr((const void*)swap_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+              (int)std::max<size_t>(smem, 48 * 1024));
   swap_fused_kernel<<<std::max(uw + ur + uf, 1), 256, smem, s>>>(piv, i0, t, st, uw, ur);
   RQ_CHECK_LAUNCH();
   count_launch();
@@ -801,12 +780,8 @@ void t_factor(Handle& h, const double* Y, int64_t ldy, int64_t mm, int64_t nb,
   gemm(h, true, false, nb, nb, mm, 1.0, Y, ldy, Y, ldy, 0.0, G, nb, s, st, kProfPanel);
   if (nb <= 64 && h.t_inverse) {
     constexpr size_t kInvSmem = 3 * 64 * 65 * 8;
-    static bool inv_attr = false;
-    if (!inv_attr) {
-      RQ_CUDA(cudaFuncSetAttribute(t_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)kInvSmem));
-      inv_attr = true;
-    }
+    kernel_attr((const void*)t_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                (int)kInvSmem);
     ProfScope prof(h, kProfPanel, (double)nb * nb * nb / 3.0, 16.0 * nb * nb, s);
     t_inverse_kernel<<<1, 256, kInvSmem, s>>>(G, nb, tau, (int)nb, T, ldt, st);
     RQ_CHECK_LAUNCH();
@@ -814,12 +789,8 @@ void t_factor(Handle& h, const double* Y, int64_t ldy, int64_t mm, int64_t nb,
     return;
   }
   const size_t smem = nb <= 128 ? ((size_t)nb * nb + nb) * 8 : (size_t)nb * 8;
-  static size_t attr = 0;
-  if (smem > attr) {
-    RQ_CUDA(cudaFuncSetAttribute(t_recurrence_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)std::max<size_t>(smem, 48 * 1024)));
-    attr = std::max<size_t>(smem, 48 * 1024);
-  }
+  kernel_attr((const void*)t_recurrence_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+              (int)std::max<size_t>(smem, 48 * 1024));
   ProfScope prof(h, kProfPanel, (double)nb * nb * nb / 3.0, 16.0 * nb * nb, s);
   t_recurrence_kernel<<<1, 256, smem, s>>>(G, nb, tau, (int)nb, T, ldt, st);
   RQ_CHECK_LAUNCH();

@@ -11,17 +11,6 @@ namespace rq {
 
 namespace {
 
-// one dynamic-shared-memory opt-in per (kernel, device): `done` is a static
-// of the calling instantiation, one bit per device ordinal (< 32)
-template <class K>
-void smem_optin(K kern, size_t bytes, unsigned& done) {
-  int dev = 0;
-  RQ_CUDA(cudaGetDevice(&dev));
-  if (dev < 32 && (done >> dev) & 1u) return;
-  RQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-  if (dev < 32) done |= 1u << dev;
-}
-
 // K chunks per output tile: maximise the occupied fraction of the last wave
 // (one CTA per SM), each chunk at least `min_kt` k-tiles deep
 int choose_splits(int64_t tiles, int64_t ktiles, int sms, int min_kt, int64_t plane,
@@ -51,8 +40,7 @@ template <bool TA, bool TB, int BM, int BN, int BK, int WM, int WN, int ST, int 
 void tc_launch(Handle& h, GemmArgs g, cudaStream_t s, int forced_splits) {
   using Cfg = TcCfg<TA, TB, BM, BN, BK, WM, WN, ST>;
   auto kern = tc_gemm_kernel<TA, TB, BM, BN, BK, WM, WN, ST, VEC, MINB, DBUF>;
-  static unsigned optin = 0;
-  smem_optin(kern, Cfg::kSmem, optin);
+  kernel_attr((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
   const int64_t gm = (g.M + BM - 1) / BM, gn = (g.N + BN - 1) / BN;
   const int64_t ktiles = (g.K + BK - 1) / BK;
   // resident CTAs per SM: the launch bound's minimum (registers and shared

@@ -155,6 +155,7 @@ def to_host_many(*ts):
     host allocator recycles them across calls), one stream sync, numpy views;
     column-major layouts are kept (no host-side reshuffle)."""
     outs = []
+    dev = next((t.device for t in ts if t is not None), None)
     for t in ts:
         if t is None:
             outs.append(None)
@@ -165,7 +166,8 @@ def to_host_many(*ts):
             h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
         h.copy_(t, non_blocking=True)
         outs.append(h)
-    torch.cuda.current_stream().synchronize()
+    if dev is not None:
+        torch.cuda.current_stream(dev).synchronize()   # the stream the copies were issued on
     return tuple(None if h is None else h.numpy() for h in outs)
 
 
@@ -223,6 +225,9 @@ def rqrcp(A, k=None, config=None, omega=None):
     return _randomized_factor(A, k, config, config.ell, config.block, _abi.RQ_RQRCP, True, omega)
 
 
+SSRQRCP_MAX_K = 256   # widest panel the native driver factors in one block (driver.cu)
+
+
 def rsrqrcp(A, k=None, config=None, omega=None):
     """Fresh sketch before every block (randomized.py:284-296)."""
     config = config if config is not None else RandomizedConfig()
@@ -234,4 +239,10 @@ def ssrqrcp(A, k, config=None, omega=None):
     """One (k + padding)-row sketch selects all k pivots (randomized.py:299-313)."""
     config = config if config is not None else RandomizedConfig()
     k = int(k)
+    if k > SSRQRCP_MAX_K:
+        # one panel of width k: the GPU panel kernels and the pivot selection
+        # keep a panel's b x b working set on chip (DESIGN.md §9 known limits)
+        raise NotImplementedError(
+            f"ssrqrcp with k = {k} > {SSRQRCP_MAX_K}: the single-sample panel is limited to "
+            f"{SSRQRCP_MAX_K} columns on the GPU (the reference accepts any k)")
     return _randomized_factor(A, k, config, k + config.padding, k, _abi.RQ_SSRQRCP, False, omega)

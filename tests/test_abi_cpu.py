@@ -96,3 +96,9 @@ def test_permutation_semantics():
     np.testing.assert_array_equal(p.restore(R)[:, p.forward], R)
     q = P.Permutation.from_order([3, 1, 4, 0, 2])
     assert list(q.forward) == [3, 1, 4, 0, 2]
+
+
+def test_ssrqrcp_wide_k_rejected_before_any_device_work():
+    import paper_1509_06820_b200 as P
+    with pytest.raises(NotImplementedError, match="k = 300"):
+        P.ssrqrcp(np.zeros((400, 400)), 300, P.RandomizedConfig(padding=8))
