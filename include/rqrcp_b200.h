@@ -190,6 +190,15 @@ int rq_column_norms(rq_handle_t h, const double* A, int64_t m, int64_t n, int64_
 int rq_frob_norm(rq_handle_t h, const double* A, int64_t m, int64_t n, int64_t lda,
                  double* out, void* stream);
 
+/* downdate_norms / NormTracker.downdate (kernels.py:189-192, 225-233):
+ * out[j] = sqrt(max(norms[j]^2 - row[j*inc]^2, 0)), bit-identical to numpy;
+ * when orig_sq and unsafe are given, unsafe[j] = (out[j]^2 before the root) <
+ * guard * orig_sq[j], the columns the caller must recompute exactly.
+ * Device pointers; out may alias norms. */
+int rq_downdate_norms(rq_handle_t h, const double* norms, const double* row, int64_t inc,
+                      int64_t n, const double* orig_sq, double guard, double* out,
+                      int32_t* unsafe, void* stream);
+
 /* ---------------------------------------------------------------- host Omega stream */
 
 /* count values of numpy's Philox(key = k0 + 2^64 k1).standard_normal() stream,

@@ -28,7 +28,26 @@ from .matio import (
     save_pgm,
 )
 from .qrcp import column_norms, qr_blocked, qr_presorted
-from .randomized import DegenerateSampleError, RandomizedConfig, rqrcp, rsrqrcp, ssrqrcp
+from .kernels import (
+    NormTracker,
+    Reflector,
+    apply_block_reflection,
+    apply_reflector,
+    compose_blocks,
+    downdate_norms,
+    form_reflector,
+)
+from .randomized import (
+    DegenerateSampleError,
+    RandomizedConfig,
+    SampleState,
+    make_sample,
+    rqrcp,
+    rsrqrcp,
+    sample_update,
+    select_pivots,
+    ssrqrcp,
+)
 from .rng import RngState, gaussian_matrix
 from .truncated import lq_factor, qr_blocked_device, trqrcp, tuxv
 
@@ -39,6 +58,17 @@ __version__ = "0.1.0"
 __all__ = [
     "BlockReflectors",
     "DegenerateSampleError",
+    "NormTracker",
+    "Reflector",
+    "SampleState",
+    "apply_block_reflection",
+    "apply_reflector",
+    "compose_blocks",
+    "downdate_norms",
+    "form_reflector",
+    "make_sample",
+    "sample_update",
+    "select_pivots",
     "Factorization",
     "MatrixFormatError",
     "OpCounters",

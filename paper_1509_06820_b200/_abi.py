@@ -72,6 +72,7 @@ SIGNATURES = {
     "rq_q_columns": (C.c_int, [vp, i64, i64, i64, dp, i64, dp, i64, dp, i64, vp]),
     "rq_column_norms": (C.c_int, [vp, dp, i64, i64, i64, C.c_int, dp, vp]),
     "rq_frob_norm": (C.c_int, [vp, dp, i64, i64, i64, dp, vp]),
+    "rq_downdate_norms": (C.c_int, [vp, dp, dp, i64, i64, dp, f64, dp, vp, vp]),
     "rq_launch_count": (C.c_int64, []),
     "rq_set_option": (C.c_int, [vp, C.c_char_p, i64]),
     "rq_debug_read": (C.c_int, [vp, C.POINTER(i64), C.c_int]),

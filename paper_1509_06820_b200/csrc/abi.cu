@@ -291,6 +291,16 @@ int rq_frob_norm(rq_handle_t h, const double* A, int64_t m, int64_t n, int64_t l
   return guarded_on(h, [&] { rq::frob_norm(H(h), A, m, n, lda, out, S(stream)); });
 }
 
+int rq_downdate_norms(rq_handle_t h, const double* norms, const double* row, int64_t inc,
+                      int64_t n, const double* orig_sq, double guard, double* out,
+                      int32_t* unsafe, void* stream) {
+  return guarded_on(h, [&] {
+    need(n >= 0 && inc >= 1, "bad shape");
+    need(norms != nullptr && row != nullptr && out != nullptr, "null argument");
+    rq::downdate_norms(norms, row, inc, n, orig_sq, guard, out, unsafe, S(stream));
+  });
+}
+
 int64_t rq_launch_count(void) { return rq::launch_count(); }
 
 int rq_set_option(rq_handle_t h, const char* name, int64_t value) {

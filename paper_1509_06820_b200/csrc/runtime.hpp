@@ -310,6 +310,10 @@ void frob_norm(Handle& h, const double* A, int64_t m, int64_t n, int64_t lda, do
                cudaStream_t s);
 void copy2d(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows,
             int64_t cols, cudaStream_t s, const Status* st = nullptr);
+// sqrt(max(norms^2 - row^2, 0)) elementwise, optional recompute flags (small.cu)
+void downdate_norms(const double* norms, const double* row, int64_t inc, int64_t n,
+                    const double* orig_sq, double guard, double* out, int32_t* unsafe,
+                    cudaStream_t s);
 // snapshot (restore = false) / conditional restore of a two-half panel's
 // columns, reflectors and level-2 counters (small.cu halves_guard_kernel)
 void halves_guard(Handle& h, double* work, int64_t ldw, int64_t mm, int64_t cols, Status* st,

@@ -381,6 +381,21 @@ __global__ void halves_guard_kernel(double* work, int64_t ldw, int64_t mm, int64
   }
   if (restore && t0 < cols) tau[t0] = 0.0;
 }
+// NormTracker.downdate / downdate_norms (kernels.py:189-192, 225-233):
+// new_sq = max(norm^2 - row^2, 0), in numpy's operation order (bit-identical);
+// with orig_sq, unsafe[j] = new_sq < guard * orig_sq[j] (the caller recomputes
+// those columns exactly).
+__global__ void norm_downdate_kernel(const double* norms, const double* row, int64_t inc,
+                                     int64_t n, const double* orig_sq, double guard, double* out,
+                                     int32_t* unsafe) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const double v = norms[j], r = row[j * inc];
+    const double sq = fmax(__dsub_rn(__dmul_rn(v, v), __dmul_rn(r, r)), 0.0);
+    out[j] = sqrt(sq);
+    if (unsafe != nullptr) unsafe[j] = orig_sq != nullptr && sq < __dmul_rn(guard, orig_sq[j]);
+  }
+}
 __global__ void fill2d_kernel(double* dst, int64_t ldd, int64_t rows, int64_t cols, double v,
                               const Status* st) {
   if (aborted(st)) return;
@@ -726,6 +741,16 @@ void copy2d(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t ro
             int64_t cols, cudaStream_t s, const Status* st) {
   if (rows <= 0 || cols <= 0) return;
   copy2d_kernel<<<grid_for(rows * cols, 148), 256, 0, s>>>(src, lds, dst, ldd, rows, cols, st);
+  RQ_CHECK_LAUNCH();
+  count_launch();
+}
+
+void downdate_norms(const double* norms, const double* row, int64_t inc, int64_t n,
+                    const double* orig_sq, double guard, double* out, int32_t* unsafe,
+                    cudaStream_t s) {
+  if (n <= 0) return;
+  norm_downdate_kernel<<<grid_for(n, 148), 256, 0, s>>>(norms, row, inc, n, orig_sq, guard, out,
+                                                       unsafe);
   RQ_CHECK_LAUNCH();
   count_launch();
 }

@@ -246,3 +246,138 @@ def ssrqrcp(A, k, config=None, omega=None):
             f"ssrqrcp with k = {k} > {SSRQRCP_MAX_K}: the single-sample panel is limited to "
             f"{SSRQRCP_MAX_K} columns on the GPU (the reference accepts any k)")
     return _randomized_factor(A, k, config, k + config.padding, k, _abi.RQ_SSRQRCP, False, omega)
+
+
+# ---------------------------------------------------------------- sample-level primitives
+# The reference's per-block building blocks (randomized.py:48-135) with its
+# signatures, for callers that drive the block loop themselves; each runs on
+# the C-ABI kernels the native driver uses (rq_sketch, rq_select_pivots,
+# rq_sample_update).  numpy in -> numpy out; CUDA tensors stay on the device.
+
+
+@dataclass
+class SampleState:
+    """The sketch and the pieces of its partial factorization
+    (randomized.py:48-66): after :func:`select_pivots` ``B`` holds the
+    transformed sample in pivoted column order, ``s11``/``s12``/``s22`` view
+    its blocks, ``reflectors`` are the sample-side Householder vectors and
+    ``frob_a`` is the Frobenius norm of the matrix being factored."""
+
+    B: object
+    ell: int
+    block: int = 0
+    s11: object = None
+    s12: object = None
+    s22: object = None
+    reflectors: BlockReflectors | None = None
+    frob_a: float = 0.0
+
+
+def _as_dev_f(x, dev):
+    return to_device_fortran(x, dev) if not (torch.is_tensor(x) and x.is_cuda) else \
+        (x if x.dtype == torch.float64 and x.dim() == 2 and x.stride(0) == 1 else
+         to_device_fortran(x, dev))
+
+
+def make_sample(A, ell, rng, counters=None):
+    """Sketch B = Omega A with a fresh ell x m standard Gaussian Omega drawn
+    from ``rng`` (randomized.py:69-82): the same host stream as the
+    reference, the product on the FP64 tensor-core GEMM (rq_sketch)."""
+    from .rng import gaussian_matrix
+    host = not (torch.is_tensor(A) and A.is_cuda)
+    dev = A.device if not host else require_cuda()
+    Ad = _as_dev_f(A, dev)
+    m, n = Ad.shape
+    if ell < 1:
+        raise ValueError("sample must have at least one row")
+    om = to_device_fortran(gaussian_matrix(rng, ell, m), dev)
+    B = fmat(ell, n, dev)
+    _abi.check(lib().rq_sketch(handle(dev), ell, m, n, ptr(om), ld(om), ptr(Ad), ld(Ad), ptr(B),
+                               ld(B), stream_ptr(dev)))
+    fr = torch.empty(1, dtype=torch.float64, device=dev)
+    _abi.check(lib().rq_frob_norm(handle(dev), ptr(Ad), m, n, ld(Ad), ptr(fr), stream_ptr(dev)))
+    if counters is not None:
+        counters.gemm_flops += 2 * ell * m * n
+        counters.bytes_touched += 8 * (ell * m + m * n + ell * n)
+    return SampleState(B=B.cpu().numpy() if host else B, ell=ell, frob_a=float(fr[0]))
+
+
+def select_pivots(sample, b, counters=None):
+    """b greedy steps of pivoted Householder elimination on the sample
+    (randomized.py:85-104): returns (local Permutation over the sample's
+    columns, pivots delivered) and leaves the transformed pivoted sample and
+    its blocks in ``sample``."""
+    B = sample.B
+    ell, nt = B.shape
+    if not 1 <= b <= min(ell, nt):
+        raise ValueError(f"cannot select {b} pivots from a {ell} x {nt} sample")
+    host = not (torch.is_tensor(B) and B.is_cuda)
+    dev = B.device if not host else require_cuda()
+    Bd = _as_dev_f(B, dev)
+    S = fmat(ell, nt, dev, fill=0.0)
+    piv = torch.zeros(b, dtype=torch.int64, device=dev)
+    Ys = fmat(ell, b, dev, fill=0.0)
+    taus = torch.zeros(b, dtype=torch.float64, device=dev)
+    got, l2 = C.c_int64(), C.c_int64()
+    _abi.check(lib().rq_select_pivots(handle(dev), ell, nt, b, ptr(Bd), ld(Bd), ptr(S), ld(S),
+                                      ptr(piv), ptr(Ys), ld(Ys), ptr(taus), C.byref(got),
+                                      C.byref(l2), stream_ptr(dev)))
+    g = int(got.value)
+    if counters is not None:
+        # apply_reflector counts 4 m n level-2 flops and touches A twice
+        # (16 m n bytes) per step: bytes = 4 x level-2 (kernels.py:47-56)
+        counters.level2_flops += int(l2.value)
+        counters.bytes_touched += 4 * int(l2.value)
+    perm = Permutation.identity(nt)
+    for j, p in enumerate(piv[:g].cpu().tolist()):
+        perm.swap(j, int(p))
+    out = S.cpu().numpy() if host else S
+    Y, tau = Ys[:, :g], taus[:g]
+    sample.B = out
+    sample.reflectors = BlockReflectors(Y.cpu().numpy() if host else Y,
+                                        tau.cpu().numpy() if host else tau)
+    sample.s11 = out[:g, :g]
+    sample.s12 = out[:g, g:]
+    sample.s22 = out[g:, g:]
+    return perm, g
+
+
+def sample_update(sample, R11, R12, counters=None):
+    """Downdate the sample past a completed block, B1 = S12 - S11 R11^{-1}
+    R12 stacked over S22 (randomized.py:107-135); raises
+    DegenerateSampleError when any |R11_jj| < eps^(3/4) * frob_a."""
+    b = R11.shape[0]
+    if sample.s11 is None or sample.s11.shape[0] != b:
+        raise ValueError("sample has no matching factorization to downdate")
+    host = not (torch.is_tensor(sample.B) and sample.B.is_cuda)
+    dev = sample.B.device if not host else require_cuda()
+    n2 = R12.shape[1]
+    if n2 == 0:
+        r = torch.as_tensor(np.asarray(R11) if not torch.is_tensor(R11) else R11,
+                            dtype=torch.float64).diagonal().abs()
+        if bool((r < np.finfo(np.float64).eps ** 0.75 * sample.frob_a).any()):
+            raise DegenerateSampleError("block triangle numerically singular; sample must be "
+                                        "re-sketched")
+        sample.B = np.zeros((sample.ell, 0)) if host else fmat(sample.ell, 0, dev)
+    else:
+        Sd = _as_dev_f(sample.B, dev)
+        R = fmat(b, b + n2, dev)
+        R[:, :b] = torch.as_tensor(R11, dtype=torch.float64, device=dev)
+        R[:, b:] = torch.as_tensor(R12, dtype=torch.float64, device=dev)
+        Bn = fmat(sample.ell, n2, dev, fill=0.0)
+        deg = C.c_int32()
+        _abi.check(lib().rq_sample_update(handle(dev), sample.ell, b, n2, ptr(Sd), ld(Sd), ptr(R),
+                                          C.c_void_p(R.data_ptr() + 8 * b * ld(R)), ld(R),
+                                          float(sample.frob_a), ptr(Bn), ld(Bn), C.byref(deg),
+                                          stream_ptr(dev)))
+        if deg.value:
+            raise DegenerateSampleError("block triangle numerically singular; sample must be "
+                                        "re-sketched")
+        if counters is not None:
+            counters.gemm_flops += 3 * b * b * n2
+            counters.bytes_touched += 8 * (b * b + b * n2 + b * b + b * n2 + b * n2)
+        sample.B = Bn.cpu().numpy() if host else Bn
+    sample.block += 1
+    sample.s11 = sample.s12 = sample.s22 = None
+    sample.reflectors = None
+    return sample

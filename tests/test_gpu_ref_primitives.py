@@ -1,0 +1,218 @@
+"""The reference's block-level primitives, with its signatures, on the B200:
+form_reflector / apply_reflector / compose_blocks / apply_block_reflection /
+downdate_norms / NormTracker (kernels.py:17-233) and SampleState /
+make_sample / select_pivots / sample_update (randomized.py:48-135), against
+the reference-generated known answers (tests/golden/kat_*.npz) and the oracle
+(oracle/port.py, bit-identical to the reference) on the same inputs.  A last
+test drives the reference's block loop (randomized.py:207-258) through these
+primitives and compares with the native driver."""
+
+import numpy as np
+import pytest
+
+from oracle import port
+from tests import _golden as G
+
+pytestmark = pytest.mark.gpu
+
+
+def test_form_reflector_known_answers():
+    import paper_1509_06820_b200 as P
+    rec = G.load("kat_reflector")
+    for i in range(6):
+        x = rec[f"x{i}"]
+        r = rec[f"r{i}"]
+        ref = P.form_reflector(x)
+        assert abs(ref.tau - r[0]) <= 1e-15 * max(1.0, abs(r[0])), i
+        assert abs(ref.beta - r[1]) <= 1e-15 * max(1.0, abs(r[1])), i
+        np.testing.assert_allclose(ref.v, r[2:], rtol=1e-15, atol=1e-16, err_msg=str(i))
+    with pytest.raises(ValueError, match="nonempty"):
+        P.form_reflector(np.zeros(0))
+
+
+def test_apply_reflector_and_counters():
+    import torch
+    import paper_1509_06820_b200 as P
+    g = np.random.default_rng(1)
+    A = g.standard_normal((70, 33))
+    r = P.form_reflector(A[:, 0])
+    X = A[:, 1:].copy()
+    ref = X - np.outer(r.tau * r.v, r.v @ X)
+    c = P.OpCounters()
+    out = P.apply_reflector(X, r.v, r.tau, c)
+    assert out is X
+    assert np.linalg.norm(X - ref) <= 1e-14 * np.linalg.norm(ref)
+    assert (c.level2_flops, c.bytes_touched) == (4 * 70 * 32, 2 * 8 * 70 * 32)
+    # device operands are updated in place on the device
+    Xd = torch.from_numpy(np.asfortranarray(A[:, 1:])).cuda()
+    P.apply_reflector(Xd, torch.from_numpy(r.v).cuda(), r.tau)
+    assert np.linalg.norm(Xd.cpu().numpy() - ref) <= 1e-14 * np.linalg.norm(ref)
+    # tau = 0 and empty blocks are no-ops, as in the reference
+    Z = A[:, :0]
+    assert P.apply_reflector(Z, r.v, r.tau) is Z
+
+
+def test_block_reflection_and_compose_vs_reference_formulas():
+    import paper_1509_06820_b200 as P
+    g = np.random.default_rng(2)
+    m = 90
+    # reflectors of two consecutive panels, as the reference builds them
+    M = g.standard_normal((m, 20))
+    Y = np.zeros((m, 20))
+    tau = np.zeros(20)
+    for j in range(20):
+        r = P.form_reflector(M[j:, j])
+        Y[j:, j] = r.v
+        tau[j] = r.tau
+        M[j:, j + 1:] -= np.outer(r.tau * r.v, r.v @ M[j:, j + 1:])
+    T1 = port.t_factor(Y[:, :12], tau[:12])
+    T2 = port.t_factor(Y[:, 12:], tau[12:])
+    Yc, Tc = P.compose_blocks(Y[:, :12], T1, Y[:, 12:], T2)
+    T_ref = np.zeros((20, 20))
+    T_ref[:12, :12], T_ref[12:, 12:] = T1, T2
+    T_ref[:12, 12:] = -T1 @ ((Y[:, :12].T @ Y[:, 12:]) @ T2)
+    np.testing.assert_array_equal(Yc, Y)
+    assert np.linalg.norm(Tc - T_ref) <= 1e-13 * np.linalg.norm(T_ref)
+    # composed T equals the single-block T of the whole reflector set
+    assert np.linalg.norm(Tc - port.t_factor(Y, tau)) <= 1e-12 * np.linalg.norm(Tc)
+    A = g.standard_normal((m, 45))
+    for transpose in (False, True):
+        X = A.copy()
+        c = P.OpCounters()
+        P.apply_block_reflection(X, Yc, Tc, transpose=transpose, counters=c)
+        W = (Tc.T if transpose else Tc) @ (Yc.T @ A)
+        ref = A - Yc @ W
+        assert np.linalg.norm(X - ref) <= 1e-13 * np.linalg.norm(ref)
+        assert c.gemm_flops == 4 * m * 20 * 45 + 20 * 20 * 45
+    with pytest.raises(ValueError, match="row mismatch"):
+        P.apply_block_reflection(np.zeros((5, 3)), Yc, Tc)
+
+
+def test_downdate_norms_and_tracker_bit_identical():
+    import paper_1509_06820_b200 as P
+    g = np.random.default_rng(3)
+    n = np.abs(g.standard_normal(300)) + 0.5
+    row = g.standard_normal(300) * 0.7
+    ref = np.sqrt(np.maximum(n * n - row * row, 0.0))
+    np.testing.assert_array_equal(P.downdate_norms(n, row), ref)
+    # the tracker reproduces the reference's (oracle's) downdates and
+    # recomputes exactly the columns the sqrt(eps) guard flags
+    A = np.asfortranarray(g.standard_normal((40, 64)))
+    A[:, 5] = A[:, 0] * (1 + 1e-9)          # forces a cancellation -> recompute
+    tr = P.NormTracker(A)
+    ref_tr = port.Norms(A)
+    np.testing.assert_array_equal(tr.norms, ref_tr.val)
+    W = A.copy()
+    for j in range(6):
+        p, nrm = tr.max_trailing(j)
+        q, nq = ref_tr.argmax_from(j)
+        assert (p, nrm) == (q, nq)
+        W[:, [j, p]] = W[:, [p, j]]
+        tr.swap(j, p)
+        ref_tr.swap(j, p)
+        r = P.form_reflector(W[j:, j])
+        W[j:, j + 1:] -= np.outer(r.tau * r.v, r.v @ W[j:, j + 1:])
+        W[j, j], W[j + 1:, j] = r.beta, 0.0
+        tr.downdate(j + 1, W[j, j + 1:], lambda c: W[j + 1:, c])
+        ref_tr.downdate(j + 1, W[j, j + 1:], lambda c: W[j + 1:, c])
+        np.testing.assert_allclose(tr.norms, ref_tr.val, rtol=1e-14, atol=0)
+
+
+def test_sample_primitives_match_oracle_and_known_answers():
+    import paper_1509_06820_b200 as P
+    # select_pivots on the reference's select known answers
+    rec = G.load("kat_select")
+    for key in sorted({k.rsplit("_", 1)[0] for k in rec}):
+        B = rec[f"{key}_B"]
+        want = int(rec[f"{key}_want"])
+        smp = P.SampleState(B=np.asfortranarray(B.copy()), ell=B.shape[0])
+        c = P.OpCounters()
+        perm, got = P.select_pivots(smp, want, c)
+        assert got == int(rec[f"{key}_got"]), key
+        np.testing.assert_array_equal(perm.forward, rec[f"{key}_perm"], err_msg=key)
+        np.testing.assert_array_equal(np.array(perm.swaps).reshape(-1, 2), rec[f"{key}_swaps"])
+        scale = float(np.linalg.norm(B))
+        assert np.linalg.norm(smp.B - rec[f"{key}_S"]) <= 1e-12 * scale, key
+        assert c.level2_flops == int(rec[f"{key}_l2"]), key
+        assert smp.s11.shape == (got, got) and smp.s22.shape == (B.shape[0] - got, B.shape[1] - got)
+    with pytest.raises(ValueError, match="cannot select 9 pivots"):
+        P.select_pivots(P.SampleState(B=np.ones((4, 6)), ell=4), 9)
+
+    # make_sample / select_pivots / sample_update vs the oracle, same stream
+    g = np.random.default_rng(4)
+    A = g.standard_normal((300, 220))
+    ell, b = 24, 16
+    s_gpu = P.make_sample(A, ell, P.RngState(7), c_gpu := P.OpCounters())
+    s_ref = port.sketch(A, ell, port.Stream(7), c_ref := port.Counters())
+    assert np.linalg.norm(s_gpu.B - s_ref.B) <= 1e-13 * np.linalg.norm(s_ref.B)
+    assert abs(s_gpu.frob_a - s_ref.frob_a) <= 1e-14 * s_ref.frob_a
+    assert (c_gpu.gemm_flops, c_gpu.bytes_touched) == (c_ref.gemm_flops, c_ref.bytes_touched)
+    s_gpu.B = s_ref.B.copy()                 # identical bytes from here on
+    perm_g, got_g = P.select_pivots(s_gpu, b)
+    perm_r, got_r = port.pick_pivots(s_ref, b, port.Counters())
+    assert got_g == got_r == b
+    np.testing.assert_array_equal(perm_g.forward, perm_r.forward)
+    # the panel on the chosen columns, then the sample downdate
+    W = A[:, perm_g.forward].copy()
+    Rfull = np.linalg.qr(W[:, :b], mode="r")
+    R12 = np.linalg.qr(W[:, :b])[0].T @ W[:, b:]
+    c1, c2 = P.OpCounters(), port.Counters()
+    P.sample_update(s_gpu, Rfull, R12, c1)
+    port.downdate_sample(s_ref, Rfull, R12, c2)
+    assert np.linalg.norm(s_gpu.B - s_ref.B) <= 1e-12 * np.linalg.norm(s_ref.B)
+    assert (c1.gemm_flops, c1.bytes_touched) == (c2.gemm_flops, c2.bytes_touched)
+    assert s_gpu.block == 1 and s_gpu.s11 is None
+    with pytest.raises(ValueError, match="no matching factorization"):
+        P.sample_update(s_gpu, Rfull, R12)
+    # a singular block triangle raises DegenerateSampleError
+    s3 = P.make_sample(A, ell, P.RngState(7))
+    P.select_pivots(s3, b)
+    Rbad = Rfull.copy()
+    Rbad[3, 3] = 0.0
+    with pytest.raises(P.DegenerateSampleError):
+        P.sample_update(s3, Rbad, R12)
+
+
+def test_reference_block_loop_through_the_primitives():
+    """The reference's _randomized_factor loop (randomized.py:207-258) written
+    against the drop-in primitives reproduces the native driver's pivots."""
+    import paper_1509_06820_b200 as P
+    A = np.random.default_rng(9).standard_normal((160, 130))
+    cfg = P.RandomizedConfig(block=16, padding=8, seed=0)
+    work = np.array(A, order="F")
+    m, n = work.shape
+    rng = P.RngState(cfg.seed)
+    frob = float(np.linalg.norm(work))
+    perm = P.Permutation.identity(n)
+    smp = P.make_sample(work, cfg.ell, rng)
+    smp.frob_a = frob
+    i0 = 0
+    while i0 < n:
+        want = min(cfg.block, n - i0)
+        lp, got = P.select_pivots(smp, want)
+        assert got == want
+        for a_, c_ in lp.swaps:
+            perm.swap(i0 + a_, i0 + c_)
+            if a_ != c_:
+                work[:, [i0 + a_, i0 + c_]] = work[:, [i0 + c_, i0 + a_]]
+        panel = work[i0:, i0:i0 + got].copy()
+        Y = np.zeros_like(panel)
+        tau = np.zeros(got)
+        for j in range(got):
+            r = P.form_reflector(panel[j:, j])
+            Y[j:, j], tau[j] = r.v, r.tau
+            P.apply_reflector(panel[j:, j + 1:], r.v, r.tau)
+            panel[j, j], panel[j + 1:, j] = r.beta, 0.0
+        work[i0:, i0:i0 + got] = panel
+        T = P.build_t_matrix(Y, tau)
+        C = work[i0:, i0 + got:]
+        if C.shape[1]:
+            C = np.array(C, order="F")
+            P.apply_block_reflection(C, Y, T, transpose=True)
+            work[i0:, i0 + got:] = C
+        i0 += got
+        if i0 < n:
+            P.sample_update(smp, work[i0 - got:i0, i0 - got:i0], work[i0 - got:i0, i0:])
+    f = P.rqrcp(A, None, cfg)
+    np.testing.assert_array_equal(perm.forward, f.perm.forward)
+    assert np.linalg.norm(work[:min(m, n)] - f.R) <= 1e-11 * np.linalg.norm(f.R)
