@@ -45,9 +45,10 @@ CONFIGS = {
     "cfg5": dict(driver="rqrcp", m=32768, n=32768, k=None, block=128, padding=8, kind="gauss",
                  desc="RQRCP full, 32768x32768 N(0,1), b=128, p=8"),
 }
-# bounded CPU samples of the same workload family for the oracle (cpu_baseline / --impl reference)
-CPU_SAMPLE = {"cfg1": 1000, "cfg2": 4096, "cfg3": 4096, "cfg4": 4000, "cfg5": 4096}
-REF_STEP_SAMPLE = {"cfg1": 1000, "cfg2": 2048, "cfg3": 4096, "cfg4": 2500, "cfg5": 2048}
+# bounded CPU sample of the same workload (n of the n x n instance of the same
+# recipe) for the oracle: one size for both cpu_baseline and --impl reference,
+# each run a few seconds on the box's host cores
+CPU_SAMPLE = {"cfg1": 1000, "cfg2": 2048, "cfg3": 4096, "cfg4": 2500, "cfg5": 2048}
 
 
 def std_flops(cfg, m=None, n=None, k=None):
@@ -121,6 +122,22 @@ def device_matrix(kind, m, n, device, seed=0):
         A.copy_(G1 @ G2 + 1e-6 * G3)
         return A
     raise ValueError(kind)
+
+
+def recipe_matrix(name, device):
+    """The configuration's A from the exact SURVEY.md §8(d) numpy recipe
+    (tests/golden/recipes.py, the bytes the parity goldens were generated
+    from), built on the host and uploaded: the bench and the full-size
+    parity tests factor the same matrix.  Input generation, outside every
+    timed region."""
+    import torch
+    from paper_1509_06820_b200.device import fmat
+    sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+    import recipes
+    Ah = recipes.build_as_golden(name)
+    A = fmat(Ah.shape[0], Ah.shape[1], device)
+    A.copy_(torch.from_numpy(Ah))
+    return A
 
 
 # ------------------------------------------------------------------ helpers
@@ -307,7 +324,7 @@ def main():
         torch.cuda.synchronize(dev)
 
     peak = fp64_peak() if rank == 0 else None
-    A = device_matrix(cfg["kind"], cfg["m"], cfg["n"], dev, seed=0 if world > 1 else rank)
+    A = recipe_matrix(args.config, dev)
     torch.cuda.synchronize(dev)
     lib = _abi.load_library()
     h = _abi.handle(local)
@@ -476,12 +493,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": args.config, "desc": cfg["desc"], "m": cfg["m"], "n": cfg["n"],
-                       "k": cfg["k"], "block": cfg["block"], "padding": cfg["padding"],
-                       "parallelism": (f"column-block-cyclic x{world} (NCCL)" if sharded
-                                       else "single GPU"),
-                       "l2": "inputs larger than L2 (A is 8*m*n bytes)",
-                       "input": "seeded numpy Gaussians; QR/products for the spectrum on GPU"},
+            "config": config_of(args.config, world, sharded),
             "pct_fp64_peak": (value / world / 1e3) / (peak["dmma_f64_tflops"] if peak else 37.2),
             "pct_fp64_peak_note": "per GPU, of the measured DMMA peak",
             "roofline": roofline,
@@ -504,6 +516,16 @@ def main():
         dist.destroy_process_group()
 
 
+def config_of(name, world, sharded):
+    cfg = CONFIGS[name]
+    return {"workload": name, "desc": cfg["desc"], "m": cfg["m"], "n": cfg["n"], "k": cfg["k"],
+            "block": cfg["block"], "padding": cfg["padding"],
+            "parallelism": (f"column-block-cyclic x{world} (NCCL)" if sharded else "single GPU"),
+            "l2": "inputs larger than L2 (A is 8*m*n bytes)",
+            "input": "exact SURVEY 8(d) numpy recipe (tests/golden/recipes.py), the bytes of "
+                     "the reference-generated parity goldens"}
+
+
 def traffic_from_profiles(family):
     """dram bytes per launch of the dominant kernel from the committed ncu
     summary (profiles/latest_traffic.json), or None."""
@@ -522,7 +544,7 @@ def main_reference(args, cfg, rank):
     cores, one bounded sample of the workload per step."""
     if rank != 0:
         return 0
-    n_s = REF_STEP_SAMPLE[args.config]
+    n_s = CPU_SAMPLE[args.config]
     for _ in range(args.warmup):
         cpu_run(args.config, n_s)
     vals, times = [], []
@@ -539,7 +561,7 @@ def main_reference(args, cfg, rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": args.config, "desc": cfg["desc"], "sample": sample},
+        "config": config_of(args.config, 1, False),
         "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": cores, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0,

@@ -206,11 +206,16 @@ class ShardedFactorization:
 
 
 def rqrcp_sharded(A_local: torch.Tensor, m: int, n: int, k=None, config=None, group=None,
-                  gather_r: bool = True) -> ShardedFactorization:
+                  gather_r: bool = True, kernels=None) -> ShardedFactorization:
     """Full/partial RQRCP of the column-block-cyclic distributed A
-    (randomized.py:183-266 semantics) on the ranks of `group`, one GPU each."""
-    from . import primitives as K
+    (randomized.py:183-266 semantics) on the ranks of `group`, one GPU each.
+
+    `kernels` supplies gemm / select_pivots / panel_qr / sample_update with
+    the signatures of paper_1509_06820_b200.primitives (the default, the
+    sm_100a kernels); the CPU multi-rank tests pass oracle-backed doubles."""
+    from . import primitives
     from .device import fmat
+    K = kernels if kernels is not None else primitives
     from .randomized import RandomizedConfig, _validate_rank
     from .rng import RngState, gaussian_matrix
 
@@ -270,16 +275,16 @@ def rqrcp_sharded(A_local: torch.Tensor, m: int, n: int, k=None, config=None, gr
                 if a != c:
                     perm[[a, c]] = perm[[c, a]]
             exchange_columns(work, layout, swap_plan(piv, got, i0), me, group)
-            meta = torch.zeros(1, dtype=torch.int64, device=dev)
+            meta = torch.zeros(2, dtype=torch.int64, device=dev)   # usable, panel level-2 flops
             lp = layout.local_index(i0)
             if me == owner:
                 P = fmat(m - i0, got, dev)
                 P.copy_(work[i0:, lp:lp + got])
                 Yp, tp, T, usable, l2p = K.panel_qr(P, tol=tol, with_t=True)
-                meta[0] = usable
-                ctr["level2_flops"] += l2p
+                meta[0], meta[1] = usable, l2p
             broadcast(meta, owner, group)
-            usable = int(meta.item())
+            usable = int(meta[0].item())
+            ctr["level2_flops"] += int(meta[1].item())
             if usable < got and not resampled:
                 B = sketch(i0)
                 ctr["resamples"] += 1

@@ -111,3 +111,82 @@ def test_exchange_and_gather_world2(n, b):
         assert p.exitcode == 0
     for rank, res in out:
         assert all(res.values()), (rank, res)
+
+
+# ---------------------------------------------------------------- the whole driver at world 2 / 3
+
+def _driver_worker(rank, world, port_, kind, m, n, b, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port_)
+    torch.set_num_threads(1)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1509_06820_b200.parallel import rqrcp_sharded
+        from paper_1509_06820_b200.randomized import RandomizedConfig
+        from tests import _cpu_kernels
+        A = _driver_matrix(kind, m, n)
+        L = BlockCyclic(n, b, world)
+        local = torch.from_numpy(shard(A, L, rank).copy())
+        f = rqrcp_sharded(local, m, n, None, RandomizedConfig(block=b, padding=8, seed=0),
+                          gather_r=True, kernels=_cpu_kernels)
+        q.put((rank, f.rank, f.perm.tolist(), f.swaps, f.R.numpy(), f.Y.numpy(),
+               dict(f.counters)))
+    finally:
+        dist.destroy_process_group()
+
+
+def _driver_matrix(kind, m, n):
+    g = np.random.default_rng(11)
+    if kind == "gauss":
+        return g.standard_normal((m, n))
+    if kind == "geom":   # 14 decades: resamples near the noise floor
+        U = np.linalg.qr(g.standard_normal((m, m)))[0][:, :n]
+        V = np.linalg.qr(g.standard_normal((n, n)))[0]
+        return (U * 10.0 ** (-14.0 * np.arange(n) / (n - 1))) @ V.T
+    return g.standard_normal((m, 9)) @ g.standard_normal((9, n))   # rank 9
+
+
+@pytest.mark.parametrize("world,kind,m,n,b", [(2, "gauss", 60, 50, 8), (3, "gauss", 70, 64, 6),
+                                              (2, "geom", 96, 80, 8), (3, "lowrank", 48, 40, 4)])
+def test_sharded_driver_matches_single_process_reference(world, kind, m, n, b):
+    """parallel.rqrcp_sharded runs its whole multi-rank control flow (sketch
+    all-gather, replicated selection, cross-rank swaps, owner panel +
+    broadcast, local trailing updates, R12 all-gather, sample update and
+    resamples) on `world` gloo ranks, with oracle-backed kernels; the result
+    must be the reference algorithm's (oracle/port.py = reference,
+    tests/test_oracle_golden.py): same rank, pivots, swaps and resample
+    count, R and Y to rounding -- up to the noise floor for rank-deficient
+    inputs."""
+    from oracle import port
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port_ = _free_port()
+    procs = [ctx.Process(target=_driver_worker, args=(r, world, port_, kind, m, n, b, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted([q.get(timeout=300) for _ in procs], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    A = _driver_matrix(kind, m, n)
+    o = port.rqrcp(A, None, b, 8, 0)
+    frob = np.linalg.norm(A)
+    d = np.abs(np.diag(o.R))
+    bad = d <= 1e3 * np.finfo(float).eps * frob
+    r_sig = int(np.argmax(bad)) if bad.any() else d.size
+    for rank, f_rank, perm, swaps, R, Y, ctr in out:
+        # every rank holds the same replicated decisions
+        assert perm == out[0][2] and swaps == out[0][3]
+        np.testing.assert_array_equal(np.asarray(perm)[:r_sig], o.perm.forward[:r_sig])
+        mine = np.zeros((R.shape[0], n))
+        mine[:, perm] = R
+        theirs = o.perm.restore(o.R)
+        assert np.linalg.norm(mine[:r_sig] - theirs[:r_sig]) <= 1e-12 * np.linalg.norm(theirs[:r_sig])
+        if r_sig == min(m, n):
+            assert f_rank == o.rank
+            assert swaps == [tuple(s) for s in o.perm.swaps]
+            assert ctr["resamples"] == o.counters.resamples
+            assert (ctr["gemm_flops"], ctr["level2_flops"]) == (o.counters.gemm_flops,
+                                                               o.counters.level2_flops)
+            assert np.linalg.norm(Y - o.Y) <= 1e-12 * np.linalg.norm(o.Y)
