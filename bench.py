@@ -344,11 +344,14 @@ def main():
         A_loc.copy_(A[:, idx])
         del A
         torch.cuda.empty_cache()
-        if cfg["driver"] != "rqrcp":
-            raise SystemExit("multi-GPU bench: only the RQRCP configs are sharded")
+        if cfg["driver"] == "tuxv":
+            raise SystemExit("multi-GPU bench: TUXV is not sharded (RQRCP and TRQRCP are)")
+        from paper_1509_06820_b200.parallel import trqrcp_sharded
         cfgP = P.RandomizedConfig(block=cfg["block"], padding=cfg["padding"], seed=0)
 
         def step(P_, cfg_, A_, _x):
+            if cfg_["driver"] == "trqrcp":
+                return trqrcp_sharded(A_loc, cfg_["m"], cfg_["n"], cfg_["k"], cfgP, gather=False)
             return rqrcp_sharded(A_loc, cfg_["m"], cfg_["n"], cfg_["k"], cfgP, gather_r=False)
         A = None
     else:

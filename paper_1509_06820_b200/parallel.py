@@ -347,6 +347,190 @@ def rqrcp_sharded(A_local: torch.Tensor, m: int, n: int, k=None, config=None, gr
 
 
 
+@dataclass
+class ShardedTruncated:
+    """Result of `trqrcp_sharded`: replicated Y, tau, permutation; this rank's
+    columns of R (k x n) and rows of W (n x k, stored transposed as k x
+    n_local, one column per position), and, when gathered, the full R and W."""
+
+    Y: torch.Tensor
+    tau: torch.Tensor
+    perm: np.ndarray
+    swaps: list
+    rank: int
+    R_local: torch.Tensor
+    Wt_local: torch.Tensor
+    R: torch.Tensor | None = None
+    W: torch.Tensor | None = None
+    layout: BlockCyclic | None = None
+    counters: dict = field(default_factory=dict)
+
+
+def trqrcp_sharded(A_local: torch.Tensor, m: int, n: int, k: int, config=None, group=None,
+                   gather: bool = True, kernels=None) -> ShardedTruncated:
+    """Truncated RQRCP (no trailing update) of the column-block-cyclic
+    distributed A, truncated.py:70-174 semantics.  A is never modified: the
+    rows of W and the columns of R follow A's columns (swapped together,
+    truncated.py:114), Y is replicated.  Per block every rank forms its own
+    columns of G = Y_b^T A - (Y_b^T Y) W^T, of W and of the new R rows; the
+    owner of the block's columns forms and broadcasts the panel; R12 is
+    all-gathered for the replicated sample update; a resample sketches each
+    rank's columns implicitly (Omega A - (Omega Y) W^T, truncated.py:53-67)
+    and all-gathers them."""
+    from . import primitives
+    from .device import fmat
+    from .randomized import RandomizedConfig, _validate_rank
+    from .rng import RngState, gaussian_matrix
+    K = kernels if kernels is not None else primitives
+
+    config = config if config is not None else RandomizedConfig()
+    world = dist.get_world_size(group)
+    me = dist.get_rank(group)
+    b, ell = config.block, config.ell
+    layout = BlockCyclic(n, b, world)
+    k = _validate_rank(k, m, n)
+    if k == 0:
+        raise ValueError("rank must be >= 1")
+    if ell > m:
+        raise ValueError(f"sample rows {ell} exceed matrix rows {m}")
+    dev = A_local.device
+    nloc = layout.n_local(me)
+    work = fmat(m, nloc, dev)
+    work.copy_(A_local)
+    ss = (work * work).sum().reshape(1)
+    dist.all_reduce(ss, group=group)
+    frob = float(ss.sqrt().item())
+    tol = EPS * frob
+    rng = RngState(config.seed)
+    Y = fmat(m, k, dev, fill=0.0)
+    tau = torch.zeros(k, dtype=torch.float64, device=dev)
+    Wt = fmat(k, nloc, dev, fill=0.0)     # W^T: column = position
+    R = fmat(k, nloc, dev, fill=0.0)
+    perm = np.arange(n)
+    swaps: list = []
+    ctr = {"gemm_flops": 0, "level2_flops": 0, "resamples": 0}
+
+    def sketch(i0: int) -> torch.Tensor:
+        om = _f(torch.from_numpy(gaussian_matrix(rng, ell, m - i0)).to(dev))
+        lc = layout.first_local_at_or_after(me, i0)
+        local = K.gemm(om, _f(work[i0:, lc:]))                     # Omega A (my columns)
+        ctr["gemm_flops"] += 2 * ell * (m - i0) * (n - i0)
+        if i0:
+            Z = K.gemm(om, _f(Y[i0:, :i0]))                         # Omega Y
+            if local.shape[1]:
+                K.gemm(Z, _f(Wt[:i0, lc:]), local, alpha=-1.0, beta=1.0)
+            ctr["gemm_flops"] += 2 * ell * (m - i0) * i0 + 2 * ell * i0 * (n - i0)
+        return _f(allgather_positions(local, layout, i0, me, group))
+
+    B = sketch(0)
+    rank_out = k
+    i0 = 0
+    while i0 < k:
+        want = min(b, k - i0)
+        owner = layout.owner(i0)
+        lp = layout.local_index(i0)
+        resampled = False
+        while True:
+            S, piv, got, _, _, l2 = K.select_pivots(B, want)
+            ctr["level2_flops"] += l2
+            if got < want and not resampled:
+                B = sketch(i0)
+                ctr["resamples"] += 1
+                resampled = True
+                continue
+            if got == 0:
+                bw = 0
+                break
+            for j in range(got):
+                a, c = i0 + j, i0 + piv[j]
+                swaps.append((a, c))
+                if a != c:
+                    perm[[a, c]] = perm[[c, a]]
+            moves = swap_plan(piv, got, i0)
+            for M_ in (work, Wt, R):                                # A's columns and followers
+                exchange_columns(M_, layout, moves, me, group)
+            meta = torch.zeros(2, dtype=torch.int64, device=dev)
+            if me == owner:
+                # materialise the selected columns: A[i0:, sel] - Y[i0:, :i0] W[sel, :i0]^T
+                P = fmat(m - i0, got, dev)
+                P.copy_(work[i0:, lp:lp + got])
+                if i0:
+                    K.gemm(_f(Y[i0:, :i0]), _f(Wt[:i0, lp:lp + got]), P, alpha=-1.0, beta=1.0)
+                Yp, tp, T, usable, l2p = K.panel_qr(P, tol=tol, with_t=True)
+                meta[0], meta[1] = usable, l2p
+            if i0:
+                ctr["gemm_flops"] += 2 * (m - i0) * i0 * got
+            broadcast(meta, owner, group)
+            usable = int(meta[0].item())
+            ctr["level2_flops"] += int(meta[1].item())
+            if usable < got and not resampled:
+                B = sketch(i0)
+                ctr["resamples"] += 1
+                resampled = True
+                continue
+            bw = usable
+            if bw:
+                rows = max(m - i0, 2 * bw)
+                blk = fmat(rows, 2 * bw + 1, dev, fill=0.0)
+                if me == owner:
+                    blk[: m - i0, :bw] = Yp[:, :bw]
+                    blk[:bw, bw:2 * bw] = T[:bw, :bw]
+                    blk[:bw, 2 * bw] = tp[:bw]
+                    blk[bw:2 * bw, bw:2 * bw] = P[:bw, :bw]        # R11
+                    R[i0:i0 + bw, lp:lp + bw] = P[:bw, :bw]
+                broadcast(blk, owner, group)
+                Y[i0:, i0:i0 + bw] = blk[: m - i0, :bw]
+                tau[i0:i0 + bw] = blk[:bw, 2 * bw]
+                T = _f(blk[:bw, bw:2 * bw])
+                R11 = _f(blk[bw:2 * bw, bw:2 * bw])
+            break
+        if bw == 0:
+            rank_out = i0
+            break
+        nt2 = n - i0 - bw
+        lc = layout.first_local_at_or_after(me, i0 + bw)
+        if nt2:
+            Yb = _f(Y[i0:, i0:i0 + bw])
+            if work.shape[1] > lc:
+                # G = Y_b^T A[i0:, mine] - (Y_b^T Y[i0:, :i0]) W[mine, :i0]^T   (truncated.py:144-149)
+                G = K.gemm(Yb, _f(work[i0:, lc:]), transa=True)
+                if i0:
+                    Z = K.gemm(Yb, _f(Y[i0:, :i0]), transa=True)
+                    K.gemm(Z, _f(Wt[:i0, lc:]), G, alpha=-1.0, beta=1.0)
+                # W[mine, i0:i0+bw] = (T^T G)^T, stored transposed
+                Wt[i0:i0 + bw, lc:] = K.gemm(T, G, transa=True)
+                # R[i0:i0+bw, mine] = A[i0:i0+bw, mine] - Y[i0:i0+bw, :i0+bw] W[mine, :i0+bw]^T
+                Rn = _f(work[i0:i0 + bw, lc:])
+                K.gemm(_f(Y[i0:i0 + bw, :i0 + bw]), _f(Wt[:i0 + bw, lc:]), Rn, alpha=-1.0,
+                       beta=1.0)
+                R[i0:i0 + bw, lc:] = Rn
+            ctr["gemm_flops"] += (2 * (m - i0) * bw * nt2
+                                  + (2 * (m - i0) * bw * i0 + 2 * bw * i0 * nt2 if i0 else 0)
+                                  + bw * bw * nt2 + 2 * bw * (i0 + bw) * nt2)
+        i0 += bw
+        if bw < want:
+            rank_out = i0
+            break
+        if i0 < k:
+            R12 = allgather_positions(_f(R[i0 - bw:i0, lc:]), layout, i0, me, group)
+            Bn, degenerate = K.sample_update(S, bw, R11, _f(R12), frob)
+            if degenerate:
+                B = sketch(i0)
+                ctr["resamples"] += 1
+            else:
+                B = Bn
+                ctr["gemm_flops"] += 3 * bw * bw * (n - i0)
+    R_local = R[:rank_out, :].clone()
+    Wt_local = Wt[:rank_out, :].clone()
+    Rg = Wg = None
+    if gather:
+        Rg = _f(allgather_positions(R_local, layout, 0, me, group))
+        Wg = allgather_positions(Wt_local, layout, 0, me, group).t()
+    return ShardedTruncated(Y=Y[:, :rank_out], tau=tau[:rank_out], perm=perm, swaps=swaps,
+                            rank=rank_out, R_local=R_local, Wt_local=Wt_local, R=Rg, W=Wg,
+                            layout=layout, counters=ctr)
+
+
 def _f(t: torch.Tensor) -> torch.Tensor:
     """Column-major copy (or view) of a 2-D tensor for the C-ABI."""
     from .device import fmat, is_fortran

@@ -72,3 +72,23 @@ def test_sharded_world1_larger_vs_oracle(group, m, n, b):
     s = rqrcp_sharded(torch.from_numpy(np.asfortranarray(A)).cuda(), m, n, None, cfg)
     np.testing.assert_array_equal(s.perm, o.perm.forward)
     assert np.linalg.norm(s.R.cpu().numpy() - o.R) <= 1e-10 * np.linalg.norm(o.R)
+
+
+@pytest.mark.parametrize("m,n,k,b", [(1200, 1000, 256, 64), (2000, 1500, 300, 32)])
+def test_sharded_trqrcp_world1_vs_oracle(group, m, n, k, b):
+    """The column-block-cyclic TRQRCP driver (parallel.trqrcp_sharded) on the
+    B200 through NCCL: pivots identical to the reference algorithm, R and W
+    to 1e-10."""
+    import torch
+    import paper_1509_06820_b200 as P
+    from oracle import port
+    from paper_1509_06820_b200.parallel import trqrcp_sharded
+    A = np.random.default_rng(m + k).standard_normal((m, n))
+    cfg = P.RandomizedConfig(block=b, padding=8, seed=0)
+    o = port.trqrcp(A, k, b, 8, 0)
+    s = trqrcp_sharded(torch.from_numpy(np.asfortranarray(A)).cuda(), m, n, k, cfg)
+    assert s.rank == o.rank
+    np.testing.assert_array_equal(s.perm, o.perm.forward)
+    assert np.linalg.norm(s.R.cpu().numpy() - o.R) <= 1e-10 * np.linalg.norm(o.R)
+    assert np.linalg.norm(s.W.cpu().numpy() - o.W) <= 1e-10 * np.linalg.norm(o.W)
+    assert s.counters["resamples"] == o.counters.resamples

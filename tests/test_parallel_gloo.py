@@ -190,3 +190,71 @@ def test_sharded_driver_matches_single_process_reference(world, kind, m, n, b):
             assert (ctr["gemm_flops"], ctr["level2_flops"]) == (o.counters.gemm_flops,
                                                                o.counters.level2_flops)
             assert np.linalg.norm(Y - o.Y) <= 1e-12 * np.linalg.norm(o.Y)
+
+
+def _trq_worker(rank, world, port_, kind, m, n, k, b, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port_)
+    torch.set_num_threads(1)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1509_06820_b200.parallel import trqrcp_sharded
+        from paper_1509_06820_b200.randomized import RandomizedConfig
+        from tests import _cpu_kernels
+        A = _driver_matrix(kind, m, n)
+        L = BlockCyclic(n, b, world)
+        local = torch.from_numpy(shard(A, L, rank).copy())
+        f = trqrcp_sharded(local, m, n, k, RandomizedConfig(block=b, padding=8, seed=0),
+                           kernels=_cpu_kernels)
+        q.put((rank, f.rank, f.perm.tolist(), f.swaps, f.R.numpy(), f.W.numpy(), f.Y.numpy(),
+               dict(f.counters)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,kind,m,n,k,b", [(2, "gauss", 60, 70, 32, 8),
+                                                (3, "gauss", 64, 50, 30, 6),
+                                                (2, "geom", 96, 80, 64, 8),
+                                                (3, "lowrank", 48, 40, 20, 4)])
+def test_sharded_trqrcp_matches_single_process_reference(world, kind, m, n, k, b):
+    """parallel.trqrcp_sharded (truncated.py:70-174 control flow, A never
+    updated, W rows and R columns following A's columns across ranks, the
+    implicit resketch all-gathered) against the reference algorithm."""
+    from oracle import port
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port_ = _free_port()
+    procs = [ctx.Process(target=_trq_worker, args=(r, world, port_, kind, m, n, k, b, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted([q.get(timeout=300) for _ in procs], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    A = _driver_matrix(kind, m, n)
+    o = port.trqrcp(A, k, b, 8, 0)
+    frob = np.linalg.norm(A)
+    d = np.abs(np.diag(o.R))
+    bad = d <= 1e3 * np.finfo(float).eps * frob
+    r_sig = int(np.argmax(bad)) if bad.any() else d.size
+    for rank, f_rank, perm, swaps, R, W, Y, ctr in out:
+        assert perm == out[0][2] and swaps == out[0][3]
+        np.testing.assert_array_equal(np.asarray(perm)[:r_sig], o.perm.forward[:r_sig])
+        mine = np.zeros((R.shape[0], n))
+        mine[:, perm] = R
+        theirs = o.perm.restore(o.R)
+        assert np.linalg.norm(mine[:r_sig] - theirs[:r_sig]) <= 1e-12 * np.linalg.norm(theirs[:r_sig])
+        if r_sig == min(k, o.rank) and o.rank == k:
+            assert f_rank == o.rank
+            assert swaps == [tuple(s) for s in o.perm.swaps]
+            assert ctr["resamples"] == o.counters.resamples
+            assert (ctr["gemm_flops"], ctr["level2_flops"]) == (o.counters.gemm_flops,
+                                                               o.counters.level2_flops)
+            # a reflector (and W column) is determined to ~ eps ||A|| / |R_jj|
+            # relative: compare column by column against that conditioning
+            eps = np.finfo(float).eps
+            for j in range(o.rank):
+                tol_j = max(1e-12, 100 * eps * frob / d[j])
+                assert np.linalg.norm(Y[:, j] - o.Y[:, j]) <= tol_j * np.linalg.norm(o.Y[:, j])
+                assert np.linalg.norm(W[:, j] - o.W[:, j]) <= tol_j * max(np.linalg.norm(o.W[:, j]), 1e-300)
