@@ -391,6 +391,10 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
     mark(1);
     // ---- my columns, one 8-lane group per column: relabel (swap j <-> p),
     //      pivot column, apply H_j, downdate, next-step candidate key
+    // each group keeps its best key of the step in a register; one shared
+    // atomic per warp after the loop (a shared atomicMax per column made the
+    // 64 groups of a CTA serialise on one address every step)
+    unsigned long long gbest = 0ull;
     for (int c = grp; c < ncol; c += NG) {
       double* col = colp(c);
       // read the column state before any lane of the group writes it
@@ -408,6 +412,69 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
         if (gl == 0) pos[c] = p;
       }
       if (pc <= j) continue;
+      if (ell <= 160) {
+        // Register form: every row j + gl + 8k of the column is loaded before
+        // any is used, so a column costs one memory round trip (the spilled
+        // columns of wide samples live in L2/HBM: the loop form below waited
+        // for one pair of loads per FMA step, ~37 us per pivot step on
+        // cfg5's 136 x 32768 sample).  Arithmetic and order are the loop
+        // form's: d0 takes rows j+gl+16q, d1 rows j+gl+8+16q, a lone tail
+        // row goes to d0.
+        double xr[20];
+#pragma unroll
+        for (int k = 0; k < 20; ++k) {
+          const int r = j + gl + 8 * k;
+          xr[k] = r < ell ? col[r] : 0.0;
+        }
+        if (tau != 0.0) {
+          double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+          for (int k = 0; k < 20; k += 2) {
+            const int r0 = j + gl + 8 * k;
+            if (r0 + 8 < ell) {
+              d0 = __fma_rn(vbuf[r0], xr[k], d0);
+              d1 = __fma_rn(vbuf[r0 + 8], xr[k + 1], d1);
+            } else if (r0 < ell) {
+              d0 = __fma_rn(vbuf[r0], xr[k], d0);
+            }
+          }
+          double w = __dadd_rn(d0, d1);
+#pragma unroll
+          for (int off = 4; off; off >>= 1) w = __dadd_rn(w, __shfl_xor_sync(gmask, w, off, 8));
+#pragma unroll
+          for (int k = 0; k < 20; ++k) {
+            const int r = j + gl + 8 * k;
+            if (r < ell) {
+              xr[k] = __dsub_rn(xr[k], __dmul_rn(tvbuf[r], w));
+              col[r] = xr[k];
+            }
+          }
+        }
+        if (j + 1 < a.nt) {
+          // NormTracker.downdate with row j (lane 0 of the group holds it)
+          const double row = __shfl_sync(gmask, xr[0], 0, 8);
+          double nsq = __dsub_rn(__dmul_rn(nv, nv), __dmul_rn(row, row));
+          nsq = nsq > 0.0 ? nsq : 0.0;
+          double nn;
+          if (!(nsq < __dmul_rn(kGuard, og))) {
+            nn = sqrt(nsq);
+            if (gl == 0) nrm[c] = nn;
+          } else {
+            __syncwarp(gmask);   // the group's stores are visible
+            double s0 = 0.0;
+            for (int r = j + 1 + gl; r < ell; r += 8) s0 = __fma_rn(col[r], col[r], s0);
+#pragma unroll
+            for (int off = 4; off; off >>= 1) s0 = __dadd_rn(s0, __shfl_xor_sync(gmask, s0, off, 8));
+            nn = sqrt(s0);
+            if (gl == 0) {
+              nrm[c] = nn;
+              orig[c] = __dmul_rn(nn, nn);
+            }
+          }
+          gbest = max(gbest, make_key(nn, pc));
+        }
+        continue;
+      }
       if (tau != 0.0) {
         double d0 = 0.0, d1 = 0.0;
         int i = j + gl;
@@ -443,9 +510,16 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
             orig[c] = __dmul_rn(nn, nn);
           }
         }
-        if (gl == 0) atomicMax(&s_bkey, make_key(nn, pc));
+        gbest = max(gbest, make_key(nn, pc));
       }
     }
+    // warp max of the groups' keys (every lane of a group holds the same gbest)
+#pragma unroll
+    for (int off = 8; off <= 16; off <<= 1) {
+      const unsigned long long o = __shfl_xor_sync(0xffffffffu, gbest, off);
+      gbest = o > gbest ? o : gbest;
+    }
+    if (lane == 0 && gbest != 0ull) atomicMax(&s_bkey, gbest);
     mark(2);
     publish((j + 1) % 3, par ^ 1);
     mark(3);

@@ -86,6 +86,37 @@ def test_select_pivots_wide_sample_vs_oracle():
         assert np.linalg.norm(S.cpu().numpy() - smp.B) <= 1e-12 * np.linalg.norm(B)
 
 
+@pytest.mark.parametrize("ell,nt,want,ctas", [(136, 5000, 128, 4), (72, 6000, 64, 3),
+                                                (40, 3000, 32, 2), (160, 2500, 100, 2)])
+def test_select_pivots_spilled_columns_vs_oracle(ell, nt, want, ctas):
+    """The shared-memory selection kernel with most columns spilled to global
+    memory (a few CTAs for a wide sample, as beside cfg5's trailing update):
+    bit-for-bit the oracle's pivots, S to rounding, the same result as the
+    register-resident path."""
+    from paper_1509_06820_b200 import _abi
+    from paper_1509_06820_b200.primitives import select_pivots
+    lib, h = _abi.load_library(), _abi.handle(0)
+    g = np.random.default_rng(ell + nt)
+    B = g.standard_normal((ell, nt)) * np.exp(g.uniform(-2, 2, nt))
+    smp = port.Sample(B=np.asfortranarray(B.copy()), ell=ell)
+    perm, got = port.pick_pivots(smp, want, port.Counters())
+    try:
+        lib.rq_set_option(h, b"select_reg", 0)
+        lib.rq_set_option(h, b"force_select", 1)
+        lib.rq_set_option(h, b"select_max_ctas", ctas)
+        S, piv, got_d, *_ = select_pivots(_dev(B), want)
+    finally:
+        lib.rq_set_option(h, b"select_reg", 1)
+        lib.rq_set_option(h, b"force_select", 0)
+        lib.rq_set_option(h, b"select_max_ctas", 0)
+    assert got_d == got
+    fwd = list(range(nt))
+    for j, p in enumerate(piv):
+        fwd[j], fwd[p] = fwd[p], fwd[j]
+    np.testing.assert_array_equal(fwd, perm.forward)
+    assert np.linalg.norm(S.cpu().numpy() - smp.B) <= 1e-12 * np.linalg.norm(B)
+
+
 def test_panel_matches_reference_fixtures():
     from paper_1509_06820_b200.primitives import panel_qr
     rec = G.load("kat_panel")

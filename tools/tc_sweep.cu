@@ -179,13 +179,18 @@ void sweep(const Shape& s, const double* A, const double* B, int reps, int which
   if (which == 0) {   // generic large
     TCO(TA, TB, 64, 64, 16, 32, 32, 3, 3, false);
     TC(TA, TB, 64, 64, 16, 32, 32, 3, 3, false);
-    TCO(TA, TB, 128, 64, 16, 64, 32, 3, 2, false);
     TC(TA, TB, 128, 64, 16, 64, 32, 3, 2, false);
+  } else if (which == 2) {   // A^T with M = 32 (b = 32 inner products)
+    TC(TA, TB, 32, 64, 16, 16, 32, 4, 4, false);
+    TC(TA, TB, 32, 128, 16, 32, 32, 3, 3, false);
+    TC(TA, TB, 32, 128, 16, 16, 64, 3, 3, false);
+    TC(TA, TB, 32, 64, 16, 32, 16, 4, 5, false);
+    TC(TA, TB, 32, 128, 32, 32, 32, 3, 2, false);
+    TC(TA, TB, 32, 64, 32, 16, 32, 3, 4, false);
+    TC(TA, TB, 64, 64, 16, 32, 32, 3, 3, false);
   } else {
-    TCO(TA, TB, 48, 64, 16, 16, 32, 4, 4, false);
-    TC(TA, TB, 48, 64, 16, 16, 32, 4, 3, false);
-    TCO(TA, TB, 80, 64, 16, 16, 32, 3, 3, false);
-    TC(TA, TB, 80, 64, 16, 16, 32, 3, 2, false);
+    TC(TA, TB, 48, 64, 16, 16, 32, 4, 4, false);
+    TC(TA, TB, 80, 64, 16, 16, 32, 3, 3, false);
   }
 }
 
@@ -206,6 +211,8 @@ int main(int argc, char** argv) {
       {"square_8192", false, false, 8192, 8192, 8192},
       {"inner_b128_cfg5", true, false, 128, 32640, 32768},
       {"trq_G_cfg3", true, false, 64, 16320, 16384},
+      {"trq_G_cfg4", true, false, 32, 11968, 20000},
+      {"trq_G_cfg4_late", true, false, 32, 11776, 19800},
       {"tuxv_AV", false, false, 20000, 256, 12000},
       {"sketch_cfg3", false, false, 72, 16384, 16384},
       {"sketch_cfg5", false, false, 136, 32768, 32768},
@@ -217,7 +224,7 @@ int main(int argc, char** argv) {
     const double* b = B;
     if (s.M == 8192 || s.M == 20000) { a = B; b = A; }   // tall A from the big buffer
     if (s.M == 8192) b = B + 8192ull * 8192;
-    const int which = (s.M == 72 || s.M == 136) ? 1 : 0;
+    const int which = (s.M == 72 || s.M == 136) ? 1 : (s.M == 32 ? 2 : 0);
     if (s.ta && !s.tb) sweep<true, false>(s, a, b, reps, which);
     else sweep<false, false>(s, a, b, reps, which);
   }
