@@ -9,7 +9,8 @@ dev = torch.device("cuda", 0)
 lib = _abi.load_library(); h = _abi.handle(0)
 lib.rq_set_option(h, b"debug_timers", 1)
 names = ["gramA", "reduce1", "chol+inv", "gramB", "reduce2", "serial2", "applyC"]
-for mm, bw, q in ((8192, 64, 0), (8192, 64, 48), (4096, 64, 48), (8192, 32, 48)):
+for mm, bw, q in ((8192, 64, 0), (8192, 64, 48), (4096, 64, 48), (2048, 64, 0), (1024, 64, 0),
+                  (8192, 32, 48)):
     lib.rq_set_option(h, b"fast_panel_max_ctas", q)
     P0 = np.random.default_rng(1).standard_normal((mm, bw))
     for _ in range(3):
