@@ -395,6 +395,17 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
     // atomic per warp after the loop (a shared atomicMax per column made the
     // 64 groups of a CTA serialise on one address every step)
     unsigned long long gbest = 0ull;
+    // this lane's rows j + gl + 8k of v, loaded once per step for all of its
+    // columns (register form below); tau v is re-formed per use with the
+    // same rounding as tvbuf
+    double vk[20];
+    if (ell <= 160) {
+#pragma unroll
+      for (int k = 0; k < 20; ++k) {
+        const int r = j + gl + 8 * k;
+        vk[k] = r < ell ? vbuf[r] : 0.0;
+      }
+    }
     for (int c = grp; c < ncol; c += NG) {
       double* col = colp(c);
       // read the column state before any lane of the group writes it
@@ -432,10 +443,10 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
           for (int k = 0; k < 20; k += 2) {
             const int r0 = j + gl + 8 * k;
             if (r0 + 8 < ell) {
-              d0 = __fma_rn(vbuf[r0], xr[k], d0);
-              d1 = __fma_rn(vbuf[r0 + 8], xr[k + 1], d1);
+              d0 = __fma_rn(vk[k], xr[k], d0);
+              d1 = __fma_rn(vk[k + 1], xr[k + 1], d1);
             } else if (r0 < ell) {
-              d0 = __fma_rn(vbuf[r0], xr[k], d0);
+              d0 = __fma_rn(vk[k], xr[k], d0);
             }
           }
           double w = __dadd_rn(d0, d1);
@@ -445,7 +456,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
           for (int k = 0; k < 20; ++k) {
             const int r = j + gl + 8 * k;
             if (r < ell) {
-              xr[k] = __dsub_rn(xr[k], __dmul_rn(tvbuf[r], w));
+              xr[k] = __dsub_rn(xr[k], __dmul_rn(__dmul_rn(tau, vk[k]), w));
               col[r] = xr[k];
             }
           }
