@@ -513,8 +513,10 @@ int Factor::overlap_split(int64_t i0, int64_t bw) const {
       // shared-memory v4: its step time grows with the columns per CTA
       // (~ell*nt1/P), the update's with its rows (~mm*nt1/(sms-P)); balance
       // the two per block.  Constant fitted on cfg5 (32768^2, ell = 136):
-      // fixed 16/24/32/44/60 CTAs gave select 2366/1689/1307/949/680 ms and
-      // update 1072/1140/1216/1356/1591 ms per factorization
+      // round 1, fixed 16/24/32/44/60 CTAs gave select 2366/1689/1307/949/680
+      // ms and update 1072/1140/1216/1356/1591 ms per factorization; after
+      // the register-held v rows (round 2) sel_balance 145/200/260/340 gave
+      // 2217/2142/2163/2301 ms (profiles/r02_cfg5_sel_balance.jsonl)
       const double mm = (double)(m_ - i0 - bw);
       P = (int)(sms / (1.0 + 1e-6 * h_.sel_balance * mm * 136.0 / (double)ell_) + 0.5);
     }
