@@ -187,6 +187,46 @@ def broadcast(t: torch.Tensor, src: int, group=None) -> torch.Tensor:
     return t
 
 
+def _panel(K, P, tol):
+    """panel_householder + _panel_rank + build_t_matrix of the owner's panel
+    (qrcp.py:206-219, randomized.py:150-155).  With the GPU kernels a 65..128
+    column panel runs as two 64-column halves (the recursive panel QR the
+    native driver uses: the first 64 reflectors from the first 64 columns,
+    applied to the rest, whose rows below 64 are factored next, T = [[T1,
+    -T1 (Y1^T Y2) T2], [0, T2]]), so both halves take the CholeskyQR2 fast
+    path; a half that is not full rank falls back to the whole panel on the
+    original columns, whose level-2 count and rank cut the reference defines."""
+    mm, got = P.shape
+    from . import primitives
+    if K is not primitives or not 64 < got <= 128 or mm < got + 64:
+        return K.panel_qr(P, tol=tol, with_t=True)
+    from .device import fmat
+    orig = fmat(mm, got, P.device)
+    orig.copy_(P)
+    h2 = got - 64
+    P1 = P[:, :64]
+    Y1, t1, T1, u1, l2a = K.panel_qr(P1, tol=tol, with_t=True)
+    if u1 == 64:
+        P2 = P[:, 64:]
+        X = K.gemm(T1, K.gemm(Y1, P2, transa=True), transa=True)     # T1^T (Y1^T P2)
+        K.gemm(Y1, X, P2, alpha=-1.0, beta=1.0)                       # P2 -= Y1 X
+        Y2, t2, T2, u2, l2b = K.panel_qr(P[64:, 64:], tol=tol, with_t=True)
+        if u2 == h2:
+            Y = fmat(mm, got, P.device, fill=0.0)
+            Y[:, :64] = Y1
+            Y[64:, 64:] = Y2
+            T = fmat(got, got, P.device, fill=0.0)
+            T[:64, :64] = T1
+            T[64:, 64:] = T2
+            G = K.gemm(_f(Y1[64:]), Y2, transa=True)                    # Y1^T Y2 (rows >= 64)
+            T[:64, 64:] = K.gemm(T1, K.gemm(G, T2), alpha=-1.0)
+            # reflectors 1..64 applied to columns 65..got (apply_reflector counts)
+            l2x = 4 * sum((mm - j) * h2 for j in range(64))
+            return Y, torch.cat([t1, t2]), T, got, l2a + l2b + l2x
+    P.copy_(orig)
+    return K.panel_qr(P, tol=tol, with_t=True)
+
+
 # ---------------------------------------------------------------- driver
 
 @dataclass
@@ -280,7 +320,7 @@ def rqrcp_sharded(A_local: torch.Tensor, m: int, n: int, k=None, config=None, gr
             if me == owner:
                 P = fmat(m - i0, got, dev)
                 P.copy_(work[i0:, lp:lp + got])
-                Yp, tp, T, usable, l2p = K.panel_qr(P, tol=tol, with_t=True)
+                Yp, tp, T, usable, l2p = _panel(K, P, tol)
                 meta[0], meta[1] = usable, l2p
             broadcast(meta, owner, group)
             usable = int(meta[0].item())
@@ -456,7 +496,7 @@ def trqrcp_sharded(A_local: torch.Tensor, m: int, n: int, k: int, config=None, g
                 P.copy_(work[i0:, lp:lp + got])
                 if i0:
                     K.gemm(_f(Y[i0:, :i0]), _f(Wt[:i0, lp:lp + got]), P, alpha=-1.0, beta=1.0)
-                Yp, tp, T, usable, l2p = K.panel_qr(P, tol=tol, with_t=True)
+                Yp, tp, T, usable, l2p = _panel(K, P, tol)
                 meta[0], meta[1] = usable, l2p
             if i0:
                 ctr["gemm_flops"] += 2 * (m - i0) * i0 * got
