@@ -160,6 +160,8 @@ def allgather_positions(local_tail: torch.Tensor, layout: BlockCyclic, pos0: int
     (rows x (n - pos0)) tensor on every rank."""
     world = layout.world
     rows = local_tail.shape[0]
+    if world == 1:
+        return local_tail                 # the rank's tail is already in position order
     counts = [int(np.sum(layout.positions(r) >= pos0)) for r in range(world)]
     width = max(counts) if counts else 0
     pad = torch.zeros((rows, width), dtype=local_tail.dtype, device=local_tail.device)
@@ -168,12 +170,16 @@ def allgather_positions(local_tail: torch.Tensor, layout: BlockCyclic, pos0: int
     gathered = [torch.empty_like(flat) for _ in range(world)]
     dist.all_gather(gathered, flat, group=group)
     out = torch.empty((rows, layout.n - pos0), dtype=local_tail.dtype, device=local_tail.device)
+    cache = layout.__dict__.setdefault("_gather_idx", {})
     for r in range(world):
-        p = layout.positions(r)
-        p = p[p >= pos0] - pos0
-        if p.size:
-            idx = torch.as_tensor(p, device=local_tail.device)
-            out[:, idx] = gathered[r][: p.size].t()
+        key = (pos0, r, str(local_tail.device))
+        idx = cache.get(key)
+        if idx is None:
+            p = layout.positions(r)
+            p = p[p >= pos0] - pos0
+            idx = cache[key] = torch.as_tensor(p, device=local_tail.device)
+        if idx.numel():
+            out[:, idx] = gathered[r][: idx.numel()].t()
     return out
 
 
@@ -313,7 +319,7 @@ def rqrcp_sharded(A_local: torch.Tensor, m: int, n: int, k=None, config=None, gr
                 a, c = i0 + j, i0 + piv[j]
                 swaps.append((a, c))
                 if a != c:
-                    perm[[a, c]] = perm[[c, a]]
+                    perm[a], perm[c] = perm[c], perm[a]
             exchange_columns(work, layout, swap_plan(piv, got, i0), me, group)
             meta = torch.zeros(2, dtype=torch.int64, device=dev)   # usable, panel level-2 flops
             lp = layout.local_index(i0)
@@ -485,7 +491,7 @@ def trqrcp_sharded(A_local: torch.Tensor, m: int, n: int, k: int, config=None, g
                 a, c = i0 + j, i0 + piv[j]
                 swaps.append((a, c))
                 if a != c:
-                    perm[[a, c]] = perm[[c, a]]
+                    perm[a], perm[c] = perm[c], perm[a]
             moves = swap_plan(piv, got, i0)
             for M_ in (work, Wt, R):                                # A's columns and followers
                 exchange_columns(M_, layout, moves, me, group)
