@@ -329,6 +329,7 @@ int rq_set_option(rq_handle_t h, const char* name, int64_t value) {
     else if (n == "use_tc") hh.use_tc = value != 0;
     else if (n == "tc_variant") hh.tc_variant = (int)value;
     else if (n == "tc_splits") hh.tc_splits = (int)value;
+    else if (n == "tc_tma") hh.tc_tma = value != 0;
     else if (n == "overlap_select") hh.overlap_select = value != 0;
     else if (n == "overlap_sel_ctas") hh.overlap_sel_ctas = (int)value;
     else if (n == "sel_balance") hh.sel_balance = (int)value;

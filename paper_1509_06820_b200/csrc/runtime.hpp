@@ -115,6 +115,7 @@ class Handle {
   bool use_tc = true;                       // plain GEMMs through tc_gemm (tc_gemm.cu)
   int tc_variant = -1;                      // tc_gemm tile family override (-1 = by shape)
   int tc_splits = 0;                        // tc_gemm split-K override (0 = by shape)
+  bool tc_tma = true;                       // tc_gemm operands through TMA (tc_tma.cuh; 16-byte aligned operands)
 
   bool use_rank_update = true;
   bool fast_panel = true;   // CholeskyQR2 + Householder reconstruction panel (panel_fast.cu)
