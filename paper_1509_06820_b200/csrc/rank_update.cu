@@ -669,6 +669,10 @@ bool rank_update(Handle& h, int64_t M, int64_t N, int64_t K, const double* Y, in
                  const Status* st, int cat, int max_ctas, Status* snap, const double* Csrc,
                  int64_t ldcs, int extra_rows) {
   if (K < 4 || (K > kKMax && K != 128) || (K % 4) != 0 || M <= 0 || N <= 0) return false;
+  // the TMA-fed grouped kernel (rank_update_tma.cu) for K in {32, 64, 128}
+  if (Csrc == nullptr && extra_rows == 0 &&
+      rank_update_tma(h, M, N, K, Y, ldy, X, ldx, C, ldc, s, st, cat, max_ctas, snap))
+    return true;
   kernel_attr((const void*)rank_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
               (int)kRuSmem);
   const auto al = [](const double* p, int64_t ld) { return ((uintptr_t)p & 15) == 0 && ld % 2 == 0; };

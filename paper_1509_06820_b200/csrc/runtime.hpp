@@ -134,6 +134,7 @@ class Handle {
   bool ru_two_ctas = false;  // rank update: two single-buffered CTAs per SM
   int ru_skew_ns = 0;
   bool ru_big = true;        // rank update: 128 x 64 tiles, C through registers
+  bool ru_tma = true;        // rank update: the TMA-fed kernel (rank_update_tma.cu) where it applies
   bool inner_kernel = true;  // H = P^T C: tall-skinny split-K kernel (csrc/inner.cu)
   int inner_ktiles = 16;     // ... k-tiles (32 deep) per CTA
   bool inner32 = true;       // ... also for 32-row blocks (b = 32)
@@ -189,6 +190,12 @@ void gemm(Handle& h, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double a
 bool tc_gemm(Handle& h, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha,
              const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
              int64_t ldc, cudaStream_t s, const Status* st, int cat);
+
+// TMA-fed persistent C -= Y X for K in {32, 64} (rank_update_tma.cu); false if
+// not applicable (option ru_tma off, shape, alignment)
+bool rank_update_tma(Handle& h, int64_t M, int64_t N, int64_t K, const double* Y, int64_t ldy,
+                     const double* X, int64_t ldx, double* C, int64_t ldc, cudaStream_t s,
+                     const Status* st, int cat, int max_ctas, Status* snap);
 
 // persistent C -= Y X for K <= 64 (rank_update.cu); false if not applicable
 bool rank_update(Handle& h, int64_t M, int64_t N, int64_t K, const double* Y, int64_t ldy,

@@ -7,6 +7,7 @@
 #include "runtime.hpp"
 #include "tc_gemm.cuh"
 #include "tc_tma.cuh"
+#include "tma_util.hpp"
 
 namespace rq {
 
@@ -105,52 +106,17 @@ int tc_pick(const Handle& h, bool ta, int64_t M) {
   return 0;
 }
 
-// ---- TMA-fed variants (tc_tma.cuh)
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiledFn encode_tiled() {
-  static EncodeTiledFn fn = nullptr;
-  if (fn == nullptr) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    RQ_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
-    if (p == nullptr || q != cudaDriverEntryPointSuccess)
-      throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
-    fn = (EncodeTiledFn)p;
-  }
-  return fn;
-}
-
-// 2-d tensor map of a column-major FP64 matrix: `inner` contiguous rows,
-// `outer` columns, leading dimension ld; box inner x outer, swizzled
-CUtensorMap tensor_map(const double* base, int64_t inner, int64_t outer, int64_t ld, int box_in,
-                       int box_out, CUtensorMapSwizzle swz) {
-  CUtensorMap m;
-  const cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
-  const cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
-  const cuuint32_t box[2] = {(cuuint32_t)box_in, (cuuint32_t)box_out};
-  const cuuint32_t es[2] = {1, 1};
-  const CUresult r = encode_tiled()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)base, dims,
-                                    strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
-                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed");
-  return m;
-}
-
+// ---- TMA-fed variants (tc_tma.cuh); tensor maps from tma_util.hpp
 template <bool TA, bool TB, int BM, int BN, int WM, int WN, int ST, int MINB>
 void tma_launch(Handle& h, GemmArgs g, cudaStream_t s, int forced_splits) {
   using Cfg = TmaCfg<TA, TB, BM, BN, WM, WN>;
   auto kern = tc_tma_kernel<TA, TB, BM, BN, WM, WN, ST, MINB>;
   constexpr size_t smem = (size_t)ST * Cfg::kStage + 1024;
   kernel_attr((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const CUtensorMap ta = TA ? tensor_map(g.A, g.K, g.M, g.lda, 8, BM, CU_TENSOR_MAP_SWIZZLE_64B)
-                            : tensor_map(g.A, g.M, g.K, g.lda, 16, 16, CU_TENSOR_MAP_SWIZZLE_128B);
-  const CUtensorMap tb = TB ? tensor_map(g.B, g.N, g.K, g.ldb, 16, 16, CU_TENSOR_MAP_SWIZZLE_128B)
-                            : tensor_map(g.B, g.K, g.N, g.ldb, 8, BN, CU_TENSOR_MAP_SWIZZLE_64B);
+  const CUtensorMap ta = TA ? tensor_map_f64(g.A, g.K, g.M, g.lda, 8, BM, CU_TENSOR_MAP_SWIZZLE_64B)
+                            : tensor_map_f64(g.A, g.M, g.K, g.lda, 16, 16, CU_TENSOR_MAP_SWIZZLE_128B);
+  const CUtensorMap tb = TB ? tensor_map_f64(g.B, g.N, g.K, g.ldb, 16, 16, CU_TENSOR_MAP_SWIZZLE_128B)
+                            : tensor_map_f64(g.B, g.K, g.N, g.ldb, 8, BN, CU_TENSOR_MAP_SWIZZLE_64B);
   const int64_t gm = (g.M + BM - 1) / BM, gn = (g.N + BN - 1) / BN;
   const int64_t ktiles = (g.K + Cfg::BK - 1) / Cfg::BK;
   const int sp = choose_splits(gm * gn, ktiles, h.num_sms * MINB, 8, g.M * g.N, forced_splits);
@@ -191,6 +157,41 @@ void tma_dispatch(Handle& h, const GemmArgs& g, cudaStream_t s, int v, int sp) {
 bool aligned16(const double* p, int64_t ld) { return ((uintptr_t)p & 15) == 0 && (ld % 2) == 0; }
 
 }  // namespace
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  if (fn == nullptr) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    RQ_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (p == nullptr || q != cudaDriverEntryPointSuccess)
+      throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+    fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+// 2-d tensor map of a column-major FP64 matrix: `inner` contiguous rows,
+// `outer` columns, leading dimension ld; box inner x outer, swizzled
+CUtensorMap tensor_map_f64(const double* base, int64_t inner, int64_t outer, int64_t ld, int box_in,
+                       int box_out, CUtensorMapSwizzle swz) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
+  const cuuint32_t box[2] = {(cuuint32_t)box_in, (cuuint32_t)box_out};
+  const cuuint32_t es[2] = {1, 1};
+  const CUresult r = encode_tiled()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)base, dims,
+                                    strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed");
+  return m;
+}
 
 bool tc_gemm(Handle& h, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha,
              const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
