@@ -516,7 +516,8 @@ int Factor::overlap_split(int64_t i0, int64_t bw) const {
       // round 1, fixed 16/24/32/44/60 CTAs gave select 2366/1689/1307/949/680
       // ms and update 1072/1140/1216/1356/1591 ms per factorization; after
       // the register-held v rows (round 2) sel_balance 145/200/260/340 gave
-      // 2217/2142/2163/2301 ms (profiles/r02_cfg5_sel_balance.jsonl)
+      // 2217/2142/2163/2301 ms, and after the TMA trailing update 150/175/
+      // 200/230 gave 2020/1988/1968/1958 ms (profiles/r02_cfg5_sel_balance.jsonl)
       const double mm = (double)(m_ - i0 - bw);
       P = (int)(sms / (1.0 + 1e-6 * h_.sel_balance * mm * 136.0 / (double)ell_) + 0.5);
     }

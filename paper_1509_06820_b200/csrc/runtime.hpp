@@ -139,7 +139,7 @@ class Handle {
   int inner_ktiles = 16;     // ... k-tiles (32 deep) per CTA
   bool inner32 = true;       // ... also for 32-row blocks (b = 32)
   int overlap_sel_ctas = 0;   // SMs for the overlapped select (0 = size heuristic)
-  int sel_balance = 200;      // v4 select/update balance constant (x 1e-6, overlap_split; cfg5 sweep 145-340: profiles/r02_cfg5_sel_balance.jsonl)
+  int sel_balance = 230;      // v4 select/update balance constant (x 1e-6, overlap_split; cfg5 sweeps: profiles/r02_cfg5_sel_balance.jsonl)
   bool gemm_vec16 = true;
   long long* dbg = nullptr;  // optional device phase-timer buffer (debug)
 
