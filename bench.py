@@ -438,10 +438,11 @@ def main():
         i = _abi.PROF_NAMES.index(dom)
         ach = FL[i] / (MS[i] * 1e-3) / 1e12
         pk = peak["dmma_f64_tflops"] if peak else 37.2
-        kname = {"update": "rank_update_big_kernel<b> (C -= Y X, K = b, persistent 128x64 tiles)",
-                 "inner": "tc_gemm_kernel (G = Y^T C, split-K)",
-                 "sketch": "tc_gemm_kernel (B = Omega A)",
-                 "small_gemm": "tc_gemm_kernel (small products)"}.get(dom, dom)
+        kname = {"update": "rank_update_grouped_kernel (C -= Y X, K = b; TMA, one CTA/SM of "
+                           "three 4-warp groups on 64x64 tiles)",
+                 "inner": "tc_tma_kernel (G = Y^T C, TMA-fed, split-K)",
+                 "sketch": "tc_tma_kernel (B = Omega A, TMA-fed)",
+                 "small_gemm": "tc_tma_kernel / block_finish_kernel (small products)"}.get(dom, dom)
         roofline = {"bound": "tensor", "kernel": kname, "achieved": ach,
                     "peak": pk, "unit": "TFLOP/s", "frac": ach / pk,
                     "traffic": traffic_from_profiles(dom),

@@ -3,7 +3,8 @@
 # the ncu launch list of the cfg2 timed pass, DRAM traffic of the roofline
 # kernel and one --set full capture of it.  Outputs in gpurun_out/r2.
 set -u
-o=gpurun_out/r2; mkdir -p $o
+o=${OUT:-gpurun_out/r2}; mkdir -p $o
+timeout 1500 python -m pytest tests -m gpu -x -q > $o/gputest.log 2>&1; tail -2 $o/gputest.log
 timeout 900 python bench.py --steps 20 --warmup 5 > $o/bench_cfg2.json 2> $o/bench_cfg2.err
 timeout 600 python bench.py --impl reference --steps 5 --warmup 1 > $o/bench_ref_cfg2.json 2> $o/bench_ref_cfg2.err
 for c in ${CONFIGS:-cfg3 cfg4 cfg5 cfg1}; do
@@ -13,9 +14,9 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --n
   --csv --log-file $o/launches_cfg2.csv python bench.py --config cfg2 --steps 1 --warmup 3 \
   --no-cpu-baseline --no-e2e > $o/ncu_launch.log 2>&1
 timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
-  --clock-control none -k regex:rank_update_big -c 200 --csv --log-file $o/traffic_update_cfg2.csv \
+  --clock-control none -k regex:rank_update_grouped -c 200 --csv --log-file $o/traffic_update_cfg2.csv \
   python bench.py --config cfg2 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > $o/ncu_traffic.log 2>&1
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:rank_update_big -s 20 -c 1 \
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:rank_update_grouped -s 20 -c 1 \
   -o $o/ncu_update_cfg2 python bench.py --config cfg2 --steps 1 --warmup 1 --no-cpu-baseline \
   --no-e2e > $o/ncu_full.log 2>&1
 tail -c 400 $o/bench_*.json
