@@ -225,7 +225,8 @@ def rqrcp(A, k=None, config=None, omega=None):
     return _randomized_factor(A, k, config, config.ell, config.block, _abi.RQ_RQRCP, True, omega)
 
 
-SSRQRCP_MAX_K = 256   # widest panel the native driver factors in one block (driver.cu)
+SSRQRCP_MAX_K = 256     # widest panel the native driver factors in one block (driver.cu)
+SSRQRCP_MAX_ELL = 1024  # rows of the pivot kernel's sample (select.cu)
 
 
 def rsrqrcp(A, k=None, config=None, omega=None):
@@ -239,13 +240,131 @@ def ssrqrcp(A, k, config=None, omega=None):
     """One (k + padding)-row sketch selects all k pivots (randomized.py:299-313)."""
     config = config if config is not None else RandomizedConfig()
     k = int(k)
-    if k > SSRQRCP_MAX_K:
-        # one panel of width k: the GPU panel kernels and the pivot selection
-        # keep a panel's b x b working set on chip (DESIGN.md §9 known limits)
+    if k + config.padding > SSRQRCP_MAX_ELL:
         raise NotImplementedError(
-            f"ssrqrcp with k = {k} > {SSRQRCP_MAX_K}: the single-sample panel is limited to "
-            f"{SSRQRCP_MAX_K} columns on the GPU (the reference accepts any k)")
+            f"ssrqrcp with k = {k}: the (k + padding)-row sample exceeds the pivot kernel's "
+            f"{SSRQRCP_MAX_ELL} rows (the reference accepts any k)")
+    if k > SSRQRCP_MAX_K:
+        return _ssrqrcp_wide(A, k, config, omega)
     return _randomized_factor(A, k, config, k + config.padding, k, _abi.RQ_SSRQRCP, False, omega)
+
+
+def _ssrqrcp_wide(A, k, config, omega):
+    """ssrqrcp with k > SSRQRCP_MAX_K: the reference's single block
+    (randomized.py:207-258 with block width k and no trailing update) driven
+    from the host over the C-ABI kernels -- the (k + p)-row sketch
+    (rq_sketch), k pivot steps on it (rq_select_pivots), the panel QR of the k
+    chosen columns as a blocked QR (rq_qr_blocked, 64-column panels: the
+    Householder QR of the column-by-column panel, to rounding), _panel_rank
+    on its diagonal (randomized.py:150-155) with the resample branches, and
+    the block reflection for the R rows (randomized.py:158-180).  Counters
+    follow the reference's formulas (the panel's level-2 count is the
+    column-by-column one)."""
+    from .device import fmat
+    from .factorization import t_factor
+    from .rng import gaussian_matrix
+    from .truncated import qr_blocked_device
+    m, n = _shape_of(A)
+    k = _validate_rank(k, m, n)
+    if k == 0:
+        raise ValueError("rank must be >= 1")
+    ell = k + config.padding
+    if ell > m:
+        raise ValueError(f"sample rows {ell} exceed matrix rows {m}")
+    host = not (torch.is_tensor(A) and A.is_cuda)
+    dev = A.device if not host else require_cuda()
+    work = to_device_fortran(A, dev)
+    ctr = OpCounters()
+    fr = torch.empty(1, dtype=torch.float64, device=dev)
+    _abi.check(lib().rq_frob_norm(handle(dev), ptr(work), m, n, ld(work), ptr(fr), stream_ptr(dev)))
+    frob = float(fr[0])
+    tol = np.finfo(np.float64).eps * frob
+    rng = RngState(config.seed)
+    first = [omega]
+
+    def sketch():
+        om = first[0]
+        first[0] = None
+        if om is None:
+            return make_sample(work, ell, rng, ctr)
+        rng.position = ell * m   # the explicit Omega replaces the first draw
+        omd = to_device_fortran(om, dev)
+        B = fmat(ell, n, dev)
+        _abi.check(lib().rq_sketch(handle(dev), ell, m, n, ptr(omd), ld(omd), ptr(work), ld(work),
+                                   ptr(B), ld(B), stream_ptr(dev)))
+        ctr.gemm_flops += 2 * ell * m * n
+        ctr.bytes_touched += 8 * (ell * m + m * n + ell * n)
+        return SampleState(B=B, ell=ell)
+
+    if omega is not None and not (torch.is_tensor(omega) and omega.is_cuda):
+        omega = np.asarray(omega, dtype=np.float64)
+        if omega.shape != (ell, m):
+            raise ValueError(f"omega must be {ell} x {m}")
+    smp = sketch()
+    smp.frob_a = frob
+    perm = Permutation.identity(n)
+    resampled = False
+    Y = tau = None
+    bw = 0
+    while True:
+        local, got = select_pivots(smp, k, ctr)
+        if got < k and not resampled:
+            smp = sketch()
+            smp.frob_a = frob
+            ctr.resamples += 1
+            resampled = True
+            continue
+        if got == 0:
+            break
+        for a_, c_ in local.swaps:          # _apply_local_swaps (randomized.py:138-147)
+            perm.swap(a_, c_)
+        work = work[:, torch.as_tensor(local.forward, device=dev)]
+        work = to_device_fortran(work, dev)
+        Yp, tp, Rp = qr_blocked_device(work[:, :got], None, 64)
+        taus = tp.cpu().numpy()
+        for j in range(got):               # panel_householder's apply_reflector counts
+            if taus[j] != 0.0 and got - j - 1 > 0:
+                ctr.level2_flops += 4 * (m - j) * (got - j - 1)
+                ctr.bytes_touched += 16 * (m - j) * (got - j - 1)
+        d = torch.diagonal(Rp[:, :got]).abs().cpu().numpy()
+        bad = d <= tol
+        usable = int(np.argmax(bad)) if bad.any() else got
+        if usable < got and not resampled:
+            smp = sketch()
+            smp.frob_a = frob
+            ctr.resamples += 1
+            resampled = True
+            continue
+        bw = usable
+        if bw:
+            work[:bw, :bw] = Rp[:bw, :bw]
+            work[bw:, :bw] = 0.0
+            Y, tau = Yp[:, :bw], tp[:bw]
+        break
+    if bw and n > bw:
+        # _block_stages without the trailing update: R12 = C[:b] - Y[:b] (T^T (Y^T C))
+        from . import primitives as K
+        Yb = to_device_fortran(Y, dev)
+        T = t_factor(Yb, tau)
+        C_ = to_device_fortran(work[:, bw:], dev)
+        X = K.gemm(T, K.gemm(Yb, C_, transa=True), transa=True)
+        R12 = to_device_fortran(work[:bw, bw:], dev)
+        K.gemm(to_device_fortran(Yb[:bw], dev), X, R12, alpha=-1.0, beta=1.0)
+        work[:bw, bw:] = R12
+        nt2 = n - bw
+        ctr.gemm_flops += 2 * m * bw * nt2 + bw * bw * nt2 + 2 * bw * bw * nt2
+        ctr.bytes_touched += 8 * (m * nt2 + m * bw + bw * nt2)
+    if not bw:
+        Y = fmat(m, 0, dev)
+        tau = torch.zeros(0, dtype=torch.float64, device=dev)
+    R = work[:bw, :].clone()
+    if host:
+        Y, tau, R = (t.cpu().numpy() for t in (Y, tau, R))
+        perm = Permutation(forward=np.asarray(perm.forward), swaps=perm.swaps)
+    else:
+        perm = Permutation(forward=torch.as_tensor(perm.forward, device=dev), swaps=perm.swaps)
+    return Factorization(reflectors=BlockReflectors(Y, tau), R=R, perm=perm, rank=bw,
+                         counters=ctr, trailing=None)
 
 
 # ---------------------------------------------------------------- sample-level primitives

@@ -98,7 +98,7 @@ def test_permutation_semantics():
     assert list(q.forward) == [3, 1, 4, 0, 2]
 
 
-def test_ssrqrcp_wide_k_rejected_before_any_device_work():
+def test_ssrqrcp_sample_beyond_the_pivot_kernel_rejected_before_any_device_work():
     import paper_1509_06820_b200 as P
-    with pytest.raises(NotImplementedError, match="k = 300"):
-        P.ssrqrcp(np.zeros((400, 400)), 300, P.RandomizedConfig(padding=8))
+    with pytest.raises(NotImplementedError, match="k = 1100"):
+        P.ssrqrcp(np.zeros((1200, 1200)), 1100, P.RandomizedConfig(padding=8))

@@ -335,3 +335,50 @@ def test_b128_second_half_decline_rewinds_to_original_columns():
     rebuilt[f.rank:, f.rank:] = f.trailing
     res = np.linalg.norm(A[:, pf] - f.q_factor(full=True) @ rebuilt)
     assert res <= 1e-12 * frob
+
+
+@pytest.mark.parametrize("m,n,k,kind", [(1000, 900, 300, "gauss"), (800, 1200, 520, "gauss"),
+                                        (900, 700, 400, "lowrank")])
+def test_ssrqrcp_wider_than_one_native_panel_vs_oracle(m, n, k, kind):
+    """ssrqrcp(A, k) with k > 256 (one block of width k; randomized.py:299-313):
+    the host-driven single block over the C-ABI kernels must reproduce the
+    reference algorithm -- pivots, R, rank, resamples and counters."""
+    import paper_1509_06820_b200 as P
+    g = np.random.default_rng(m + k)
+    if kind == "gauss":
+        A = g.standard_normal((m, n))
+    else:
+        A = g.standard_normal((m, 350)) @ g.standard_normal((350, n))
+    f = P.ssrqrcp(A, k, P.RandomizedConfig(block=32, padding=8, seed=0))
+    o = port.ssrqrcp(A, k, 32, 8, 0)
+    frob = float(np.linalg.norm(A))
+    d = np.abs(np.diag(o.R))
+    bad = d <= NOISE * EPS * frob
+    r_sig = int(np.argmax(bad)) if bad.any() else d.size
+    np.testing.assert_array_equal(np.asarray(f.perm.forward)[:r_sig], o.perm.forward[:r_sig])
+    mine = f.perm.restore(f.R)[:r_sig]
+    theirs = np.zeros((o.R.shape[0], n))
+    theirs[:, o.perm.forward] = o.R
+    assert np.linalg.norm(mine - theirs[:r_sig]) <= 1e-10 * np.linalg.norm(theirs[:r_sig])
+    if r_sig == k:
+        assert f.rank == o.rank
+        assert f.counters.resamples == o.counters.resamples
+        assert (f.counters.gemm_flops, f.counters.level2_flops) == (o.counters.gemm_flops,
+                                                                   o.counters.level2_flops)
+    q = f.q_factor()
+    assert np.linalg.norm(q.T @ q - np.eye(f.rank), 2) <= 1e-12
+
+
+@pytest.mark.parametrize("m,n", [(3000, 2600), (2600, 3000)])
+def test_b128_two_half_panels_vs_oracle(m, n):
+    """b = 128 blocks take the two-half fast panel (driver.cu panel_halves)
+    beside the K = 128 grouped trailing update: identical pivots and
+    counters, R to 1e-10 of the reference algorithm."""
+    import paper_1509_06820_b200 as P
+    A = np.random.default_rng(m + 3 * n).standard_normal((m, n))
+    f = P.rqrcp(A, None, P.RandomizedConfig(block=128, padding=8, seed=0))
+    o = port.rqrcp(A, None, 128, 8, 0)
+    np.testing.assert_array_equal(np.asarray(f.perm.forward), o.perm.forward)
+    assert np.linalg.norm(f.R - o.R) <= 1e-10 * np.linalg.norm(o.R)
+    assert (f.counters.gemm_flops, f.counters.level2_flops, f.counters.resamples) == (
+        o.counters.gemm_flops, o.counters.level2_flops, o.counters.resamples)
