@@ -439,7 +439,7 @@ def main():
         ach = FL[i] / (MS[i] * 1e-3) / 1e12
         pk = peak["dmma_f64_tflops"] if peak else 37.2
         kname = {"update": "rank_update_grouped_kernel (C -= Y X, K = b; TMA, one CTA/SM of "
-                           "three 4-warp groups on 64x64 tiles)",
+                           "three 4-warp groups on 64x64 tiles, C tile prefetched by TMA)",
                  "inner": "tc_tma_kernel (G = Y^T C, TMA-fed, split-K)",
                  "sketch": "tc_tma_kernel (B = Omega A, TMA-fed)",
                  "small_gemm": "tc_tma_kernel / block_finish_kernel (small products)"}.get(dom, dom)

@@ -340,7 +340,7 @@ int rq_set_option(rq_handle_t h, const char* name, int64_t value) {
     else if (n == "ru_two_ctas") hh.ru_two_ctas = value != 0;
     else if (n == "ru_skew_ns") hh.ru_skew_ns = (int)value;
     else if (n == "ru_big") hh.ru_big = value != 0;
-    else if (n == "ru_tma") hh.ru_tma = value != 0;
+    else if (n == "ru_tma") hh.ru_tma = (int)value;
     else if (n == "inner_kernel") hh.inner_kernel = value != 0;
     else if (n == "inner_ktiles") hh.inner_ktiles = (int)value;
     else if (n == "inner32") hh.inner32 = value != 0;

@@ -73,17 +73,20 @@ struct FastArgs {
 RQ_DEV double ldcg(const double* p) { return __ldcg(p); }
 
 // rows [ch*64, ch*64+64) x cols [0, n8) of the column-major panel into a
-// row-major chunk (zero padded)
-RQ_DEV void load_chunk(const FastArgs& a, int64_t ch, double* C) {
+// row-major chunk (zero padded), in two halves so the next chunk's global
+// loads (load_regs) are in flight while the current chunk is multiplied
+RQ_DEV void load_regs(const FastArgs& a, int64_t ch, double (&v)[16]) {
   const int64_t r0 = ch * kFRows;
   const int r = threadIdx.x & (kFRows - 1), c0 = threadIdx.x / kFRows;  // 4 columns per pass
   const int64_t gr = r0 + r;
-  double v[16];
 #pragma unroll
   for (int k = 0; k < 16; ++k) {
     const int c = c0 + 4 * k;
     v[k] = (c < a.n && gr < a.mm) ? a.P[gr + (int64_t)c * a.ldp] : 0.0;
   }
+}
+RQ_DEV void store_regs(const FastArgs& a, const double (&v)[16], double* C) {
+  const int r = threadIdx.x & (kFRows - 1), c0 = threadIdx.x / kFRows;
 #pragma unroll
   for (int k = 0; k < 16; ++k) {
     const int c = c0 + 4 * k;
@@ -273,10 +276,13 @@ __global__ void __launch_bounds__(kFT, 1) panel_fast_kernel(FastArgs a) {
   // ---- phase A: partial G1 = P^T P
 #pragma unroll
   for (int q = 0; q < 5; ++q) acc[q][0] = acc[q][1] = 0.0;
+  double pre[16];   // the next chunk, loaded while the current one is multiplied
+  if (me < a.nchunks) load_regs(a, me, pre);
   for (int64_t ch = me; ch < a.nchunks; ch += Q) {
     __syncthreads();
-    load_chunk(a, ch, W0);
+    store_regs(a, pre, W0);
     __syncthreads();
+    if (ch + Q < a.nchunks) load_regs(a, ch + Q, pre);
     chunk_gram(W0, n8, ld, acc);
   }
   store_gram(a.gpart + (size_t)me * nn, n8, acc);
@@ -414,10 +420,12 @@ __global__ void __launch_bounds__(kFT, 1) panel_fast_kernel(FastArgs a) {
   for (int i = r0; i < n8; i += rstep) W2[i * ld + c0] = ldcg(a.gmat + 2 * nn + i * n8 + c0);
 #pragma unroll
   for (int q = 0; q < 5; ++q) acc[q][0] = acc[q][1] = 0.0;
+  if (!resident && me < a.nchunks) load_regs(a, me, pre);
   for (int64_t ch = me; ch < a.nchunks; ch += Q) {
     __syncthreads();
-    if (!resident) load_chunk(a, ch, W0);
+    if (!resident) store_regs(a, pre, W0);
     __syncthreads();
+    if (!resident && ch + Q < a.nchunks) load_regs(a, ch + Q, pre);
     chunk_mm<false, true>(W0, W2, W1, kFRows, n8, ld);
     __syncthreads();
     chunk_gram(W1, n8, ld, acc);
@@ -638,10 +646,12 @@ __global__ void __launch_bounds__(kFT, 1) panel_fast_kernel(FastArgs a) {
 
   // ---- phase C: Y_below = P_below M, zeros below the diagonal of the panel rows
   for (int i = r0; i < n8; i += rstep) W2[i * ld + c0] = ldcg(a.gmat + 3 * nn + i * n8 + c0);
+  if (!resident && me < a.nchunks) load_regs(a, me, pre);
   for (int64_t ch = me; ch < a.nchunks; ch += Q) {
     __syncthreads();
-    if (!resident) load_chunk(a, ch, W0);
+    if (!resident) store_regs(a, pre, W0);
     __syncthreads();
+    if (!resident && ch + Q < a.nchunks) load_regs(a, ch + Q, pre);
     chunk_mm<false, true>(W0, W2, W1, kFRows, n8, ld);
     __syncthreads();
     const int64_t g0 = ch * kFRows;

@@ -134,7 +134,8 @@ class Handle {
   bool ru_two_ctas = false;  // rank update: two single-buffered CTAs per SM
   int ru_skew_ns = 0;
   bool ru_big = true;        // rank update: 128 x 64 tiles, C through registers
-  bool ru_tma = true;        // rank update: the TMA-fed kernel (rank_update_tma.cu) where it applies
+  int ru_tma = 2;            // rank update: the TMA-fed kernel (rank_update_tma.cu) where it applies;
+                             // 0 off, 1 C from HBM in the epilogue, 2/3 C tile prefetched by TMA
   bool inner_kernel = true;  // H = P^T C: tall-skinny split-K kernel (csrc/inner.cu)
   int inner_ktiles = 16;     // ... k-tiles (32 deep) per CTA
   bool inner32 = true;       // ... also for 32-row blocks (b = 32)

@@ -20,7 +20,8 @@ def _dev(x):
 @pytest.mark.parametrize("ta", [False, True])
 @pytest.mark.parametrize("tb", [False, True])
 @pytest.mark.parametrize("shape", [(64, 96, 40), (130, 70, 3000), (7, 5, 3), (300, 257, 129),
-                                   (72, 1000, 8192)])
+                                   (72, 1000, 8192), (138, 202, 1030), (64, 100, 20000),
+                                   (2050, 66, 48)])
 def test_gemm_matches_fp64_reference(ta, tb, shape):
     from paper_1509_06820_b200.primitives import gemm
     m, n, k = shape
@@ -253,7 +254,8 @@ def test_t_factor_inverse_matches_recurrence(nb):
 
 
 @pytest.mark.parametrize("M,N,K", [(20000, 224, 32), (5000, 1000, 32), (20000, 224, 64),
-                                   (4100, 3000, 64), (8192, 256, 128), (300, 100, 32)])
+                                   (4100, 3000, 64), (8192, 256, 128), (300, 100, 32),
+                                   (4100, 3002, 128), (130, 70, 64), (66, 2, 32)])
 def test_rank_update_multi_tile(M, N, K):
     """C -= Y X through the persistent rank-b kernels when a CTA owns several
     tiles (tall trailing blocks; K = 128 as two 64-deep passes), against
@@ -263,3 +265,14 @@ def test_rank_update_multi_tile(M, N, K):
     Y, X, C0 = g.standard_normal((M, K)), g.standard_normal((K, N)), g.standard_normal((M, N))
     out = gemm(_dev(Y), _dev(X), _dev(C0), alpha=-1.0, beta=1.0).cpu().numpy()
     assert np.abs(out - (C0 - Y @ X)).max() <= 64 * K * np.finfo(float).eps * 10
+    # the grouped TMA kernel's variants (C from HBM; C tile prefetched by TMA
+    # with k 16 / k 8 stages) run the same DMMA order: bitwise identical
+    from paper_1509_06820_b200 import _abi
+    lib, h = _abi.load_library(), _abi.handle(0)
+    try:
+        for v in (1, 3):
+            lib.rq_set_option(h, b"ru_tma", v)
+            alt = gemm(_dev(Y), _dev(X), _dev(C0), alpha=-1.0, beta=1.0).cpu().numpy()
+            np.testing.assert_array_equal(alt, out)
+    finally:
+        lib.rq_set_option(h, b"ru_tma", 2)

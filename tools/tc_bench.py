@@ -96,7 +96,7 @@ def main():
         r["cublas_tf"] = round(flops / us / 1e6, 2)
         scale = float(ref.abs().max())
         for label, opts in [("auto", {"tc_variant": -1})] + \
-                [(f"v{v}", {"tc_variant": v}) for v in variants] + [("cpasync", {"tc_tma": 0}), ("rubig", {"ru_tma": 0}), ("old", {"use_tc": 0}),
+                [(f"v{v}", {"tc_variant": v}) for v in variants] + [("cpasync", {"tc_tma": 0}), ("rubig", {"ru_tma": 0}), ("ru2", {"ru_tma": 2}), ("ru3", {"ru_tma": 3}), ("old", {"use_tc": 0}),
                                                                      ("noru", {"use_rank_update": 0})]:
             for k_, v_ in opts.items():
                 _abi.check(lib.rq_set_option(h, k_.encode(), v_))
@@ -111,7 +111,7 @@ def main():
             _abi.check(lib.rq_set_option(h, b"use_tc", 1))
             _abi.check(lib.rq_set_option(h, b"use_rank_update", 1))
             _abi.check(lib.rq_set_option(h, b"tc_tma", 1))
-            _abi.check(lib.rq_set_option(h, b"ru_tma", 1))
+            _abi.check(lib.rq_set_option(h, b"ru_tma", 2))
             _abi.check(lib.rq_set_option(h, b"tc_variant", -1))
         print(json.dumps(r), flush=True)
 
