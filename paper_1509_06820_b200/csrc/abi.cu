@@ -316,6 +316,7 @@ int rq_set_option(rq_handle_t h, const char* name, int64_t value) {
     else if (n == "use_rank_update") hh.use_rank_update = value != 0;
     else if (n == "fast_panel") hh.fast_panel = value != 0;
     else if (n == "fast_panel_max_ctas") hh.fast_panel_max_ctas = (int)value;
+    else if (n == "fast_panel_pad") hh.fast_panel_pad = (int)std::max<int64_t>(1, std::min<int64_t>(value, 8));
     else if (n == "fast_panel_spec") hh.fast_panel_spec = (int)value;
     else if (n == "profile_trace") hh.tracing = value != 0;
     else if (n == "select_max_ctas") hh.select_max_ctas = (int)value;

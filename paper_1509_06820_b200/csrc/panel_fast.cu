@@ -685,7 +685,7 @@ const int* panel_fast(Handle& h, int64_t mm, int64_t bw, const double* P, int64_
                       int usable_total, bool degen_commit) {
   if (!panel_fast_eligible(h, mm, bw)) return nullptr;
   const int n8 = (int)((bw + 7) / 8 * 8);
-  const int ld = n8 + 1;
+  const int ld = n8 + h.fast_panel_pad;
   const int64_t nchunks = (mm + kFRows - 1) / kFRows;
   int Q = (int)std::min<int64_t>(h.num_sms, nchunks);
   if (h.fast_panel_max_ctas > 0) Q = std::min(Q, h.fast_panel_max_ctas);

@@ -120,6 +120,8 @@ class Handle {
   bool use_rank_update = true;
   bool fast_panel = true;   // CholeskyQR2 + Householder reconstruction panel (panel_fast.cu)
   int fast_panel_max_ctas = 0;  // 0 = one CTA per SM
+  int fast_panel_pad = 4;       // smem row stride of the fast panel: n8 + pad doubles (4: the
+                                // DMMA fragment loads of a 16-lane phase hit 16 distinct banks)
   // speculative driver on a declined fast panel: 0 = always rewind, 1 = rewind
   // once then queue the exact kernel behind every fast panel, 2 = never rewind
   int fast_panel_spec = 1;

@@ -200,6 +200,17 @@ def test_fast_panel_matches_oracle(mm, bw):
     assert np.all((tau >= 1.0) & (tau <= 2.0))
     np.testing.assert_allclose(T, port.t_factor(Yo, to), rtol=1e-10, atol=1e-13)
     assert (usable, l2) == (usable_e, l2e) == (bw, l2)
+    # the shared-memory row stride is a layout choice only: bitwise the same
+    from paper_1509_06820_b200 import _abi
+    lib, h = _abi.load_library(), _abi.handle(0)
+    try:
+        for pad in (1, 8):
+            lib.rq_set_option(h, b"fast_panel_pad", pad)
+            got = _panel_with(P0, True)
+            for x, y in zip(got[:4], (R, Y, tau, T)):
+                np.testing.assert_array_equal(x, y)
+    finally:
+        lib.rq_set_option(h, b"fast_panel_pad", 4)
 
 
 @pytest.mark.parametrize("kind", ["dup", "tiny_col", "zero_col", "near_tol"])
