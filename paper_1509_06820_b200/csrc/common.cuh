@@ -89,6 +89,34 @@ RQ_DEV void grid_barrier_patient(unsigned int* counter, unsigned int& epoch) {
   __syncthreads();
 }
 
+// The patient barrier in two halves: a CTA that has published what the others
+// wait for arrives, keeps working on results nobody reads inside the kernel,
+// and waits afterwards.
+RQ_DEV void grid_barrier_arrive(unsigned int* counter, unsigned int& epoch) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    epoch += 1;
+    __threadfence();
+    atomicAdd(counter, 1u);
+  }
+}
+RQ_DEV void grid_barrier_wait(unsigned int* counter, const unsigned int& epoch) {
+  if (threadIdx.x == 0) {
+    const unsigned int target = epoch * gridDim.x;
+    unsigned int seen, ns = 32;
+    int polls = 0;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(counter) : "memory");
+      if (seen >= target) break;
+      if (++polls > 16) {
+        __nanosleep(ns);
+        ns = ns < 512 ? 2 * ns : 512;
+      }
+    }
+  }
+  __syncthreads();
+}
+
 // numpy's pairwise summation (pairwise_sum_DOUBLE: 8 accumulators for
 // n <= 128, recursive halving on multiples of 8 above) of x[i]*x[i] over a
 // strided vector; bit-identical to np.linalg.norm(B, axis=0)**2 on an

@@ -66,7 +66,8 @@ struct FastArgs {
   Status* st;
   unsigned int* bar;                // [0] barrier, [1] exit count, [2] fail, [4] skip flag
   double* gpart;                    // [Q][n8*n8]
-  double* gmat;                     // [4][n8*n8]: G1, R1, R1^{-1}, G2 then M
+  double* gmat;                     // [5][n8*n8]: G1, R1, R1^{-1}, G2, M
+  double* gx;                       // [2][n8*n8] + [n8]: L, U, signs (CTA 0 -> the stage-2 helpers)
   long long* dbg;
 };
 
@@ -437,7 +438,15 @@ __global__ void __launch_bounds__(kFT, 1) panel_fast_kernel(FastArgs a) {
   grid_barrier_patient(&a.bar[0], epoch);
   mark(4);
 
-  // ---- CTA 0: F, R~, LU with signs, outputs for the top rows, M
+  // ---- CTA 0: F, R~, LU with signs (stage 1 of the second serial section)
+  // Stage 2 (after one more grid barrier) is spread over three CTAs: CTA 0
+  // keeps the critical product M = R1^{-1} (I - F) S U^{-1} (phase C needs it),
+  // CTA 1 forms the sample update's M, CTA 2 the T factor and block_finish's
+  // A1, A2 -- all from L, U and the signs CTA 0 publishes in gx.
+  double* gxL = a.gx;                  // L = Y1 (strictly lower part), row-major n8 x n8
+  double* gxU = a.gx + nn;             // U, row-major
+  double* gxs = a.gx + 2 * nn;         // signs s_j
+  double* Mdst = a.gmat + 4 * nn;      // M (gmat[3] keeps G2: the helpers re-form F from it)
   if (me == 0) {
     // CTA 0 factored chunk 0 in phase B: with one chunk per CTA its W1 still
     // holds Q1 rows [0, 64), i.e. Q1_top
@@ -539,83 +548,14 @@ __global__ void __launch_bounds__(kFT, 1) panel_fast_kernel(FastArgs a) {
         else s_fail = 1;
       }
     }
+    for (int j = n + tid; j < n8; j += kFT) s_dinv[j] = 1.0;
     __syncthreads();
-    sub(6);
     if (!s_fail) {
-      // top rows: R = S R~ in the panel rows (zeros below the diagonal), Y_top = L
-      for (int e = tid; e < n * n; e += kFT) {
-        const int l = e / n, i = e - l * n;
-        if (i < a.rrows) a.Rdst[i + (int64_t)l * a.ldr] = i <= l ? s_sign[i] * Rt[i * ld + l] : 0.0;
-        a.Y[i + (int64_t)l * a.ldy] = i < l ? 0.0 : (i == l ? 1.0 : T5[i * ld + l]);
+      for (int i = r0; i < n8; i += rstep) {
+        gxL[i * n8 + c0] = (i > c0 && i < n) ? T5[i * ld + c0] : 0.0;
+        gxU[i * n8 + c0] = Q1[i * ld + c0];
       }
-      for (int j = tid; j < n; j += kFT) a.tau[j] = fabs(s_c[j]) + 1.0;
-      for (int j = n + tid; j < n8; j += kFT) s_dinv[j] = 1.0;
-      __syncthreads();   // Rt / T5 are read above; W0 <- Y1^T (unit upper) for the T factor
-      for (int i = r0; i < n8; i += rstep)
-        W0[i * ld + c0] = i == c0 ? 1.0 : (i < c0 && c0 < n ? T5[c0 * ld + i] : 0.0);
-      __syncthreads();   // T5 (L) is the scratch below
-      upper_inverse<kFT>(Q1, s_dinv, R1, T5, n8, ld);   // U^{-1}
-      __syncthreads();
-      sub(7);
-      for (int i = r0; i < n; i += rstep) R1[i * ld + c0] *= s_sign[i];   // V = S U^{-1}
-      __syncthreads();
-      chunk_mm<true, true>(F, R1, T5, n8, n8, ld);   // F V
-      __syncthreads();
-      for (int i = r0; i < n8; i += rstep) R1[i * ld + c0] -= T5[i * ld + c0];   // M' = (I - F) V
-      __syncthreads();
-      chunk_mm<true, true>(Ri, R1, T5, n8, n8, ld);  // M = R1^{-1} M'
-      __syncthreads();
-      for (int i = r0; i < n8; i += rstep) a.gmat[3 * nn + i * n8 + c0] = T5[i * ld + c0];
-      if (a.msu != nullptr) {
-        // sample update's M = S11 R11^{-1} (randomized.py:107-135): R11 = S R~,
-        // R~^{-1} = R1^{-1} (I - F) to O(|F|^2), so M = S11 R1^{-1} (I - F) S.
-        // A committed panel cleared the degenerate guard (same threshold).
-        __syncthreads();
-        for (int i = r0; i < n8; i += rstep)
-          W4[i * ld + c0] = (i < n && c0 < n) ? a.S11[i + (int64_t)c0 * a.lds11] : 0.0;
-        __syncthreads();
-        chunk_mm<false, true>(W4, Ri, W5, n8, n8, ld);   // S11 R1^{-1}
-        __syncthreads();
-        chunk_mm<false, true>(W5, F, W4, n8, n8, ld);    // (S11 R1^{-1}) F
-        __syncthreads();
-        for (int e = tid; e < n * n; e += kFT) {
-          const int l = e / n, i = e - l * n;
-          a.msu[i + (int64_t)l * n] = s_sign[l] * (W5[i * ld + l] - W4[i * ld + l]);
-        }
-        if (tid == 0) a.st->degenerate = s_degen;
-        __syncthreads();
-      }
-      if (a.T != nullptr) {
-        // compact-WY T of the reconstructed reflectors: U = -T Y1^T, so
-        // T = -U Y1^{-T} (kernels.py:139-147 builds the same T by recurrence)
-        for (int j = tid; j < n8; j += kFT) s_dinv[j] = 1.0;
-        __syncthreads();
-        upper_inverse<kFT>(W0, s_dinv, W2, W3, n8, ld);   // Y1^{-T}
-        chunk_mm<true, true>(Q1, W2, W4, n8, n8, ld);
-        __syncthreads();
-        for (int e = tid; e < n * n; e += kFT) {
-          const int l = e / n, i = e - l * n;
-          a.T[i + (int64_t)l * a.ldt] = i <= l ? -W4[i * ld + l] : 0.0;
-        }
-        if (a.a12 != nullptr) {
-          // X = T^T G with G = Y1^T C_top + M^T H  =>  X = A1^T C_top + A2^T H,
-          // A1 = Y1 T, A2 = M T (block_finish_kernel applies them per column tile)
-          __syncthreads();
-          for (int i = r0; i < n8; i += rstep) {
-            W3[i * ld + c0] = W0[c0 * ld + i];                    // Y1 (unit lower) = (Y1^T)^T
-            W5[i * ld + c0] = a.gmat[3 * nn + i * n8 + c0];       // M (this CTA wrote it)
-          }
-          __syncthreads();
-          chunk_mm<false, true>(W3, W4, W2, n8, n8, ld);   // Y1 (-T)
-          chunk_mm<false, true>(W5, W4, W1, n8, n8, ld);   // M (-T)
-          __syncthreads();
-          for (int e = tid; e < n * n; e += kFT) {   // row-major: block_finish's staging layout
-            const int i = e / n, l = e - i * n;
-            a.a12[e] = -W2[i * ld + l];
-            a.a12[(int64_t)n * n + e] = -W1[i * ld + l];
-          }
-        }
-      }
+      for (int j = tid; j < n8; j += kFT) gxs[j] = j < n ? s_sign[j] : 1.0;
     }
     if (tid == 0) {
       a.bar[2] = s_fail;
@@ -625,17 +565,8 @@ __global__ void __launch_bounds__(kFT, 1) panel_fast_kernel(FastArgs a) {
         __threadfence();
         a.st->abort = kAbortPanelFast;
       }
-      if (!s_fail) {
-        // _panel_rank: every column usable; level-2 counters of the
-        // column-by-column reflections this path replaces
-        int64_t l2 = a.l2_extra;
-        for (int j = 0; j + 1 < n; ++j) l2 += (a.mm - j) * (int64_t)(n - j - 1);
-        a.st->usable = a.usable_total > 0 ? a.usable_total : n;
-        a.st->level2 += 4 * l2;
-        a.st->l2bytes += 16 * l2;
-      }
     }
-    sub(8);
+    sub(6);
   }
   mark(5);
   grid_barrier_patient(&a.bar[0], epoch);
@@ -644,8 +575,141 @@ __global__ void __launch_bounds__(kFT, 1) panel_fast_kernel(FastArgs a) {
     return;
   }
 
+  // ---- stage 2: CTA 0 -> M and the top rows; CTA 1 -> sample update's M; CTA 2 -> T, A1, A2
+  bool arrived = false;
+  if (me == 0) {
+    double* Rt = W0;
+    double* Q1 = W1;   // U
+    double* Ri = W2;
+    double* F = W3;
+    double* R1 = W4;   // U^{-1}, V, M'
+    double* T5 = W5;   // L, then scratch
+    // Y_top = L before T5 becomes scratch
+    for (int e = tid; e < n * n; e += kFT) {
+      const int l = e / n, i = e - l * n;
+      a.Y[i + (int64_t)l * a.ldy] = i < l ? 0.0 : (i == l ? 1.0 : T5[i * ld + l]);
+    }
+    __syncthreads();
+    upper_inverse<kFT>(Q1, s_dinv, R1, T5, n8, ld);   // U^{-1}
+    __syncthreads();
+    sub(7);
+    for (int i = r0; i < n; i += rstep) R1[i * ld + c0] *= s_sign[i];   // V = S U^{-1}
+    __syncthreads();
+    chunk_mm<true, true>(F, R1, T5, n8, n8, ld);   // F V
+    __syncthreads();
+    for (int i = r0; i < n8; i += rstep) R1[i * ld + c0] -= T5[i * ld + c0];   // M' = (I - F) V
+    __syncthreads();
+    chunk_mm<true, true>(Ri, R1, T5, n8, n8, ld);  // M = R1^{-1} M'
+    __syncthreads();
+    for (int i = r0; i < n8; i += rstep) Mdst[i * n8 + c0] = T5[i * ld + c0];
+    // M is what the other CTAs wait for: arrive now, finish the top rows, then wait
+    grid_barrier_arrive(&a.bar[0], epoch);
+    arrived = true;
+    // top rows: R = S R~ in the panel rows (zeros below the diagonal)
+    for (int e = tid; e < n * n; e += kFT) {
+      const int l = e / n, i = e - l * n;
+      if (i < a.rrows) a.Rdst[i + (int64_t)l * a.ldr] = i <= l ? s_sign[i] * Rt[i * ld + l] : 0.0;
+    }
+    for (int j = tid; j < n; j += kFT) a.tau[j] = fabs(s_c[j]) + 1.0;
+    if (tid == 0) {
+      if (a.msu != nullptr) a.st->degenerate = s_degen;
+      // _panel_rank: every column usable; level-2 counters of the
+      // column-by-column reflections this path replaces
+      int64_t l2 = a.l2_extra;
+      for (int j = 0; j + 1 < n; ++j) l2 += (a.mm - j) * (int64_t)(n - j - 1);
+      a.st->usable = a.usable_total > 0 ? a.usable_total : n;
+      a.st->level2 += 4 * l2;
+      a.st->l2bytes += 16 * l2;
+    }
+    sub(8);
+  } else if (me == 1 && a.msu != nullptr) {
+    // sample update's M = S11 R11^{-1} (randomized.py:107-135): R11 = S R~,
+    // R~^{-1} = R1^{-1} (I - F) to O(|F|^2), so M = S11 R1^{-1} (I - F) S.
+    // A committed panel cleared the degenerate guard (same threshold).
+    // (W0 may hold this CTA's resident panel rows; W2 = R1^{-1} since phase B)
+    for (int i = r0; i < n8; i += rstep) {
+      const int l = c0, e = i * n8 + l;
+      double f = 0.0;
+      if (i <= l && l < n) {
+        const double E = ldcg(a.gmat + 3 * nn + e) - (i == l ? 1.0 : 0.0);
+        f = (i == l) ? 0.5 * E : E;
+      }
+      W3[i * ld + l] = f;
+      W4[i * ld + l] = (i < n && l < n) ? a.S11[i + (int64_t)l * a.lds11] : 0.0;
+    }
+    for (int j = tid; j < n8; j += kFT) s_sign[j] = ldcg(gxs + j);
+    __syncthreads();
+    chunk_mm<false, true>(W4, W2, W5, n8, n8, ld);   // S11 R1^{-1}
+    __syncthreads();
+    chunk_mm<false, true>(W5, W3, W4, n8, n8, ld);   // (S11 R1^{-1}) F
+    __syncthreads();
+    for (int e = tid; e < n * n; e += kFT) {
+      const int l = e / n, i = e - l * n;
+      a.msu[i + (int64_t)l * n] = s_sign[l] * (W5[i * ld + l] - W4[i * ld + l]);
+    }
+  } else if (me == 2 && a.T != nullptr) {
+    // compact-WY T of the reconstructed reflectors: U = -T Y1^T, so
+    // T = -U Y1^{-T} (kernels.py:139-147 builds the same T by recurrence)
+    for (int i = r0; i < n8; i += rstep) {
+      W1[i * ld + c0] = ldcg(gxU + i * n8 + c0);
+      W3[i * ld + c0] = i == c0 ? 1.0 : (i < c0 ? ldcg(gxL + c0 * n8 + i) : 0.0);   // Y1^T
+    }
+    for (int j = tid; j < n8; j += kFT) {
+      s_dinv[j] = 1.0;
+      s_sign[j] = ldcg(gxs + j);
+    }
+    __syncthreads();
+    upper_inverse<kFT>(W3, s_dinv, W4, W5, n8, ld);   // X = Y1^{-T}
+    __syncthreads();
+    chunk_mm<true, true>(W1, W4, W5, n8, n8, ld);     // U X = -T
+    __syncthreads();
+    for (int e = tid; e < n * n; e += kFT) {
+      const int l = e / n, i = e - l * n;
+      a.T[i + (int64_t)l * a.ldt] = i <= l ? -W5[i * ld + l] : 0.0;
+    }
+    if (a.a12 != nullptr) {
+      // X = T^T G with G = Y1^T C_top + M^T H  =>  X = A1^T C_top + A2^T H,
+      // A1 = Y1 T, A2 = M T = -R1^{-1} (I - F) S Y1^{-T} (U^{-1} U cancels, so
+      // A2 does not wait for CTA 0's M); block_finish_kernel applies them
+      for (int i = r0; i < n8; i += rstep)   // Y1 (unit lower)
+        W3[i * ld + c0] = i == c0 ? 1.0 : (i > c0 ? ldcg(gxL + i * n8 + c0) : 0.0);
+      __syncthreads();
+      chunk_mm<false, true>(W3, W5, W1, n8, n8, ld);   // Y1 (-T)
+      __syncthreads();
+      for (int e = tid; e < n * n; e += kFT) {   // row-major: block_finish's staging layout
+        const int i = e / n, l = e - i * n;
+        a.a12[e] = -W1[i * ld + l];
+      }
+      __syncthreads();
+      for (int i = r0; i < n8; i += rstep) {
+        const int l = c0, e = i * n8 + l;
+        double f = 0.0;
+        if (i <= l && l < n) {
+          const double E = ldcg(a.gmat + 3 * nn + e) - (i == l ? 1.0 : 0.0);
+          f = (i == l) ? 0.5 * E : E;
+        }
+        W1[i * ld + l] = f;                              // F
+        W3[i * ld + l] = s_sign[i] * W4[i * ld + l];     // N = S Y1^{-T}
+      }
+      __syncthreads();
+      chunk_mm<true, true>(W1, W3, W5, n8, n8, ld);      // F N
+      __syncthreads();
+      for (int i = r0; i < n8; i += rstep) W3[i * ld + c0] -= W5[i * ld + c0];   // (I - F) N
+      __syncthreads();
+      chunk_mm<true, true>(W2, W3, W1, n8, n8, ld);      // R1^{-1} (I - F) N = -A2
+      __syncthreads();
+      for (int e = tid; e < n * n; e += kFT) {
+        const int i = e / n, l = e - i * n;
+        a.a12[(int64_t)n * n + e] = -W1[i * ld + l];
+      }
+    }
+  }
+  mark(6);
+  if (!arrived) grid_barrier_arrive(&a.bar[0], epoch);
+  grid_barrier_wait(&a.bar[0], epoch);
+
   // ---- phase C: Y_below = P_below M, zeros below the diagonal of the panel rows
-  for (int i = r0; i < n8; i += rstep) W2[i * ld + c0] = ldcg(a.gmat + 3 * nn + i * n8 + c0);
+  for (int i = r0; i < n8; i += rstep) W2[i * ld + c0] = ldcg(Mdst + i * n8 + c0);
   if (!resident && me < a.nchunks) load_regs(a, me, pre);
   for (int64_t ch = me; ch < a.nchunks; ch += Q) {
     __syncthreads();
@@ -663,7 +727,7 @@ __global__ void __launch_bounds__(kFT, 1) panel_fast_kernel(FastArgs a) {
       if (gr < a.rrows && !a.defer_zero) a.Rdst[gr + (int64_t)c * a.ldr] = 0.0;
     }
   }
-  mark(6);
+  mark(7);
   finish();
 }
 
@@ -690,6 +754,7 @@ const int* panel_fast(Handle& h, int64_t mm, int64_t bw, const double* P, int64_
   int Q = (int)std::min<int64_t>(h.num_sms, nchunks);
   if (h.fast_panel_max_ctas > 0) Q = std::min(Q, h.fast_panel_max_ctas);
   if (max_ctas > 0) Q = std::min(Q, max_ctas);
+  Q = std::max(Q, 3);   // CTAs 1 and 2 carry the second serial section's side products
   const size_t smem = (size_t)6 * kFRows * ld * 8;
   const int nn = n8 * n8;
   FastArgs a{};
@@ -717,10 +782,11 @@ const int* panel_fast(Handle& h, int64_t mm, int64_t bw, const double* P, int64_
     zeroed = a.bar;
   }
   a.gpart = (double*)h.buf("pf_part", (size_t)Q * nn * 8, s);
-  a.gmat = (double*)h.buf("pf_mat", (size_t)4 * nn * 8, s);
+  a.gmat = (double*)h.buf("pf_mat", (size_t)5 * nn * 8, s);
+  a.gx = (double*)h.buf("pf_x", ((size_t)2 * nn + n8) * 8, s);
   // on commit, M = R1^{-1} (I - F) S U^{-1} (Y_below = P_below M) is left
-  // row-major in gmat[3]: as a column-major matrix with ld n8 it is M^T
-  if (m_rowmajor != nullptr) *m_rowmajor = a.gmat + 3 * nn;
+  // row-major in gmat[4]: as a column-major matrix with ld n8 it is M^T
+  if (m_rowmajor != nullptr) *m_rowmajor = a.gmat + 4 * nn;
   if (m_ld != nullptr) *m_ld = n8;
   a.dbg = h.dbg;
   kernel_attr((const void*)panel_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
