@@ -321,6 +321,7 @@ int rq_set_option(rq_handle_t h, const char* name, int64_t value) {
     else if (n == "profile_trace") hh.tracing = value != 0;
     else if (n == "select_max_ctas") hh.select_max_ctas = (int)value;
     else if (n == "select_reg") hh.select_reg = value != 0;
+    else if (n == "select_fused") hh.select_fused = value != 0;
     else if (n == "omega_ahead") hh.omega_ahead = value != 0;
     else if (n == "floor_lookahead") hh.floor_lookahead = (int)value;
     else if (n == "t_inverse") hh.t_inverse = value != 0;
@@ -333,6 +334,7 @@ int rq_set_option(rq_handle_t h, const char* name, int64_t value) {
     else if (n == "tc_tma") hh.tc_tma = value != 0;
     else if (n == "overlap_select") hh.overlap_select = value != 0;
     else if (n == "overlap_sel_ctas") hh.overlap_sel_ctas = (int)value;
+    else if (n == "sel_cpg2_cols") hh.sel_cpg2_cols = value;
     else if (n == "sel_balance") hh.sel_balance = (int)value;
     else if (n == "su_gemm") hh.su_gemm = value != 0;
     else if (n == "overlap_inner") hh.overlap_inner = value != 0;

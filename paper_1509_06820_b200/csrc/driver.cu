@@ -504,7 +504,10 @@ int Factor::overlap_split(int64_t i0, int64_t bw) const {
     // v5 (register-resident) needs <= 3 columns per 8-lane group (<= 1 for
     // ell > 72); take the SMs for it only while that stays within 80, else
     // the shared-memory v4 runs on the default share
-    const int64_t per = ell_ <= 72 ? 3 * 64 : 64;   // v5 columns per CTA
+    // v5 columns per CTA: 3 per group while the update is the longer of the
+    // two, 2 (shorter apply phase, more SMs) once the select is
+    int64_t per = ell_ <= 72 ? 3 * 64 : 64;
+    if (ell_ <= 72 && nt1 <= h_.sel_cpg2_cols) per = 2 * 64;
     const int cap = (sms * 80) / 148;
     const int64_t need = (nt1 + per - 1) / per;
     if (need <= cap) {

@@ -106,6 +106,7 @@ class Handle {
   int64_t panel_rows_per_cta = 128;         // cluster variant: rows per CTA (power-of-2 CTA count)
   int select_max_ctas = 0;                  // cap of the grid variant (0 = one CTA per SM)
   bool select_reg = true;                   // register-resident select (v5) where it fits
+  bool select_fused = true;                 // v5 grid variant: barrier counter and key in one 16-byte word
   bool omega_ahead = true;                  // pre-draw resample Omega on a host thread
   int floor_lookahead = 1;                  // speculative blocks queued once near the noise floor
   bool t_inverse = true;                    // T factor as a DMMA triangular inverse (nb <= 64)
@@ -141,6 +142,7 @@ class Handle {
   bool inner_kernel = true;  // H = P^T C: tall-skinny split-K kernel (csrc/inner.cu)
   int inner_ktiles = 16;     // ... k-tiles (32 deep) per CTA
   bool inner32 = true;       // ... also for 32-row blocks (b = 32)
+  int64_t sel_cpg2_cols = 6400; // overlapped v5 select: 2 columns per group at or below this sample width
   int overlap_sel_ctas = 0;   // SMs for the overlapped select (0 = size heuristic)
   int sel_balance = 230;      // v4 select/update balance constant (x 1e-6, overlap_split; cfg5 sweeps: profiles/r02_cfg5_sel_balance.jsonl)
   bool gemm_vec16 = true;

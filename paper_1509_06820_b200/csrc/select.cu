@@ -48,6 +48,9 @@ struct SelArgs {
   // grid exchange (global/L2)
   unsigned int* bar;
   unsigned long long* gkey;  // [3] rotating candidate keys
+  // fused exchange (v5 grid variant): {arrival count, max key} pairs read with
+  // one 16-byte acquire load, so the barrier's last poll also delivers the key
+  ulonglong2* pair;          // [3], rotating with the step like gkey (nullptr: off)
   double* gcol;     // [2][P][ell+1]
   double* gsq;      // [P]
   long long* dbg;   // optional phase timers (CTA 0, thread 0): [8] cycles
@@ -625,6 +628,27 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_reg_kernel(SelArgs a) {
     if constexpr (kCluster) cg::this_cluster().sync();
     else grid_barrier(a.bar, epoch);
   };
+  __shared__ unsigned long long s_wk;
+  const bool fused = !kCluster && a.pair != nullptr;
+  // grid barrier whose arrival counter shares a 16-byte word with the step's
+  // key slot: the acquire load that sees the last arrival has the final key
+  // (every CTA's atomicMax precedes its fenced arrival; a .b128 load is one
+  // scalar access in the PTX memory model, LDG.E.128.STRONG.GPU in SASS)
+  auto fsync = [&](int slot) {
+    __syncthreads();
+    if (tid == 0) {
+      ulonglong2* pr = a.pair + slot;
+      __threadfence();
+      atomicAdd((unsigned long long*)&pr->x, 1ull);
+      unsigned long long c, k;
+      do {
+        asm volatile("{ .reg .b128 q; ld.acquire.gpu.global.b128 q, [%2]; mov.b128 {%0, %1}, q; }"
+                     : "=l"(c), "=l"(k) : "l"(pr) : "memory");
+      } while (c < (unsigned long long)P);
+      s_wk = k;
+    }
+    __syncthreads();
+  };
   auto slot_max = [&](int slot) -> unsigned long long {
     unsigned long long k = 0ull;
     if constexpr (kCluster) {
@@ -635,7 +659,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_reg_kernel(SelArgs a) {
         k = o > k ? o : k;
       }
     } else {
-      k = __ldcg(a.gkey + slot);
+      k = fused ? s_wk : __ldcg(a.gkey + slot);
     }
     return k;
   };
@@ -689,7 +713,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_reg_kernel(SelArgs a) {
     og[t] = __dmul_rn(nv[t], nv[t]);
     pc[t] = valid ? c0 + c : -1;
   }
-  xsync();  // key slots are zero everywhere before anyone publishes
+  if (!fused) xsync();  // key slots are zero everywhere before anyone publishes (fused: host memset)
 
   // publish the block's best candidate for step jn (key slot jn % 3, column
   // parity jn & 1); the caller has passed a block barrier since the keys
@@ -698,7 +722,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_reg_kernel(SelArgs a) {
     if constexpr (kCluster) {
       if (tid < P) cg::this_cluster().map_shared_rank(&s_key[jn % 3][0], tid)[me] = bk;
     } else {
-      if (tid == 0) atomicMax(a.gkey + (jn % 3), bk);
+      if (tid == 0) atomicMax(fused ? (unsigned long long*)&a.pair[jn % 3].y : a.gkey + (jn % 3), bk);
     }
     const int bpos = key_pos(bk);
 #pragma unroll
@@ -746,7 +770,8 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_reg_kernel(SelArgs a) {
     __syncthreads();
     publish(0, block_key(0));
   }
-  xsync();
+  if (fused) fsync(0);
+  else xsync();
   double tol;
   {
     for (int q = tid; q < P; q += kSelThreads) {
@@ -948,12 +973,14 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_reg_kernel(SelArgs a) {
       if constexpr (kCluster) {
         for (int q = 0; q < P; ++q) s_key[(j + 2) % 3][q] = 0ull;
       } else if (me == 0) {
-        a.gkey[(j + 2) % 3] = 0ull;
+        if (fused) a.pair[(j + 2) % 3] = make_ulonglong2(0ull, 0ull);
+        else a.gkey[(j + 2) % 3] = 0ull;
       }
     }
     publish(j + 1, bk);
     mark(2);
-    xsync();
+    if (fused) fsync((j + 1) % 3);
+    else xsync();
     mark(3);
   }
   if (timing) {
@@ -1037,11 +1064,12 @@ bool launch_select_reg(Handle& h, bool grid, int P, int cpb, int64_t ell, int64_
   ProfScope prof(h, kProfSelect, 4.0 * ell * nt * want, 16.0 * ell * nt, s);
   count_launch();
   if (grid) {
-    a.bar = (unsigned int*)h.buf("sel_bar", 64, s);
+    a.bar = (unsigned int*)h.buf("sel_bar", 128, s);
     a.gkey = (unsigned long long*)h.buf("sel_gkey", 64, s);
     a.gcol = (double*)h.buf("sel_gcol", (size_t)2 * P * (ell + 1) * 8, s);
     a.gsq = (double*)h.buf("sel_gsq", (size_t)P * 8, s);
-    RQ_CUDA(cudaMemsetAsync(a.bar, 0, 64, s));
+    a.pair = h.select_fused ? (ulonglong2*)((char*)a.bar + 64) : nullptr;
+    RQ_CUDA(cudaMemsetAsync(a.bar, 0, 128, s));
   }
 #define RQ_SEL_REG(R, C)                                                   \
   if (rpl == R && cpg == C) {                                             \
@@ -1106,7 +1134,7 @@ void select_pivots(Handle& h, int64_t ell, int64_t nt, int64_t want, const doubl
   ProfScope prof(h, kProfSelect, 4.0 * ell * nt * want, 16.0 * ell * nt, s);
   count_launch();
   if (grid) {
-    a.bar = (unsigned int*)h.buf("sel_bar", 64, s);
+    a.bar = (unsigned int*)h.buf("sel_bar", 128, s);
     a.gkey = (unsigned long long*)h.buf("sel_gkey", 64, s);
     a.gcol = (double*)h.buf("sel_gcol", (size_t)2 * P * (ell + 1) * 8, s);
     a.gsq = (double*)h.buf("sel_gsq", (size_t)P * 8, s);

@@ -9,8 +9,8 @@ from paper_1509_06820_b200.device import to_device_fortran
 dev = torch.device("cuda", 0)
 lib = _abi.load_library(); h = _abi.handle(0)
 g = np.random.default_rng(0)
-for ll in [int(x) for x in os.environ.get("LL", "1").split(",")]:
-  lib.rq_set_option(h, b"select_ll", ll)
+for ll in [int(x) for x in os.environ.get("FUSED", "1").split(",")]:
+  lib.rq_set_option(h, b"select_fused", ll)
   for nt, force, ctas in ((8128, 1, 44), (6000, 1, 44), (4096, 1, 80), (2048, 1, 80), (2048, 2, 0), (1024, 2, 0), (512, 2, 0), (256, 2, 0), (1024, 1, 80), (512, 1, 80)):
       B = to_device_fortran(g.standard_normal((72, nt)), dev)
       lib.rq_set_option(h, b"force_select", force)
@@ -22,7 +22,7 @@ for ll in [int(x) for x in os.environ.get("LL", "1").split(",")]:
       buf = (C.c_int64 * 64)()
       lib.rq_debug_read(h, buf, 64)
       steps = max(buf[7], 1)
-      print(json.dumps({"ll": ll, "nt": nt, "force": force, "ctas": ctas, "winner_split": [round(buf[32 + k] / steps) for k in range(4)],
+      print(json.dumps({"fused": ll, "nt": nt, "force": force, "ctas": ctas, "winner_split": [round(buf[32 + k] / steps) for k in range(4)],
                         "per_step": [round(buf[k] / steps) for k in range(4)],
                         "total_per_step": round(sum(buf[k] for k in range(4)) / steps)}), flush=True)
       lib.rq_set_option(h, b"debug_timers", 0)
