@@ -334,6 +334,8 @@ int rq_set_option(rq_handle_t h, const char* name, int64_t value) {
     else if (n == "tc_tma") hh.tc_tma = value != 0;
     else if (n == "overlap_select") hh.overlap_select = value != 0;
     else if (n == "overlap_sel_ctas") hh.overlap_sel_ctas = (int)value;
+    else if (n == "select_on_main") hh.select_on_main = value != 0;
+    else if (n == "select_main_mflop") hh.select_main_mflop = (int)value;
     else if (n == "sel_cpg2_cols") hh.sel_cpg2_cols = value;
     else if (n == "sel_balance") hh.sel_balance = (int)value;
     else if (n == "su_gemm") hh.su_gemm = value != 0;

@@ -118,10 +118,11 @@ class Factor {
   bool panel_halves(int64_t i0, int64_t got);
   bool msu_ready_ = false;   // the fast panel left the sample update's M in "su_Mpre"
   bool fin_ready_ = false;   // ... and A1 = Y1 T, A2 = M T in "fin_A12": block_finish() path
-  void trailing(int64_t i0, int64_t bw, int max_ctas, const Status* pred);
+  void trailing(int64_t i0, int64_t bw, int max_ctas, const Status* pred, cudaStream_t s = nullptr);
   void stream_out(int64_t upto, bool final);
   int64_t host_done_ = 0;   // columns whose host copies are enqueued
   int overlap_split(int64_t i0, int64_t bw) const;
+  bool select_is_longer(int64_t i0, int64_t bw) const;
   int panel_split(int64_t mm, int64_t nt2, int64_t bw) const;
   void update(int64_t i0_new, int64_t bw, bool spec, Counters& c);
   bool slow_block(int64_t& i0, bool resampled, int64_t& rank, bool resume_panel = false);
@@ -473,14 +474,15 @@ bool Factor::panel_overlap_inner(int64_t i0, int64_t bw) {
 // `pred` is the Status predicate: a snapshot of the abort word taken before
 // the block's sample update, so a degenerate verdict (which keeps this block
 // committed, randomized.py:253-258) cannot skip the rows it still owes.
-void Factor::trailing(int64_t i0, int64_t bw, int max_ctas, const Status* pred) {
+void Factor::trailing(int64_t i0, int64_t bw, int max_ctas, const Status* pred, cudaStream_t s) {
   const int64_t mm = m_ - i0, nt2 = n_ - i0 - bw;
   if (nt2 <= 0 || mm <= bw) return;
+  if (s == nullptr) s = s_;
   const double* Yb = p_.Y + i0 + bw + i0 * p_.ldy;
   double* C = p_.work + i0 + bw + (i0 + bw) * p_.ldw;
-  if (!rank_update(h_, mm - bw, nt2, bw, Yb, p_.ldy, X_, bw, C, p_.ldw, s_, pred, kProfUpdate,
+  if (!rank_update(h_, mm - bw, nt2, bw, Yb, p_.ldy, X_, bw, C, p_.ldw, s, pred, kProfUpdate,
                    max_ctas))
-    gemm(h_, false, false, mm - bw, nt2, bw, -1.0, Yb, p_.ldy, X_, bw, 1.0, C, p_.ldw, s_, pred,
+    gemm(h_, false, false, mm - bw, nt2, bw, -1.0, Yb, p_.ldy, X_, bw, 1.0, C, p_.ldw, s, pred,
          kProfUpdate);
 }
 
@@ -527,6 +529,13 @@ int Factor::overlap_split(int64_t i0, int64_t bw) const {
     if (nt1 <= 72 * 64) P = std::max(P, cap);
   }
   return std::max(16, std::min(P, sms - 16));
+}
+
+// Whether the next block's select outlasts this block's trailing update
+// (cfg2 trace: they cross where the update is ~5 GFLOP, block ~24 of 128)
+bool Factor::select_is_longer(int64_t i0, int64_t bw) const {
+  const double w = 2.0 * (double)(m_ - i0 - bw) * (double)(n_ - i0 - bw) * (double)bw;
+  return w < 1e-3 * (double)h_.select_main_mflop * 1e9;
 }
 
 // SMs for the fast panel while the inner product's P_below^T C_below term
@@ -804,20 +813,36 @@ FactorResult Factor::run() {
       cudaStream_t s2 = h_.side_stream();
       RQ_CUDA(cudaEventRecord(h_.ev_fork, s_));
       RQ_CUDA(cudaStreamWaitEvent(s2, h_.ev_fork, 0));
-      select(i0 + want, std::min(b_, k_ - i0 - want), true, s2, P);
-      trailing(i0, want, h_.num_sms - P, pre_);
+      // the longer of the two stays on the main stream, so the chain
+      // select -> swaps -> panel (or update -> swaps) has no cross-stream hop
+      if (h_.select_on_main && select_is_longer(i0, want)) {
+        trailing(i0, want, h_.num_sms - P, pre_, s2);
+        select(i0 + want, std::min(b_, k_ - i0 - want), true, s_, P);
+      } else {
+        select(i0 + want, std::min(b_, k_ - i0 - want), true, s2, P);
+        trailing(i0, want, h_.num_sms - P, pre_);
+      }
       RQ_CUDA(cudaEventRecord(h_.ev_join, s2));
       RQ_CUDA(cudaStreamWaitEvent(s_, h_.ev_join, 0));
       next_selected = true;
     }
     e.slot = slot;
-    RQ_CUDA(cudaMemcpyAsync(&hring_[slot], &st_->abort, sizeof(int), cudaMemcpyDeviceToHost, s_));
-    RQ_CUDA(cudaEventRecord(ev_[slot], s_));
+    // abort-word snapshot for the host's retire check, off the compute stream
+    // (it may also see a later block's trigger: the rewind below takes the
+    // block from Status, not from the slot)
+    {
+      cudaStream_t ss = h_.stat_stream();
+      RQ_CUDA(cudaEventRecord(h_.ev_stat, s_));
+      RQ_CUDA(cudaStreamWaitEvent(ss, h_.ev_stat, 0));
+      RQ_CUDA(cudaMemcpyAsync(&hring_[slot], &st_->abort, sizeof(int), cudaMemcpyDeviceToHost, ss));
+      RQ_CUDA(cudaEventRecord(ev_[slot], ss));
+    }
     slot = (slot + 1) % (kLookahead + 1);
     pend.push_back(e);
     i0 += want;
   }
   const Status fin = read_status();
+  if (speculate) RQ_CUDA(cudaStreamSynchronize(h_.stat_stream()));
   stream_out(n_, true);
   if (p_.host_Y != nullptr || p_.host_R != nullptr)
     RQ_CUDA(cudaStreamSynchronize(h_.copy_stream()));

@@ -116,6 +116,14 @@ cudaStream_t Handle::copy_stream() {
   return copy_;
 }
 
+cudaStream_t Handle::stat_stream() {
+  if (stat_ == nullptr) {
+    RQ_CUDA(cudaStreamCreateWithFlags(&stat_, cudaStreamNonBlocking));
+    RQ_CUDA(cudaEventCreateWithFlags(&ev_stat, cudaEventDisableTiming));
+  }
+  return stat_;
+}
+
 cudaStream_t Handle::omega_stream() {
   if (omega_ == nullptr) {
     RQ_CUDA(cudaStreamCreateWithFlags(&omega_, cudaStreamNonBlocking));
@@ -128,6 +136,10 @@ Handle::~Handle() {
   if (omega_ != nullptr) {
     cudaStreamDestroy(omega_);
     cudaEventDestroy(ev_omega);
+  }
+  if (stat_ != nullptr) {
+    cudaStreamDestroy(stat_);
+    cudaEventDestroy(ev_stat);
   }
   if (copy_ != nullptr) {
     cudaStreamDestroy(copy_);

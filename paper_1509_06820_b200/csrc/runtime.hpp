@@ -91,6 +91,11 @@ class Handle {
   // and the speculative driver's retire events (created once per handle)
   cudaStream_t side_stream();
   cudaStream_t copy_stream();
+  // the speculative driver's per-block abort-word snapshots (4-byte D2H copies)
+  // go through their own stream: on the compute stream each one is ~10 us of
+  // copy-engine latency between two blocks
+  cudaStream_t stat_stream();
+  cudaEvent_t ev_stat = nullptr;
   cudaStream_t omega_stream();   // uploads of pre-drawn resample Omega
   cudaEvent_t ev_copy = nullptr;
   cudaEvent_t ev_omega = nullptr;
@@ -143,6 +148,8 @@ class Handle {
   int inner_ktiles = 16;     // ... k-tiles (32 deep) per CTA
   bool inner32 = true;       // ... also for 32-row blocks (b = 32)
   int64_t sel_cpg2_cols = 6400; // overlapped v5 select: 2 columns per group at or below this sample width
+  bool select_on_main = true;    // overlapped select on the main stream once it outlasts the update
+  int select_main_mflop = 5000;  // ... i.e. below this much trailing-update work (MFLOP)
   int overlap_sel_ctas = 0;   // SMs for the overlapped select (0 = size heuristic)
   int sel_balance = 230;      // v4 select/update balance constant (x 1e-6, overlap_split; cfg5 sweeps: profiles/r02_cfg5_sel_balance.jsonl)
   bool gemm_vec16 = true;
@@ -173,6 +180,7 @@ class Handle {
   cudaEvent_t trace_base_ = nullptr;
   cudaStream_t side_ = nullptr;
   cudaStream_t copy_ = nullptr;
+  cudaStream_t stat_ = nullptr;
   cudaStream_t omega_ = nullptr;
   std::vector<cudaEvent_t> free_ev_;
   cudaEvent_t take_event();
