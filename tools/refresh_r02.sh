@@ -20,3 +20,9 @@ timeout 900 ncu --set full --import-source on --clock-control none -k regex:rank
   -o $o/ncu_update_cfg2 python bench.py --config cfg2 --steps 1 --warmup 1 --no-cpu-baseline \
   --no-e2e > $o/ncu_full.log 2>&1
 tail -c 400 $o/bench_*.json
+# the two latency-chain kernels (block ~60 of cfg2), one --set full capture each
+for k in panel_fast_kernel select_reg_kernel; do
+  timeout 900 ncu --set full --import-source on --clock-control none -k regex:$k -s 60 -c 1 \
+    -o $o/ncu_${k}_cfg2 python bench.py --config cfg2 --steps 1 --warmup 1 --no-cpu-baseline \
+    --no-e2e > $o/ncu_full_$k.log 2>&1
+done
