@@ -217,13 +217,19 @@ int rq_omega_fill(uint64_t k0, uint64_t k1, uint64_t raw, double* out, int64_t c
  * (1 = CholeskyQR2 + Householder-reconstruction panel first, falling back to
  * the column-by-column kernel when the panel is ill-conditioned; 0 = always
  * column-by-column), "fast_panel_max_ctas", "fast_panel_spec", "use_rank_update",
- * "gemm_vec16", "select_reg", "select_max_ctas", "overlap_select",
- * "overlap_sel_ctas" (next block's select beside the trailing update),
- * "su_gemm", "overlap_inner", "overlap_panel_ctas" (inner product beside the
- * fast panel), "block_finish" (X, R12 and the sample update fused per column
- * tile), "sel_balance" (x 1e-6: SM share of a shared-memory select beside the
- * trailing update, from the trailing rows), "use_cublas" (1 = plain scratch
- * products through cuBLAS DGEMM, 0 = the in-tree DMMA GEMM), "omega_ahead",
+ * "select_reg", "select_fused" (grid select: barrier counter and key slot in
+ * one 16-byte word), "select_max_ctas", "overlap_select", "overlap_sel_ctas"
+ * (next block's select beside the trailing update), "sel_cpg2_cols" (that
+ * select takes two columns per 8-lane group from this sample width down),
+ * "select_on_main" / "select_main_mflop" (the select goes on the main stream
+ * once the trailing update is below this many MFLOP), "su_gemm",
+ * "overlap_inner", "overlap_panel_ctas" (inner product beside the fast panel),
+ * "block_finish" (X, R12 and the sample update fused per column tile),
+ * "sel_balance" (x 1e-6: SM share of a shared-memory select beside the
+ * trailing update, from the trailing rows), "use_tc" / "tc_tma" / "tc_variant"
+ * / "tc_splits" (plain products: DMMA GEMM family, TMA feed, tile family and
+ * split-K overrides), "ru_tma" / "ru_big" (trailing update variants),
+ * "inner_kernel" / "inner_ktiles", "fast_panel_pad", "omega_ahead",
  * "floor_lookahead", "t_inverse", "panel_halves", "degen_commit",
  * "finish_narrow", "inner32", "panel_rows_per_cta", "profile_trace",
  * "debug_timers"; unknown names return RQ_ERR_INVALID */
