@@ -522,7 +522,9 @@ int Factor::overlap_split(int64_t i0, int64_t bw) const {
       // ms and update 1072/1140/1216/1356/1591 ms per factorization; after
       // the register-held v rows (round 2) sel_balance 145/200/260/340 gave
       // 2217/2142/2163/2301 ms, and after the TMA trailing update 150/175/
-      // 200/230 gave 2020/1988/1968/1958 ms (profiles/r02_cfg5_sel_balance.jsonl)
+      // 200/230 gave 2020/1988/1968/1958 ms (profiles/r02_cfg5_sel_balance.jsonl);
+      // after the status-stream and panel changes 110/130/150/170/185/200/230/
+      // 260 gave 1980/1937/1902/1882/1873/1869/1908/1989 ms (r02c_cfg5_sel_balance)
       const double mm = (double)(m_ - i0 - bw);
       P = (int)(sms / (1.0 + 1e-6 * h_.sel_balance * mm * 136.0 / (double)ell_) + 0.5);
     }

@@ -151,7 +151,7 @@ class Handle {
   bool select_on_main = true;    // overlapped select on the main stream once it outlasts the update
   int select_main_mflop = 5000;  // ... i.e. below this much trailing-update work (MFLOP)
   int overlap_sel_ctas = 0;   // SMs for the overlapped select (0 = size heuristic)
-  int sel_balance = 230;      // v4 select/update balance constant (x 1e-6, overlap_split; cfg5 sweeps: profiles/r02_cfg5_sel_balance.jsonl)
+  int sel_balance = 200;      // v4 select/update balance constant (x 1e-6, overlap_split; cfg5 sweeps: profiles/r02_cfg5_sel_balance.jsonl)
   bool gemm_vec16 = true;
   long long* dbg = nullptr;  // optional device phase-timer buffer (debug)
 
