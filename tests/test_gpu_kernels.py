@@ -118,6 +118,44 @@ def test_select_pivots_spilled_columns_vs_oracle(ell, nt, want, ctas):
     assert np.linalg.norm(S.cpu().numpy() - smp.B) <= 1e-12 * np.linalg.norm(B)
 
 
+@pytest.mark.parametrize("ell,nt,want,ctas", [(72, 8128, 64, 44), (72, 3000, 64, 80), (40, 2000, 32, 0),
+                                                (136, 3000, 128, 60), (72, 500, 64, 80)])
+def test_select_fused_exchange_is_bitwise_the_barrier_variant(ell, nt, want, ctas):
+    """Grid variant of the register-resident select: the fused exchange
+    (barrier counter and key slot in one 16-byte word, one .b128 acquire poll)
+    against the separate barrier + key read -- same pivots, S bit for bit, and
+    stable over repeated launches (the {count, key} pairs are reset per
+    launch); both equal the oracle's pivots."""
+    from paper_1509_06820_b200 import _abi
+    from paper_1509_06820_b200.primitives import select_pivots
+    lib, h = _abi.load_library(), _abi.handle(0)
+    g = np.random.default_rng(ell * nt)
+    B = g.standard_normal((ell, nt)) * np.exp(g.uniform(-2, 2, nt))
+    smp = port.Sample(B=np.asfortranarray(B.copy()), ell=ell)
+    perm, got = port.pick_pivots(smp, want, port.Counters())
+    out = {}
+    try:
+        lib.rq_set_option(h, b"force_select", 1)
+        lib.rq_set_option(h, b"select_max_ctas", ctas)
+        for fused in (1, 0, 1):
+            lib.rq_set_option(h, b"select_fused", fused)
+            S, piv, got_d, *_ = select_pivots(_dev(B), want)
+            assert got_d == got
+            out.setdefault(fused, []).append((S.cpu().numpy(), list(piv)))
+    finally:
+        lib.rq_set_option(h, b"select_fused", 1)
+        lib.rq_set_option(h, b"force_select", 0)
+        lib.rq_set_option(h, b"select_max_ctas", 0)
+    S0, piv0 = out[0][0]
+    for S1, piv1 in out[1]:
+        assert piv1 == piv0
+        np.testing.assert_array_equal(S1, S0)
+    fwd = list(range(nt))
+    for j, p in enumerate(piv0):
+        fwd[j], fwd[p] = fwd[p], fwd[j]
+    np.testing.assert_array_equal(fwd, perm.forward)
+
+
 def test_panel_matches_reference_fixtures():
     from paper_1509_06820_b200.primitives import panel_qr
     rec = G.load("kat_panel")
@@ -135,7 +173,10 @@ def test_panel_matches_reference_fixtures():
         s += 1
 
 
-@pytest.mark.parametrize("mm,bw", [(8192, 64), (32768, 128), (1000, 32), (257, 17)])
+# (130, 64), (100, 20), (200, 33): fewer row chunks than the three CTAs the fast
+# panel spreads its second serial section over (the grid is padded to 3)
+@pytest.mark.parametrize("mm,bw", [(8192, 64), (32768, 128), (1000, 32), (257, 17), (130, 64),
+                                   (100, 20), (200, 33)])
 def test_panel_large_vs_oracle(mm, bw):
     from paper_1509_06820_b200.primitives import panel_qr
     P0 = np.random.default_rng(mm + bw).standard_normal((mm, bw))

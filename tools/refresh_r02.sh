@@ -26,3 +26,12 @@ for k in panel_fast_kernel select_reg_kernel; do
     -o $o/ncu_${k}_cfg2 python bench.py --config cfg2 --steps 1 --warmup 1 --no-cpu-baseline \
     --no-e2e > $o/ncu_full_$k.log 2>&1
 done
+# the dominant product of cfg3 (TRQRCP's G = Y_b^T A, tc_tma_kernel) and cfg5's K = 128 trailing
+# update: several launches each (the small side products share the kernels); the summaries take
+# the longest one
+timeout 1200 ncu --set full --import-source on --clock-control none -k regex:tc_tma_kernel -s 10 -c 16 \
+  -o $o/ncu_tc_tma_cfg3 python bench.py --config cfg3 --steps 1 --warmup 1 --no-cpu-baseline \
+  --no-e2e > $o/ncu_full_tc_cfg3.log 2>&1
+timeout 1500 ncu --set full --import-source on --clock-control none -k regex:rank_update_grouped -s 20 -c 4 \
+  -o $o/ncu_update_cfg5 python bench.py --config cfg5 --steps 1 --warmup 1 --no-cpu-baseline \
+  --no-e2e > $o/ncu_full_update_cfg5.log 2>&1
