@@ -452,6 +452,11 @@ def main():
                     "algorithmic_flops_per_launch": FL[i] / max(L[i], 1),
                     "avg_launch_us": MS[i] * 1e3 / max(L[i], 1),
                     "share": kernels[dom]["share"]}
+        if dom == "update":
+            roofline["note"] = ("the trailing update runs beside the next block's pivot selection "
+                                "on the SMs that leaves free (cfg2: 104 of 148, 68 from block ~56 "
+                                "on; cfg5: ~90-105); `achieved` is per launch on that share, "
+                                "`peak` is the whole chip's")
     res_counters = f.counters
     if sharded:
         from paper_1509_06820_b200.factorization import OpCounters

@@ -2,7 +2,7 @@
 // Householder vectors reconstructed from the orthonormal factor (Ballard et
 // al., "Reconstructing Householder vectors from TSQR").  Same outputs as the
 // column-by-column panel kernel (panel.cu: R in the panel rows, unit-lower
-// Y, tau; qrcp.py:206-219 panel_householder), but with 5 grid barriers per
+// Y, tau; qrcp.py:206-219 panel_householder), but with 6 grid barriers per
 // panel instead of one exchange per column.
 //
 // Why it reproduces the reference's reflectors: the Householder QR of a full
@@ -20,8 +20,10 @@
 //   G2 = (P R1^{-1})^T (P R1^{-1})   all CTAs
 //   R2 = I + F  (F = triu(G2 - I), diagonal halved; exact to O(|G2 - I|^2)
 //               because |G2 - I| <= 1e-10 is required)
-//   R~ = R2 R1,  Q~_top = P_top R1^{-1} (I - F),  LU with signs -> S, U, Y_top
-//   Y_below = P_below R1^{-1} (I - F) S U^{-1}     all CTAs
+//   R~ = R2 R1,  Q~_top = P_top R1^{-1} (I - F),  LU with signs -> S, U, Y_top   CTA 0
+//   M = R1^{-1} (I - F) S U^{-1} (CTA 0)  |  sample update's S11 R1^{-1} (I - F) S
+//   (CTA 1)  |  T = -U Y1^{-T}, A1 = Y1 T, A2 = -R1^{-1} (I - F) S Y1^{-T} (CTA 2)
+//   Y_below = P_below M                            all CTAs
 //
 // The fast path only commits when it is safe to skip the reference's
 // column-by-column arithmetic: Cholesky succeeds, diag-ratio of R1 <= 1e3,
