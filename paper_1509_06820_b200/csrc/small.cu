@@ -17,11 +17,15 @@ constexpr int kSuThreads = 64;
 __global__ void __launch_bounds__(kSuThreads) sample_update_kernel(
     int ell, int b, int64_t n2, const double* __restrict__ S, int64_t lds,
     const double* __restrict__ R11, const double* __restrict__ R12, int64_t ldr, double thresh,
-    double* __restrict__ Bn, int64_t ldb, Status* st, int abort_on_degenerate, int64_t i0) {
+    double* __restrict__ Bn, int64_t ldb, Status* st, int abort_on_degenerate, int64_t i0,
+    int r11_staged) {
   if (aborted(st)) return;
   extern __shared__ __align__(16) double sm[];
-  double* r11 = sm;                    // b x b, col-major ld b
-  double* xs = sm + (size_t)b * b;     // b x kSuThreads
+  // R11 staged in shared memory (b x b, col-major ld b) while it fits beside
+  // the solve vectors; wider blocks (b > ~140) read it through L1/L2
+  const double* r11 = r11_staged ? sm : R11;
+  const int64_t ld11 = r11_staged ? b : ldr;
+  double* xs = sm + (r11_staged ? (size_t)b * b : 0);     // b x kSuThreads
   const int tid = threadIdx.x;
   // degenerate test first, as the reference raises before solving (:117)
   __shared__ int s_bad;
@@ -42,9 +46,11 @@ __global__ void __launch_bounds__(kSuThreads) sample_update_kernel(
     return;
   }
   if (blockIdx.x == 0 && tid == 0) st->degenerate = 0;
-  for (int e = tid; e < b * b; e += kSuThreads) {
-    const int i = e % b, j = e / b;
-    r11[e] = R11[i + (size_t)j * ldr];
+  if (r11_staged) {
+    for (int e = tid; e < b * b; e += kSuThreads) {
+      const int i = e % b, j = e / b;
+      sm[e] = R11[i + (size_t)j * ldr];
+    }
   }
   __syncthreads();
   const int64_t c = (int64_t)blockIdx.x * kSuThreads + tid;
@@ -53,10 +59,10 @@ __global__ void __launch_bounds__(kSuThreads) sample_update_kernel(
   for (int i = 0; i < b; ++i) x[i * kSuThreads] = R12[i + (size_t)c * ldr];
   // back substitution (np.linalg.solve on the upper-triangular R11)
   for (int i = b - 1; i >= 0; --i) {
-    const double xi = __ddiv_rn(x[i * kSuThreads], r11[i + i * b]);
+    const double xi = __ddiv_rn(x[i * kSuThreads], r11[i + i * ld11]);
     x[i * kSuThreads] = xi;
     for (int l = 0; l < i; ++l)
-      x[l * kSuThreads] = __fma_rn(-r11[l + i * b], xi, x[l * kSuThreads]);
+      x[l * kSuThreads] = __fma_rn(-r11[l + i * ld11], xi, x[l * kSuThreads]);
   }
   // B1 = S12 - S11 @ X   (S11 upper triangular: only l >= i contribute)
   const double* s12 = S + (size_t)(b + c) * lds;
@@ -687,7 +693,9 @@ void sample_update(Handle& h, int64_t ell, int64_t b, int64_t n2, const double* 
     RQ_CHECK_LAUNCH();
     return;
   }
-  const size_t smem = ((size_t)b * b + (size_t)b * kSuThreads) * 8;
+  size_t smem = ((size_t)b * b + (size_t)b * kSuThreads) * 8;
+  const bool staged = smem <= h.smem_optin;
+  if (!staged) smem = (size_t)b * kSuThreads * 8;
   kernel_attr((const void*)sample_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
               (int)std::max<size_t>(smem, 48 * 1024));
   if (smem > h.smem_optin) throw InvalidArg("sample update block too wide");
@@ -696,7 +704,7 @@ void sample_update(Handle& h, int64_t ell, int64_t b, int64_t n2, const double* 
   count_launch();
   sample_update_kernel<<<blocks, kSuThreads, smem, s>>>(
       (int)ell, (int)b, n2, S, lds, R11, R12, ldr, kEps34 * frob, Bnew, ldb, st,
-      abort_on_degenerate ? 1 : 0, i0);
+      abort_on_degenerate ? 1 : 0, i0, staged ? 1 : 0);
   RQ_CHECK_LAUNCH();
 }
 

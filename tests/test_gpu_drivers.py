@@ -276,6 +276,31 @@ def test_panel_widths_vs_oracle(m, n, b, k, variant):
         (o.counters.gemm_flops, o.counters.level2_flops)
 
 
+@pytest.mark.parametrize("m,n,b,variant", [(1300, 1100, 160, "rqrcp"), (1100, 1400, 200, "rqrcp"),
+                                           (1600, 1500, 256, "rqrcp"), (1500, 1300, 192, "trqrcp"),
+                                           (1200, 1200, 144, "rsrqrcp")])
+def test_block_widths_above_128_vs_oracle(m, n, b, variant):
+    """Block widths 128 < b <= 256 (the reference accepts any b): the exact
+    panel, the recurrence T, plain DMMA GEMMs for the K = b products and the
+    sample update with R11 read through the cache instead of shared memory."""
+    import paper_1509_06820_b200 as P
+    A = np.random.default_rng(m + n + b).standard_normal((m, n))
+    cfg = P.RandomizedConfig(block=b, padding=8, seed=0)
+    k = None if variant != "trqrcp" else 2 * b + 40
+    f = getattr(P, variant)(A, k, cfg)
+    o = getattr(port, variant)(A, k, b, 8, 0)
+    assert f.rank == o.rank
+    np.testing.assert_array_equal(np.asarray(f.perm.forward), o.perm.forward)
+    assert np.linalg.norm(f.R - o.R) <= 1e-10 * np.linalg.norm(o.R)
+    assert (f.counters.gemm_flops, f.counters.level2_flops, f.counters.resamples) == \
+        (o.counters.gemm_flops, o.counters.level2_flops, o.counters.resamples)
+    if variant != "trqrcp":
+        q = f.q_factor()
+        frob = np.linalg.norm(A)
+        assert np.linalg.norm(A[:, np.asarray(f.perm.forward)] - q @ f.R) <= 1e-12 * frob
+        assert np.linalg.norm(q.T @ q - np.eye(q.shape[1]), 2) <= 1e-12
+
+
 @pytest.mark.parametrize("k", [160, 200, 256])
 def test_ssrqrcp_wide_sample_vs_oracle(k):
     """ssrqrcp's single block takes k pivots from a (k + p)-row sample: sample
