@@ -35,6 +35,7 @@ constexpr int kMaxCluster = 16;
 
 struct SelArgs {
   int ell, nt, want;
+  int pbits;        // position bits of the argmax key: 16, or 20 for samples wider than 65535 columns
   int abort_on_short;
   int64_t i0;
   const double* B; int64_t ldb;
@@ -67,12 +68,16 @@ RQ_DEV double warp_sum(double v) {
 // position, np.argmax first-max).  Unsigned order of keys = reference order
 // of candidates up to a 2^-36 relative norm resolution (a near-tie far inside
 // the downdating error).  0 = no candidate.  The owner CTA of a position is
-// read from a position -> owner map every CTA keeps identically.
-RQ_DEV unsigned long long make_key(double nrm, int pos) {
-  const unsigned long long hi = ((unsigned long long)__double_as_longlong(nrm)) >> 16;
-  return (hi << 16) | (unsigned long long)(0xFFFF - pos);
+// read from a position -> owner map every CTA keeps identically.  Samples
+// wider than 65535 columns take 20 position bits (44 norm bits, a 2^-32 band).
+RQ_DEV unsigned long long make_key(double nrm, int pos, int pb) {
+  const unsigned long long hi = ((unsigned long long)__double_as_longlong(nrm)) >> pb;
+  return (hi << pb) | (unsigned long long)(((1 << pb) - 1) - pos);
 }
-RQ_DEV int key_pos(unsigned long long k) { return 0xFFFF - (int)(k & 0xFFFF); }
+RQ_DEV int key_pos(unsigned long long k, int pb) {
+  const int mask = (1 << pb) - 1;
+  return mask - (int)(k & (unsigned long long)mask);
+}
 
 template <bool kCluster>
 __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
@@ -92,6 +97,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
     me = blockIdx.x;
   }
   const int ell = a.ell, ldl = a.ldl, ncs = a.ncs;
+  const int pb = a.pbits;
   const int c0 = me * a.cpb;
   const int ncol = max(0, min(a.nt - c0, a.cpb));
   double* gsp = a.gstore ? a.gstore + (size_t)me * (a.cpb - ncs) * ldl : nullptr;
@@ -187,7 +193,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
         if (tid == 0) atomicMax(a.gkey + slot, bk);
       }
       // the winning group copies its column (+ exact norm) to the publish slot
-      const int bpos = key_pos(bk);
+      const int bpos = key_pos(bk, pb);
       for (int c = grp; c < ncol; c += NG) {
         if (pos[c] != bpos) continue;
         const double* src = colp(c);
@@ -200,7 +206,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
 
   // step-0 candidates
   for (int c = grp; c < ncol; c += NG)
-    if (gl == 0) atomicMax(&s_bkey, make_key(nrm[c], pos[c]));
+    if (gl == 0) atomicMax(&s_bkey, make_key(nrm[c], pos[c], pb));
   publish(0, 0);
   xsync();
   double tol;
@@ -232,7 +238,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
     // ---- warp 0: winner (one key read) and the reflector (kernels.py:26-44)
     if (warp == 0) {
       const unsigned long long wk = slot_max(j % 3);
-      const int owner = wk ? (int)omap[key_pos(wk)] : -1;
+      const int owner = wk ? (int)omap[key_pos(wk, pb)] : -1;
       double xv[5];  // ell <= 160 (longer samples: the loop form below)
       double xnorm = -1.0;
       if (ell > 160) {
@@ -278,9 +284,9 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
         }
         if (lane == 0) {
           s_stepi[0] = halt ? -1 : owner;
-          s_stepi[1] = key_pos(wk);
+          s_stepi[1] = key_pos(wk, pb);
           if (!halt) {
-            const int pp = key_pos(wk);
+            const int pp = key_pos(wk, pb);
             const unsigned char oj = omap[j];
             omap[j] = omap[pp];
             omap[pp] = oj;
@@ -355,9 +361,9 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
       }
       if (lane == 0) {
         s_stepi[0] = halt ? -1 : owner;
-        s_stepi[1] = key_pos(wk);
+        s_stepi[1] = key_pos(wk, pb);
         if (!halt) {  // the swap j <-> p moves the owners too
-          const int pp = key_pos(wk);
+          const int pp = key_pos(wk, pb);
           const unsigned char oj = omap[j];
           omap[j] = omap[pp];
           omap[pp] = oj;
@@ -485,7 +491,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
               orig[c] = __dmul_rn(nn, nn);
             }
           }
-          gbest = max(gbest, make_key(nn, pc));
+          gbest = max(gbest, make_key(nn, pc, pb));
         }
         continue;
       }
@@ -524,7 +530,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_kernel(SelArgs a) {
             orig[c] = __dmul_rn(nn, nn);
           }
         }
-        gbest = max(gbest, make_key(nn, pc));
+        gbest = max(gbest, make_key(nn, pc, pb));
       }
     }
     // warp max of the groups' keys (every lane of a group holds the same gbest)
@@ -608,6 +614,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_reg_kernel(SelArgs a) {
     me = blockIdx.x;
   }
   const int ell = a.ell, ldl = a.ldl;
+  const int pb = a.pbits;
   const int c0 = me * a.cpb;
   const int ncol = max(0, min(a.nt - c0, a.cpb));
   const int cstride = ell + 1;
@@ -724,7 +731,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_reg_kernel(SelArgs a) {
     } else {
       if (tid == 0) atomicMax(fused ? (unsigned long long*)&a.pair[jn % 3].y : a.gkey + (jn % 3), bk);
     }
-    const int bpos = key_pos(bk);
+    const int bpos = key_pos(bk, pb);
 #pragma unroll
     for (int t = 0; t < CPG; ++t) {
       if (pc[t] != bpos) continue;
@@ -762,7 +769,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_reg_kernel(SelArgs a) {
 #pragma unroll
     for (int t = 0; t < CPG; ++t) {
       if (pc[t] < 0) continue;
-      const unsigned long long kt = make_key(nv[t], pc[t]);
+      const unsigned long long kt = make_key(nv[t], pc[t], pb);
       k = kt > k ? kt : k;
     }
     k = group_key(k);
@@ -804,7 +811,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_reg_kernel(SelArgs a) {
     // ---- warp 0: winner and reflector into the shared v / tau v
     if (warp == 0) {
       const unsigned long long wk = slot_max(j % 3);
-      const int pw = key_pos(wk);
+      const int pw = key_pos(wk, pb);
       const int owner = wk ? (int)omap[pw] : -1;
       double xv[5];  // ell <= 160
       double xnorm = -1.0;
@@ -955,7 +962,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_reg_kernel(SelArgs a) {
           og[t] = __dmul_rn(nn, nn);
         }
         nv[t] = nn;
-        const unsigned long long kt = make_key(nn, q);
+        const unsigned long long kt = make_key(nn, q, pb);
         key = kt > key ? kt : key;
       }
     }
@@ -1053,6 +1060,7 @@ bool launch_select_reg(Handle& h, bool grid, int P, int cpb, int64_t ell, int64_
   if (smem > h.smem_optin) return false;
   SelArgs a{};
   a.ell = (int)ell; a.nt = (int)nt; a.want = (int)want;
+  a.pbits = nt > 65535 ? 20 : 16;
   a.abort_on_short = abort_on_short ? 1 : 0;
   a.i0 = i0;
   a.B = B; a.ldb = ldb;
@@ -1093,7 +1101,7 @@ void select_pivots(Handle& h, int64_t ell, int64_t nt, int64_t want, const doubl
     throw InvalidArg("cannot select " + std::to_string(want) + " pivots from a " +
                      std::to_string(ell) + " x " + std::to_string(nt) + " sample");
   if (ell > 1024) throw InvalidArg("sample rows > 1024 not supported by the pivot kernel");
-  if (nt > 65535) throw InvalidArg("sample wider than 65535 columns");
+  if (nt >= (1 << 20)) throw InvalidArg("sample wider than 2^20 - 1 columns");
   const bool grid = h.force_select == 1 ||
                     (h.force_select == 0 && nt > h.select_cluster_max_cols);
   int P;
@@ -1121,6 +1129,7 @@ void select_pivots(Handle& h, int64_t ell, int64_t nt, int64_t want, const doubl
   const size_t smem = (size_t)ncs * colbytes + meta;
   SelArgs a{};
   a.ell = (int)ell; a.nt = (int)nt; a.want = (int)want;
+  a.pbits = nt > 65535 ? 20 : 16;
   a.abort_on_short = abort_on_short ? 1 : 0;
   a.i0 = i0;
   a.B = B; a.ldb = ldb;

@@ -301,6 +301,22 @@ def test_block_widths_above_128_vs_oracle(m, n, b, variant):
         assert np.linalg.norm(q.T @ q - np.eye(q.shape[1]), 2) <= 1e-12
 
 
+def test_trqrcp_more_than_65535_columns_vs_oracle():
+    """A matrix wider than the 16-bit position range of the default argmax
+    key (the reference has no width limit)."""
+    import paper_1509_06820_b200 as P
+    g = np.random.default_rng(66000)
+    m, n, k, b = 600, 66000, 96, 32
+    A = g.standard_normal((m, 200)) @ g.standard_normal((200, n)) + 1e-3 * g.standard_normal((m, n))
+    A[:, 65999] *= 50.0
+    f = P.trqrcp(A, k, P.RandomizedConfig(block=b, padding=8, seed=0))
+    o = port.trqrcp(A, k, b, 8, 0)
+    assert f.rank == o.rank == k
+    assert int(np.asarray(f.perm.forward)[0]) == 65999
+    np.testing.assert_array_equal(np.asarray(f.perm.forward), o.perm.forward)
+    assert np.linalg.norm(f.R - o.R) <= 1e-10 * np.linalg.norm(o.R)
+
+
 @pytest.mark.parametrize("k", [160, 200, 256])
 def test_ssrqrcp_wide_sample_vs_oracle(k):
     """ssrqrcp's single block takes k pivots from a (k + p)-row sample: sample

@@ -87,6 +87,28 @@ def test_select_pivots_wide_sample_vs_oracle():
         assert np.linalg.norm(S.cpu().numpy() - smp.B) <= 1e-12 * np.linalg.norm(B)
 
 
+def test_select_pivots_sample_wider_than_16_bit_positions():
+    """nt > 65535: the argmax key switches to 20 position bits."""
+    from paper_1509_06820_b200.primitives import select_pivots
+    g = np.random.default_rng(70000)
+    ell, nt, want = 40, 70000, 32
+    B = g.standard_normal((ell, nt)) * np.exp(g.uniform(-2, 2, nt))
+    # the largest columns at both ends of the position range
+    B[:, 69999] *= 40.0
+    B[:, 65536] *= 30.0
+    B[:, 3] *= 20.0
+    smp = port.Sample(B=np.asfortranarray(B.copy()), ell=ell)
+    perm, got = port.pick_pivots(smp, want, port.Counters())
+    S, piv, got_d, *_ = select_pivots(_dev(B), want)
+    assert got_d == got
+    assert max(int(p) for p in piv) > 65535   # a pivot beyond the 16-bit range
+    fwd = list(range(nt))
+    for j, p in enumerate(piv):
+        fwd[j], fwd[p] = fwd[p], fwd[j]
+    np.testing.assert_array_equal(fwd, perm.forward)
+    assert np.linalg.norm(S.cpu().numpy() - smp.B) <= 1e-12 * np.linalg.norm(B)
+
+
 @pytest.mark.parametrize("ell,nt,want,ctas", [(136, 5000, 128, 4), (72, 6000, 64, 3),
                                                 (40, 3000, 32, 2), (160, 2500, 100, 2)])
 def test_select_pivots_spilled_columns_vs_oracle(ell, nt, want, ctas):
