@@ -614,7 +614,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_reg_kernel(SelArgs a) {
     me = blockIdx.x;
   }
   const int ell = a.ell, ldl = a.ldl;
-  const int pb = a.pbits;
+  constexpr int pb = 16;   // register-resident samples are < 65536 columns wide (launch_select_reg)
   const int c0 = me * a.cpb;
   const int ncol = max(0, min(a.nt - c0, a.cpb));
   const int cstride = ell + 1;
@@ -1053,7 +1053,7 @@ bool launch_select_reg(Handle& h, bool grid, int P, int cpb, int64_t ell, int64_
   constexpr int NG = kSelThreads / 8, NW = kSelThreads / 32;
   const int cpg = cpb <= NG ? 1 : (cpb <= 2 * NG ? 2 : (cpb <= 3 * NG ? 3 : 0));
   const int rpl = ell <= 40 ? 5 : (ell <= 72 ? 9 : (ell <= 136 ? 17 : (ell <= 160 ? 20 : 0)));
-  if (cpg == 0 || rpl == 0 || (rpl > 9 && cpg > 1)) return false;
+  if (cpg == 0 || rpl == 0 || (rpl > 9 && cpg > 1) || nt > 65535) return false;
   const int ldl = (int)(ell | 1);
   const size_t smem = ((size_t)cpb * ldl + 2 * (size_t)NW * ell + 2 * (ell + 1) + cpb) * 8 +
                       (size_t)nt + 64;
