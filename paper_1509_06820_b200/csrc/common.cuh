@@ -154,12 +154,43 @@ RQ_DEV double pairwise_block_sumsq(const double* x, int n, int stride) {
   return res;
 }
 
+// numpy's recursion (left half n2 = n/2 rounded down to a multiple of 8, then
+// the rest) as an explicit post-order walk: device recursion would need a
+// call stack the launch cannot size (samples taller than 1024 rows overflowed
+// the default one)
 __device__ inline double pairwise_sumsq(const double* x, int n, int stride) {
   if (n <= 128) return pairwise_block_sumsq(x, n, stride);
-  int n2 = n / 2;
-  n2 -= n2 % 8;
-  return __dadd_rn(pairwise_sumsq(x, n2, stride),
-                   pairwise_sumsq(x + (size_t)n2 * stride, n - n2, stride));
+  constexpr int kDepth = 24;   // n halves per level down to <= 128: 2^31 needs 24
+  int off[kDepth], len[kDepth], stage[kDepth];
+  double left[kDepth];
+  int sp = 0;
+  off[0] = 0; len[0] = n; stage[0] = 0;
+  double ret = 0.0;
+  while (sp >= 0) {
+    if (stage[sp] == 0) {
+      if (len[sp] <= 128) {
+        ret = pairwise_block_sumsq(x + (size_t)off[sp] * stride, len[sp], stride);
+        --sp;
+      } else {
+        int n2 = len[sp] / 2;
+        n2 -= n2 % 8;
+        stage[sp] = 1;
+        off[sp + 1] = off[sp]; len[sp + 1] = n2; stage[sp + 1] = 0;
+        ++sp;
+      }
+    } else if (stage[sp] == 1) {
+      left[sp] = ret;
+      int n2 = len[sp] / 2;
+      n2 -= n2 % 8;
+      stage[sp] = 2;
+      off[sp + 1] = off[sp] + n2; len[sp + 1] = len[sp] - n2; stage[sp + 1] = 0;
+      ++sp;
+    } else {
+      ret = __dadd_rn(left[sp], ret);
+      --sp;
+    }
+  }
+  return ret;
 }
 
 }  // namespace rq

@@ -1100,7 +1100,7 @@ void select_pivots(Handle& h, int64_t ell, int64_t nt, int64_t want, const doubl
   if (want < 1 || want > std::min(ell, nt))
     throw InvalidArg("cannot select " + std::to_string(want) + " pivots from a " +
                      std::to_string(ell) + " x " + std::to_string(nt) + " sample");
-  if (ell > 1024) throw InvalidArg("sample rows > 1024 not supported by the pivot kernel");
+  if (ell > 4096) throw InvalidArg("sample rows > 4096 not supported by the pivot kernel");
   if (nt >= (1 << 20)) throw InvalidArg("sample wider than 2^20 - 1 columns");
   const bool grid = h.force_select == 1 ||
                     (h.force_select == 0 && nt > h.select_cluster_max_cols);

@@ -226,7 +226,7 @@ def rqrcp(A, k=None, config=None, omega=None):
 
 
 SSRQRCP_MAX_K = 256     # widest panel the native driver factors in one block (driver.cu)
-SSRQRCP_MAX_ELL = 1024  # rows of the pivot kernel's sample (select.cu)
+SSRQRCP_MAX_ELL = 4096  # rows of the pivot kernel's sample (select.cu)
 
 
 def rsrqrcp(A, k=None, config=None, omega=None):

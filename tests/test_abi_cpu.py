@@ -100,5 +100,5 @@ def test_permutation_semantics():
 
 def test_ssrqrcp_sample_beyond_the_pivot_kernel_rejected_before_any_device_work():
     import paper_1509_06820_b200 as P
-    with pytest.raises(NotImplementedError, match="k = 1100"):
-        P.ssrqrcp(np.zeros((1200, 1200)), 1100, P.RandomizedConfig(padding=8))
+    with pytest.raises(NotImplementedError, match="k = 4100"):
+        P.ssrqrcp(np.zeros((4200, 4200)), 4100, P.RandomizedConfig(padding=8))

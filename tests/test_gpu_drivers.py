@@ -379,6 +379,7 @@ def test_b128_second_half_decline_rewinds_to_original_columns():
 
 
 @pytest.mark.parametrize("m,n,k,kind", [(1000, 900, 300, "gauss"), (800, 1200, 520, "gauss"),
+                                         (1700, 1500, 1200, "gauss"),   # sample taller than 1024 rows
                                         (900, 700, 400, "lowrank")])
 def test_ssrqrcp_wider_than_one_native_panel_vs_oracle(m, n, k, kind):
     """ssrqrcp(A, k) with k > 256 (one block of width k; randomized.py:299-313):

@@ -74,7 +74,7 @@ def test_select_pivots_wide_sample_vs_oracle():
     from paper_1509_06820_b200.primitives import select_pivots
     g = np.random.default_rng(5)
     for ell, nt, want in ((72, 8192, 64), (40, 1000, 32), (136, 5000, 128), (20, 33, 12),
-                          (300, 2000, 250), (264, 700, 256)):
+                          (300, 2000, 250), (264, 700, 256), (1100, 1500, 1050)):
         B = g.standard_normal((ell, nt)) * np.exp(g.uniform(-2, 2, nt))
         smp = port.Sample(B=np.asfortranarray(B.copy()), ell=ell)
         perm, got = port.pick_pivots(smp, want, port.Counters())
