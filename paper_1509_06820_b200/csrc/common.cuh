@@ -154,6 +154,15 @@ RQ_DEV double pairwise_block_sumsq(const double* x, int n, int stride) {
   return res;
 }
 
+// n <= 256: one split at most (the register-resident pivot kernel's samples)
+__device__ inline double pairwise_sumsq_256(const double* x, int n, int stride) {
+  if (n <= 128) return pairwise_block_sumsq(x, n, stride);
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  return __dadd_rn(pairwise_block_sumsq(x, n2, stride),
+                   pairwise_block_sumsq(x + (size_t)n2 * stride, n - n2, stride));
+}
+
 // numpy's recursion (left half n2 = n/2 rounded down to a multiple of 8, then
 // the rest) as an explicit post-order walk: device recursion would need a
 // call stack the launch cannot size (samples taller than 1024 rows overflowed

@@ -686,7 +686,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_reg_kernel(SelArgs a) {
   __syncthreads();
   double mysq = 0.0;
   for (int c = tid; c < ncol; c += kSelThreads) {
-    const double sq = pairwise_sumsq(stage + (size_t)c * ldl, ell, 1);
+    const double sq = pairwise_sumsq_256(stage + (size_t)c * ldl, ell, 1);   // ell <= 160 here
     nrm0[c] = sqrt(sq);
     mysq = __dadd_rn(mysq, sq);
   }
