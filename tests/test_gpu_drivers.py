@@ -218,6 +218,28 @@ def test_tuxv_tall_vs_oracle():
     assert abs(np.linalg.norm(A - f.approx()) - np.linalg.norm(A - o.approx())) <= 1e-3 * frob
 
 
+@pytest.mark.parametrize("j_max", [2, 3])
+def test_tuxv_extra_half_iterations_vs_oracle(j_max):
+    """tuxv(j_max > 1): the extra QLP half-iterations U^T A -> LQ -> A V -> QR
+    (truncated.py:230-252) against the oracle: singular values, the
+    approximation, rank and the counters the iterations add."""
+    import paper_1509_06820_b200 as P
+    g = np.random.default_rng(40 + j_max)
+    m, n, r = 1500, 1100, 96
+    U = np.linalg.qr(g.standard_normal((m, r + 40)))[0]
+    V = np.linalg.qr(g.standard_normal((n, r + 40)))[0]
+    s = 10.0 ** (-6.0 * np.arange(r + 40) / (r + 39))
+    A = np.asfortranarray((U * s) @ V.T)
+    cfg = P.RandomizedConfig(block=32, padding=8, seed=0)
+    o = port.tuxv(A, r, 32, 8, 0, j_max=j_max)
+    f = P.tuxv(A, r, cfg, j_max=j_max)
+    assert f.rank == o.rank
+    np.testing.assert_allclose(f.singular_values(), o.singular_values(), rtol=1e-9)
+    frob = np.linalg.norm(A)
+    assert np.linalg.norm(f.approx() - o.approx()) <= 1e-9 * frob
+    assert f.counters.gemm_flops == o.counters.gemm_flops
+
+
 def test_harness_callers_vs_reference():
     """The GPU harness (harness.py:89-241 callers): the counter CSV is byte-
     identical to the reference's, the pivot trace has the same pivots, sigma
