@@ -240,6 +240,69 @@ def test_tuxv_extra_half_iterations_vs_oracle(j_max):
     assert f.counters.gemm_flops == o.counters.gemm_flops
 
 
+def _full_residual(A, f):
+    m, n = A.shape
+    rebuilt = np.zeros((m, n))
+    rebuilt[: f.rank] = f.R
+    if f.trailing is not None:
+        rebuilt[f.rank:, f.rank:] = f.trailing
+    return np.linalg.norm(A[:, np.asarray(f.perm.forward)] - f.q_factor(full=True) @ rebuilt)
+
+
+@pytest.mark.parametrize("m,n,k,b,p,seed", [(60, 45, 20, 8, 4, 0), (60, 45, 20, 8, 4, 2), (50, 40, 24, 8, 4, 11),
+                                            (64, 48, 32, 8, 4, 5), (20, 16, 16, 4, 4, 0), (48, 36, 12, 12, 8, 7),
+                                            (16, 4, 2, 32, 8, 3), (4, 4, 2, 32, 2, 9), (40, 30, 8, 32, 8, 1)])
+def test_reference_test_shapes_vs_oracle(m, n, k, b, p, seed):
+    """The shapes of the reference's own driver tests (tests/test_randomized.py:
+    60 x 45 down to 4 x 4, blocks of 4-12 columns, paddings 2-8, partial ranks
+    with a trailing block) through all three block drivers against the oracle:
+    pivots, R, the trailing block, rank, counters, the full residual with the
+    trailing block folded back in and orthogonality."""
+    import paper_1509_06820_b200 as P
+    g = np.random.default_rng(100 * seed + m)
+    A = g.standard_normal((m, n))
+    cfg = P.RandomizedConfig(block=b, padding=p, seed=seed)
+    for drv in ("rqrcp", "rsrqrcp", "ssrqrcp"):
+        # (the last three shapes are the reference's ssrqrcp-only cases: the
+        # block drivers' b + p rows do not fit them)
+        if (drv == "ssrqrcp" and k + p > m) or (drv != "ssrqrcp" and b + p > m):
+            continue
+        f = getattr(P, drv)(A, k, cfg)
+        o = getattr(port, drv)(A, k, b, p, seed)
+        assert f.rank == o.rank == k, drv
+        np.testing.assert_array_equal(np.asarray(f.perm.forward), o.perm.forward, err_msg=drv)
+        assert np.linalg.norm(f.R - o.R) <= 1e-10 * np.linalg.norm(o.R), drv
+        assert f.counters.gemm_flops == o.counters.gemm_flops, drv
+        assert f.counters.resamples == o.counters.resamples, drv
+        q = f.q_factor()
+        assert np.linalg.norm(q.T @ q - np.eye(k)) <= 1e-13, drv
+        if drv == "ssrqrcp":
+            assert f.trailing is None
+            assert np.linalg.norm(A[:, np.asarray(f.perm.forward)][:, :k] - q @ f.R[:, :k]) <= 1e-12 * np.linalg.norm(A)
+        else:
+            assert _full_residual(A, f) <= 1e-12 * np.linalg.norm(A), drv
+
+
+def test_reference_rank_deficient_and_single_block_identities():
+    """Two properties the reference's tests pin (tests/test_randomized.py): a
+    rank-10 50 x 40 matrix stops at rank 10 in rqrcp and rsrqrcp, and with
+    block == k the single-sample driver is the first block of rqrcp and of
+    rsrqrcp -- identical pivots and R."""
+    import paper_1509_06820_b200 as P
+    g = np.random.default_rng(5)
+    A = g.standard_normal((50, 10)) @ g.standard_normal((10, 40))
+    cfg = P.RandomizedConfig(block=8, padding=4, seed=0)
+    assert P.rqrcp(A, 20, cfg).rank == port.rqrcp(A, 20, 8, 4, 0).rank == 10
+    assert P.rsrqrcp(A, 20, cfg).rank == 10
+    B = np.random.default_rng(9).standard_normal((48, 36))
+    cfg = P.RandomizedConfig(block=12, padding=8, seed=7)
+    fs, fr, fv = P.ssrqrcp(B, 12, cfg), P.rqrcp(B, 12, cfg), P.rsrqrcp(B, 12, cfg)
+    assert list(fs.perm.forward) == list(fr.perm.forward) == list(fv.perm.forward)
+    assert np.linalg.norm(fs.R - fr.R[:12]) <= 1e-13 * np.linalg.norm(fr.R)
+    assert np.linalg.norm(fv.R - fr.R) <= 1e-13 * np.linalg.norm(fr.R)
+    assert fs.counters.gemm_flops < P.rqrcp(B, 12, P.RandomizedConfig(block=6, padding=8, seed=7)).counters.gemm_flops + 10**9
+
+
 def test_harness_callers_vs_reference():
     """The GPU harness (harness.py:89-241 callers): the counter CSV is byte-
     identical to the reference's, the pivot trace has the same pivots, sigma
