@@ -303,6 +303,86 @@ def test_reference_rank_deficient_and_single_block_identities():
     assert fs.counters.gemm_flops < P.rqrcp(B, 12, P.RandomizedConfig(block=6, padding=8, seed=7)).counters.gemm_flops + 10**9
 
 
+def _decaying(seed, m, n, base=0.9):
+    g = np.random.default_rng(seed)
+    q1 = np.linalg.qr(g.standard_normal((m, m)))[0]
+    q2 = np.linalg.qr(g.standard_normal((n, n)))[0]
+    r = min(m, n)
+    return (q1[:, :r] * base ** np.arange(r)) @ q2[:r]
+
+
+@pytest.mark.parametrize("m,n,k,b,p,seed", [(64, 48, 16, 8, 4, 3), (48, 64, 24, 8, 4, 3), (50, 50, 32, 8, 4, 3),
+                                            (30, 20, 6, 6, 4, 2), (40, 32, 16, 8, 8, 4)])
+def test_reference_truncated_shapes_vs_oracle(m, n, k, b, p, seed):
+    """The shapes of the reference's trqrcp tests (tests/test_truncated.py):
+    same pivots as rqrcp, R rows to rounding, the oracle's W panel, the
+    single-block W invariant W^T = T^T Y^T (A P), orthonormal Q."""
+    import paper_1509_06820_b200 as P
+    A = np.random.default_rng(42 + m).standard_normal((m, n))
+    cfg = P.RandomizedConfig(block=b, padding=p, seed=seed)
+    ft, fr = P.trqrcp(A, k, cfg), P.rqrcp(A, k, cfg)
+    o = port.trqrcp(A, k, b, p, seed)
+    assert list(ft.perm.forward) == list(fr.perm.forward) == list(o.perm.forward)
+    scale = 100 * EPS * np.linalg.norm(A)
+    assert np.linalg.norm(ft.R - fr.R) <= scale
+    assert np.linalg.norm(ft.R - o.R) <= scale
+    assert np.linalg.norm(ft.reflectors.Y - fr.reflectors.Y) <= scale
+    assert np.linalg.norm(ft.reflectors.W - o.W) <= 10 * scale
+    assert ft.counters.gemm_flops == o.counters.gemm_flops
+    q = ft.q_factor()
+    assert np.linalg.norm(q.T @ q - np.eye(k)) <= 1e-13
+    if k == b:   # a single block: the inner-product panel is definitional
+        Y, T = ft.reflectors.Y, port.t_factor(ft.reflectors.Y, ft.reflectors.tau)
+        AP = A[:, np.asarray(ft.perm.forward)]
+        assert np.linalg.norm(ft.reflectors.W[k:].T - T.T @ (Y.T @ AP[:, k:])) <= 1e-12 * np.linalg.norm(A)
+        assert np.all(ft.reflectors.W[:k] == 0.0)
+
+
+def test_reference_truncated_small_cases():
+    """Small known answers of the reference's truncated tests: a rank-12 and a
+    rank-10 input (exact reconstruction, numerical rank), lq_factor of a row
+    vector and of a lower-triangular matrix, tuxv of diag(5, 3, 1), the
+    svd_of_x rotation, the recorded iteration count and a monotone refinement
+    sweep."""
+    import paper_1509_06820_b200 as P
+    g = np.random.default_rng(7)
+    A = g.standard_normal((50, 12)) @ g.standard_normal((12, 40))
+    f = P.trqrcp(A, 12, P.RandomizedConfig(block=4, padding=4, seed=1))
+    assert np.linalg.norm(A[:, np.asarray(f.perm.forward)] - f.reconstruct()) <= 1e-10 * np.linalg.norm(A)
+    A = g.standard_normal((60, 10)) @ g.standard_normal((10, 50))
+    f = P.trqrcp(A, 24, P.RandomizedConfig(block=8, padding=4, seed=0))
+    assert f.rank == 10 and f.R.shape == (10, 50)
+    L, V = P.lq_factor(np.array([[3.0, 4.0]]))
+    np.testing.assert_allclose(L, [[-5.0]], atol=1e-15)
+    np.testing.assert_allclose(V, [[-0.6], [-0.8]], atol=1e-15)
+    Z = np.array([[2.0, 0.0], [1.0, 3.0]])
+    L, V = P.lq_factor(Z)
+    np.testing.assert_allclose(np.abs(V), np.eye(2), atol=1e-14)
+    np.testing.assert_allclose(L @ V.T, Z, atol=1e-14)
+    assert np.linalg.norm(np.triu(L, 1)) == 0.0
+    D = np.diag([5.0, 3.0, 1.0])
+    f = P.tuxv(D, 2, P.RandomizedConfig(block=2, padding=1, seed=0))
+    np.testing.assert_allclose(f.singular_values(), [5.0, 3.0], atol=1e-12)
+    np.testing.assert_allclose(np.linalg.norm(D - f.approx()), 1.0, atol=1e-12)
+    A = np.random.default_rng(14).standard_normal((40, 30))
+    cfg = P.RandomizedConfig(block=5, padding=5, seed=6)
+    plain, rot = P.tuxv(A, 10, cfg), P.tuxv(A, 10, cfg, svd_of_x=True)
+    d = np.diag(rot.X)
+    assert np.linalg.norm(rot.X - np.diag(d)) <= 1e-12
+    assert np.all(d >= 0.0) and np.all(np.diff(d) <= 1e-12)
+    np.testing.assert_allclose(rot.approx(), plain.approx(), atol=1e-12)
+    np.testing.assert_allclose(d, np.linalg.svd(plain.X, compute_uv=False), atol=1e-12)
+    A = np.random.default_rng(15).standard_normal((24, 18))
+    assert P.tuxv(A, 6, P.RandomizedConfig(block=3, padding=3, seed=0), j_max=4).iterations == 4
+    A = _decaying(8, 64, 48)
+    cfg = P.RandomizedConfig(block=4, padding=4, seed=7)
+    errs = [np.linalg.norm(A - P.tuxv(A, 8, cfg, j_max=j).approx()) for j in (1, 2, 3, 5)]
+    for lo, hi in zip(errs[1:], errs[:-1]):
+        assert lo <= hi * (1.0 + 1e-10)
+    sv = np.linalg.svd(A, compute_uv=False)
+    assert errs[-1] >= np.sqrt(np.sum(sv[8:] ** 2)) * (1.0 - 1e-10)
+
+
 def test_harness_callers_vs_reference():
     """The GPU harness (harness.py:89-241 callers): the counter CSV is byte-
     identical to the reference's, the pivot trace has the same pivots, sigma
