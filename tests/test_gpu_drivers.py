@@ -200,6 +200,46 @@ def test_qr_blocked_presorted_vs_reference():
         assert np.linalg.norm(Ap[:, :f.rank] - q @ f.R[:, :f.rank]) <= 1e-12 * np.linalg.norm(A), key
 
 
+def test_reference_plain_qr_small_cases():
+    """Small known answers of the reference's plain-QR tests
+    (tests/test_qrcp.py): identity, block-size invariance on 64 x 48, wide and
+    tall 9 x 17 / 17 x 9 inputs with the full Q, presorted diag(1, 3, 2), ties
+    kept in order, the first diagonal equal to the largest column norm."""
+    import paper_1509_06820_b200 as P
+
+    def rec_err(f, A):
+        m, n = A.shape
+        rebuilt = np.zeros((m, n))
+        rebuilt[: f.rank] = f.R
+        if f.trailing is not None:
+            rebuilt[f.rank:, f.rank:] = f.trailing
+        return np.linalg.norm(A[:, np.asarray(f.perm.forward)] - f.q_factor(full=True) @ rebuilt) / np.linalg.norm(A)
+
+    np.testing.assert_allclose(np.abs(P.qr_blocked(np.eye(3)).R), np.eye(3))
+    A = np.random.default_rng(8).standard_normal((64, 48))
+    f1, f2 = P.qr_blocked(A, b=16), P.qr_blocked(A, b=48)
+    np.testing.assert_allclose(f1.R, f2.R, atol=50 * EPS * 64 * np.linalg.norm(A))
+    assert rec_err(f1, A) <= 100 * EPS * 64
+    g = np.random.default_rng(10)
+    for shape in ((9, 17), (17, 9)):
+        A = g.standard_normal(shape)
+        f = P.qr_blocked(A, b=4)
+        o = port.qr_blocked(np.asfortranarray(A.copy()), b=4)
+        assert np.linalg.norm(f.R - o[2][: f.R.shape[0]]) <= 1e-12 * np.linalg.norm(A)
+        assert rec_err(f, A) <= 100 * EPS * max(shape)
+        Q = f.q_factor(full=True)
+        assert np.linalg.norm(Q.T @ Q - np.eye(shape[0])) <= 100 * EPS * max(shape)
+    f = P.qr_presorted(np.diag([1.0, 3.0, 2.0]))
+    assert list(f.perm.forward) == [1, 2, 0]
+    np.testing.assert_allclose(np.abs(np.diag(f.R)), [3.0, 2.0, 1.0])
+    assert list(P.qr_presorted(np.eye(5)).perm.forward) == [0, 1, 2, 3, 4]
+    g = np.random.default_rng(13)
+    A = g.standard_normal((12, 10)) * np.exp(g.uniform(-2, 2, 10))
+    f = P.qr_presorted(A)
+    assert abs(abs(f.R[0, 0]) - np.linalg.norm(A, axis=0).max()) <= 1e-10
+    assert rec_err(f, A) <= 100 * EPS * 12
+
+
 def test_tuxv_tall_vs_oracle():
     """TUXV whose blocked QRs (b = 32) run on tall 12000-row blocks: several
     trailing-update tiles per CTA (the cfg4 shape class)."""
