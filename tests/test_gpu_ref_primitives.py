@@ -216,3 +216,81 @@ def test_reference_block_loop_through_the_primitives():
     f = P.rqrcp(A, None, cfg)
     np.testing.assert_array_equal(perm.forward, f.perm.forward)
     assert np.linalg.norm(work[:min(m, n)] - f.R) <= 1e-11 * np.linalg.norm(f.R)
+
+
+def test_reference_sample_primitive_small_cases():
+    """Small properties the reference's own tests pin for the sample
+    primitives (tests/test_randomized.py), at their sizes: one GEMM's counters
+    and shapes, a zero matrix, ell validation, descending-norm selection on a
+    diagonal sample, the definitional QRCP of a square sample, R12 = 0 keeps
+    S12 and S22 bit for bit, a 1e-300 diagonal raises."""
+    import paper_1509_06820_b200 as P
+    A = np.random.default_rng(0).standard_normal((12, 9))
+    c = P.OpCounters()
+    s = P.make_sample(A, 6, P.RngState(3), c)
+    assert s.B.shape == (6, 9) and s.ell == 6
+    assert c.gemm_flops == 2 * 6 * 12 * 9
+    assert np.all(P.make_sample(np.zeros((5, 4)), 3, P.RngState(0), P.OpCounters()).B == 0.0)
+    with pytest.raises(ValueError):
+        P.make_sample(np.eye(4), 0, P.RngState(0), P.OpCounters())
+    B = np.zeros((4, 6))
+    np.fill_diagonal(B, [2.0, 5.0, 1.0, 4.0])
+    smp = P.SampleState(B=B.copy(), ell=4, frob_a=float(np.linalg.norm(B)))
+    perm, got = P.select_pivots(smp, 4, P.OpCounters())
+    assert got == 4 and list(perm.forward[:4]) == [1, 3, 0, 2]
+    # square sample, all pivots: the eliminated sample carries the QRCP's R
+    B = np.random.default_rng(7).standard_normal((5, 5))
+    smp = P.SampleState(B=B.copy(), ell=5, frob_a=float(np.linalg.norm(B)))
+    perm, got = P.select_pivots(smp, 5, P.OpCounters())
+    ref = port.Sample(B=np.asfortranarray(B.copy()), ell=5)
+    perm_r, got_r = port.pick_pivots(ref, 5, port.Counters())
+    assert got == got_r == 5 and list(perm.forward) == list(perm_r.forward)
+    assert np.linalg.norm(np.triu(smp.B) - np.triu(ref.B)) <= 1e-12 * np.linalg.norm(B)
+    Qr = np.linalg.qr(B[:, perm.forward], mode="r")
+    assert np.linalg.norm(np.abs(np.triu(smp.B)) - np.abs(Qr)) <= 1e-12 * np.linalg.norm(B)
+    # R12 = 0: the correction vanishes exactly
+    g = np.random.default_rng(1)
+    B = g.standard_normal((5, 8))
+    smp = P.SampleState(B=B.copy(), ell=5, frob_a=float(np.linalg.norm(B)))
+    _, got = P.select_pivots(smp, 2, P.OpCounters())
+    assert got == 2
+    s12, s22 = smp.s12.copy(), smp.s22.copy()
+    r11 = np.triu(g.standard_normal((2, 2))) + 5.0 * np.eye(2)
+    P.sample_update(smp, r11, np.zeros((2, 6)), P.OpCounters())
+    np.testing.assert_array_equal(smp.B[:2], s12)
+    np.testing.assert_array_equal(smp.B[2:], s22)
+    g = np.random.default_rng(2)
+    B = g.standard_normal((4, 6))
+    smp = P.SampleState(B=B.copy(), ell=4, frob_a=float(np.linalg.norm(B)))
+    P.select_pivots(smp, 2, P.OpCounters())
+    with pytest.raises(P.DegenerateSampleError):
+        P.sample_update(smp, np.array([[1.0, 0.5], [0.0, 1e-300]]), g.standard_normal((2, 4)),
+                        P.OpCounters())
+
+
+def test_reference_select_quality_monte_carlo():
+    """The reference's replay check (tests/test_randomized.py): 200 seeded
+    6 x 10 samples, 4 pivots each; every pick must be the argmax of the
+    independently recomputed residual norms (within the 0.5x floor the
+    reference uses), and equal the oracle's pick."""
+    import paper_1509_06820_b200 as P
+    good = 0
+    for t in range(200):
+        B = np.random.default_rng(t).standard_normal((6, 10))
+        smp = P.SampleState(B=B.copy(), ell=6, frob_a=float(np.linalg.norm(B)))
+        perm, got = P.select_pivots(smp, 4, P.OpCounters())
+        assert got == 4
+        ref = port.Sample(B=np.asfortranarray(B.copy()), ell=6)
+        perm_r, _ = port.pick_pivots(ref, 4, port.Counters())
+        assert list(perm.forward) == list(perm_r.forward), t
+        work = B[:, perm.forward].copy()
+        ok = True
+        for step in range(4):
+            norms = np.sum(work[step:, step:] ** 2, axis=0)
+            ok = ok and norms[0] >= 0.5 * norms.max()
+            v, tau, beta = port.householder(work[step:, step].copy())
+            work[step, step] = beta
+            work[step + 1:, step] = 0.0
+            port.reflect_left(work[step:, step + 1:], v, tau)
+        good += ok
+    assert good == 200
