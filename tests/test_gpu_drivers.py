@@ -629,3 +629,59 @@ def test_b128_two_half_panels_vs_oracle(m, n):
     assert np.linalg.norm(f.R - o.R) <= 1e-10 * np.linalg.norm(o.R)
     assert (f.counters.gemm_flops, f.counters.level2_flops, f.counters.resamples) == (
         o.counters.gemm_flops, o.counters.level2_flops, o.counters.resamples)
+
+
+def test_reference_acceptance_criteria_on_the_hot_path():
+    """The reference's release criteria that concern this path
+    (tests/test_acceptance.py), with its instances and pinned tolerances:
+    01 reconstruction and orthogonality of every full factorization (20
+    instances x qr / qr_presorted / rqrcp / rsrqrcp), 04 trqrcp == rqrcp
+    pivots with R rows within 100 eps ||A|| (20 instances), 05 tuxv equals
+    the factor-everything-then-truncate oracle within 1e-9 (10 instances),
+    06a sample reuse keeps gemm(rqrcp) / gemm(rsrqrcp) <= 0.72 on 256 x 256."""
+    import paper_1509_06820_b200 as P
+    shapes = [(256, 256), (192, 256), (256, 192), (128, 128), (96, 64)]
+    algos = {"qr": lambda a, s: P.qr_blocked(a),
+             "qr_presorted": lambda a, s: P.qr_presorted(a),
+             "rqrcp": lambda a, s: P.rqrcp(a, None, P.RandomizedConfig(block=32, padding=8, seed=s)),
+             "rsrqrcp": lambda a, s: P.rsrqrcp(a, None, P.RandomizedConfig(block=32, padding=8, seed=s))}
+    for idx in range(20):
+        m, n = shapes[idx % len(shapes)]
+        a = np.random.default_rng(idx).standard_normal((m, n))
+        frob = np.linalg.norm(a)
+        for name, run in algos.items():
+            f = run(a, idx)
+            assert f.rank == min(m, n), (name, idx)
+            q = f.q_factor()
+            assert np.linalg.norm(a[:, np.asarray(f.perm.forward)] - q @ f.R) <= 100 * EPS * max(m, n) * frob, (name, idx)
+            assert np.linalg.norm(q.T @ q - np.eye(f.rank)) <= 100 * EPS * min(m, n), (name, idx)
+        if idx % 5 == 0:   # the randomized drivers also against the oracle
+            o = port.rqrcp(a, None, 32, 8, idx)
+            f = algos["rqrcp"](a, idx)
+            np.testing.assert_array_equal(np.asarray(f.perm.forward), o.perm.forward)
+    shapes = [(128, 96), (96, 128), (128, 128), (160, 96)]
+    ks = [16, 32, 48, 64]
+    for idx in range(20):
+        m, n = shapes[idx % len(shapes)]
+        k = min(ks[idx % len(ks)], min(m, n))
+        a = np.random.default_rng(100 + idx).standard_normal((m, n))
+        cfg = P.RandomizedConfig(block=16, padding=8, seed=idx)
+        ft, fr = P.trqrcp(a, k, cfg), P.rqrcp(a, k, cfg)
+        assert list(ft.perm.forward) == list(fr.perm.forward), idx
+        assert np.linalg.norm(ft.R - fr.R) <= 100 * EPS * np.linalg.norm(a), idx
+    shapes = [(128, 96), (96, 64), (80, 80), (128, 48), (64, 64)]
+    ks = [16, 32, 24, 16, 32]
+    for idx in range(10):
+        m, n = shapes[idx % len(shapes)]
+        k = ks[idx % len(ks)]
+        a = np.random.default_rng(200 + idx).standard_normal((m, n))
+        cfg = P.RandomizedConfig(block=16, padding=8, seed=idx)
+        t = P.tuxv(a, k, cfg, j_max=1)
+        full = P.rqrcp(a, None, cfg)
+        _, v = P.lq_factor(full.perm.restore(full.R))
+        oracle = (a @ v[:, :k]) @ v[:, :k].T
+        assert np.linalg.norm(t.approx() - oracle) <= 1e-9 * np.linalg.norm(a), idx
+    a = np.random.default_rng(0).standard_normal((256, 256))
+    cfg = P.RandomizedConfig(block=16, padding=8, seed=0)
+    f1, f2 = P.rqrcp(a, None, cfg), P.rsrqrcp(a, None, cfg)
+    assert f1.counters.gemm_flops / f2.counters.gemm_flops <= 0.72
