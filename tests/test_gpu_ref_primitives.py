@@ -294,3 +294,65 @@ def test_reference_select_quality_monte_carlo():
             port.reflect_left(work[step:, step + 1:], v, tau)
         good += ok
     assert good == 200
+
+
+def test_reference_kernel_small_known_answers():
+    """The reference's small known answers for the block kernels
+    (tests/test_kernels.py): [3, 4] -> beta -5, tau 1.6, v [1, 0.5]; an
+    aligned vector still flips; the zero vector; T of one reflector and of
+    orthogonal reflectors; empty and mismatched compose_blocks; the block
+    reflection's round trip, flop count and no-op cases; column norms of the
+    identity; norm downdates 5, 4 -> 3 and never negative."""
+    import paper_1509_06820_b200 as P
+    r = P.form_reflector(np.array([3.0, 4.0]))
+    assert r.beta == -5.0 and abs(r.tau - 1.6) <= 1e-15
+    np.testing.assert_allclose(r.v, [1.0, 0.5])
+    H = np.eye(2) - r.tau * np.outer(r.v, r.v)
+    np.testing.assert_allclose(H @ [3.0, 4.0], [-5.0, 0.0], atol=1e-14)
+    r2 = P.form_reflector(np.array([2.0, 0.0, 0.0]))
+    assert r2.tau == 2.0 and r2.beta == -2.0
+    np.testing.assert_allclose(r2.v, [1.0, 0.0, 0.0])
+    r0 = P.form_reflector(np.zeros(2))
+    assert r0.tau == 0.0 and r0.beta == 0.0 and r0.v[0] == 1.0
+    # involution and annihilation on random vectors
+    for n, seed in ((1, 0), (7, 3), (40, 9)):
+        x = np.random.default_rng(seed).standard_normal(n)
+        rr = P.form_reflector(x)
+        H = np.eye(n) - rr.tau * np.outer(rr.v, rr.v)
+        e1 = np.zeros(n); e1[0] = rr.beta
+        assert np.linalg.norm(H @ x - e1) <= 1e-13 * max(1.0, np.linalg.norm(x))
+        assert np.linalg.norm(H @ H - np.eye(n)) <= 1e-13
+    np.testing.assert_allclose(P.build_t_matrix(r.v.reshape(2, 1), np.array([r.tau])), [[r.tau]])
+    Y = np.array([[1.0, 0.0], [0.0, 1.0], [1.0, 0.0], [0.0, 2.0]])
+    tau = 2.0 / np.sum(Y * Y, axis=0)
+    np.testing.assert_allclose(P.build_t_matrix(Y, tau), np.diag(tau), atol=1e-15)
+    g = np.random.default_rng(4)
+    Y3, T3 = g.standard_normal((8, 3)), g.standard_normal((3, 3))
+    Yc, Tc = P.compose_blocks(Y3, T3, np.zeros((8, 0)), np.zeros((0, 0)))
+    np.testing.assert_allclose(Yc, Y3)
+    np.testing.assert_allclose(Tc, T3)
+    _, Tc = P.compose_blocks(np.zeros((8, 0)), np.zeros((0, 0)), Y3, T3)
+    np.testing.assert_allclose(Tc, T3)
+    with pytest.raises(ValueError):
+        P.compose_blocks(np.ones((4, 1)), np.ones((1, 1)), np.ones((5, 1)), np.ones((1, 1)))
+    # a genuine 5-reflector block on 20 rows: H then H^T is the identity
+    m, n, b = 20, 9, 5
+    M = np.random.default_rng(7).standard_normal((m, b))
+    Yb, tb = port.panel_qr(np.asfortranarray(M.copy()))
+    Tb = P.build_t_matrix(Yb, tb)
+    assert np.linalg.norm(Tb - port.t_factor(Yb, tb)) <= 1e-14 * np.linalg.norm(Tb)
+    A0 = np.random.default_rng(8).standard_normal((m, n))
+    A = A0.copy()
+    c = P.OpCounters()
+    P.apply_block_reflection(A, Yb, Tb, counters=c)
+    P.apply_block_reflection(A, Yb, Tb, transpose=True, counters=c)
+    np.testing.assert_allclose(A, A0, atol=1e-12)
+    assert c.gemm_flops == 2 * (4 * m * b * n + b * b * n) and c.bytes_touched > 0
+    with pytest.raises(ValueError):
+        P.apply_block_reflection(np.ones((7, 3)), Yb[:8, :2], Tb[:2, :2])
+    A1 = np.ones((8, 3))
+    P.apply_block_reflection(A1, np.zeros((8, 0)), np.zeros((0, 0)))
+    np.testing.assert_allclose(A1, 1.0)
+    np.testing.assert_allclose(P.column_norms(np.eye(4)), np.ones(4))
+    assert abs(P.downdate_norms(np.array([5.0]), np.array([4.0]))[0] - 3.0) <= 1e-15
+    assert P.downdate_norms(np.array([3.0]), np.array([3.0000001]))[0] == 0.0
