@@ -904,6 +904,99 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_reg_kernel(SelArgs a) {
       vr[r] = (i >= j && i < ell) ? wv[i] : 0.0;
     }
     unsigned long long key = 0ull;
+    if constexpr (CPG > 1) {
+      // Several columns per group: the same arithmetic per column as the
+      // one-column form below, but phase by phase over the columns (dot
+      // products, reductions, updates, norms), without per-column branches,
+      // so the columns' dependent chains overlap.  Inactive columns (pivoted
+      // ones, the pivot itself, empty slots) run the arithmetic too and
+      // discard it.
+      int qq[CPG];
+      bool act[CPG], isp[CPG];
+#pragma unroll
+      for (int t = 0; t < CPG; ++t) {
+        int q = pc[t];
+        isp[t] = q >= 0 && q == p;
+        if (!isp[t] && q == j && p != j) {
+          q = p;
+          pc[t] = p;
+        }
+        act[t] = !isp[t] && q > j;
+        qq[t] = q;
+      }
+      if (tau != 0.0) {
+        double w[CPG];
+#pragma unroll
+        for (int t = 0; t < CPG; ++t) {
+          double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+          for (int r = 0; r < RPL; r += 2) {
+            d0 = __fma_rn(vr[r], x[t][r], d0);
+            if (r + 1 < RPL) d1 = __fma_rn(vr[r + 1], x[t][r + 1], d1);
+          }
+          w[t] = __dadd_rn(d0, d1);
+        }
+#pragma unroll
+        for (int off = 4; off; off >>= 1)
+#pragma unroll
+          for (int t = 0; t < CPG; ++t)
+            w[t] = __dadd_rn(w[t], __shfl_xor_sync(0xffffffffu, w[t], off, 8));
+#pragma unroll
+        for (int t = 0; t < CPG; ++t)
+#pragma unroll
+          for (int r = 0; r < RPL; ++r) {
+            const int i = gl + 8 * r;
+            if (act[t] && i >= j) x[t][r] = __dsub_rn(x[t][r], __dmul_rn(__dmul_rn(tau, vr[r]), w[t]));
+          }
+      }
+#pragma unroll
+      for (int t = 0; t < CPG; ++t) {
+        if (!isp[t]) continue;
+        // pivot column: rows < j keep R, row j = beta, below = 0 (qrcp.py:80-81)
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) {
+          const int i = gl + 8 * r;
+          if (i == j) x[t][r] = beta;
+          else if (i > j) x[t][r] = 0.0;
+        }
+        pc[t] = j;
+      }
+      if (j + 1 < a.nt) {
+        // NormTracker.downdate with row j of the updated sample (kernels.py:222-233)
+        double nn[CPG];
+        bool rec[CPG];
+#pragma unroll
+        for (int t = 0; t < CPG; ++t) {
+          const double rsel = pick_uniform<RPL>(x[t], j >> 3);
+          const double row = __shfl_sync(0xffffffffu, rsel, j & 7, 8);
+          double nsq = __dsub_rn(__dmul_rn(nv[t], nv[t]), __dmul_rn(row, row));
+          nsq = nsq > 0.0 ? nsq : 0.0;
+          rec[t] = act[t] && nsq < __dmul_rn(kGuard, og[t]);
+          nn[t] = sqrt(nsq);
+        }
+#pragma unroll
+        for (int t = 0; t < CPG; ++t) {
+          if (!rec[t]) continue;   // (uniform over the group: its lanes share the column)
+          double s0 = 0.0;
+#pragma unroll
+          for (int r = 0; r < RPL; ++r) {
+            const int i = gl + 8 * r;
+            if (i > j && i < ell) s0 = __fma_rn(x[t][r], x[t][r], s0);
+          }
+#pragma unroll
+          for (int off = 4; off; off >>= 1) s0 = __dadd_rn(s0, __shfl_xor_sync(gmask, s0, off, 8));
+          nn[t] = sqrt(s0);
+          og[t] = __dmul_rn(nn[t], nn[t]);
+        }
+#pragma unroll
+        for (int t = 0; t < CPG; ++t) {
+          if (!act[t]) continue;
+          nv[t] = nn[t];
+          const unsigned long long kt = make_key(nn[t], qq[t], pb);
+          key = kt > key ? kt : key;
+        }
+      }
+    } else {
 #pragma unroll
     for (int t = 0; t < CPG; ++t) {
       int q = pc[t];
@@ -966,6 +1059,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) select_reg_kernel(SelArgs a) {
         key = kt > key ? kt : key;
       }
     }
+    }   // CPG == 1
     key = group_key(key);
     if (lane == 0) s_wkey[par ^ 1][warp] = key;
     mark(1);
